@@ -1,0 +1,221 @@
+/*
+ * nirc_b200.h — C ABI of the B200 (sm_100a) Neural Incident Radiance Cache
+ * hot path.  Every entry point is `extern "C"`, takes plain pointers and
+ * sizes, returns an int status and is stream-ordered on the `cudaStream_t`
+ * passed last (as `void*`, so the header needs no CUDA include).  All data
+ * pointers are DEVICE pointers unless a parameter name ends in `_host`.
+ *
+ * The reference (`nirclab`, pure Python + numba) has no FFI; the boundary
+ * it replaces is its Python module API and the `jit_kernel` backend seam
+ * (pkg/src/nirclab/backend.py:27-49).  Each entry point below names the
+ * reference function it stands in for.  The Python shim in
+ * `paper_2412_04634_b200/` binds these with ctypes and keeps the
+ * reference's signatures; INTEGRATION.md shows the binding.
+ *
+ * Ownership: the caller (torch) owns every buffer.  The library keeps no
+ * global state except per-device cached weight images.
+ */
+#ifndef NIRC_B200_H
+#define NIRC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NIRC_MAX_LAYERS 9
+#define NIRC_MAX_LEVELS 16
+#define NIRC_MAX_BANDS 8
+
+/* Status codes.  The shim maps them onto the reference's exceptions
+ * (pkg/src/nirclab/errors.py:8-33): CONFIG -> ConfigError,
+ * DIVERGENCE -> DivergenceError, BAD_PDF -> InvalidSampleError. */
+enum {
+  NIRC_OK = 0,
+  NIRC_E_CONFIG = 2,
+  NIRC_E_DIVERGENCE = 3,
+  NIRC_E_BAD_PDF = 4,
+  NIRC_E_CUDA = 5,
+  NIRC_E_UNSUPPORTED = 6
+};
+
+/* Network layout; mirrors NetSpec (pkg/src/nirclab/mlp.py:26-62).
+ * theta = [hash tables (levels*2^table_log2*feats)] ++ per layer W (dout x din,
+ * row-major) ++ b.  sh_k[l*8+m] holds NORM[l,0] for m == 0 and
+ * sqrt(2)*NORM[l,m] for m > 0 (pkg/src/nirclab/sh.py:21-33), computed on
+ * the host with the reference's expression order. */
+typedef struct nirc_spec {
+  int32_t levels, table_log2, feats, bands, in_dim, n_layers, out_act, pad0;
+  int32_t dims[NIRC_MAX_LAYERS + 1];
+  int32_t pad1[2];
+  int64_t w_off[NIRC_MAX_LAYERS];
+  int64_t b_off[NIRC_MAX_LAYERS];
+  int32_t res[NIRC_MAX_LEVELS];
+  double bb_min[3];
+  double bb_inv[3];
+  int64_t grid_len, theta_len;
+  double sh_k[64];
+} nirc_spec_t;
+
+/* Flat scene, mirrors ScnPack (pkg/src/nirclab/scene.py:42-53).  All arrays
+ * are device pointers, f64 unless noted; vectors are (n,3) row-major. */
+typedef struct nirc_scene {
+  int32_t n_tri, n_sph, n_mat, n_light, n_bvh, env_kind, env_h, env_w;
+  const double *tri_v0, *tri_e1, *tri_e2, *tri_ng, *tri_area, *tri_lq;
+  const int32_t *tri_mat;
+  const double *sph_c, *sph_r, *sph_lq;
+  const int32_t *sph_mat;
+  const int32_t *mat_kind;
+  const double *mat_albedo, *mat_rough, *mat_emit;
+  const int32_t *lt_kind, *lt_prim;
+  const double *lt_cdf, *lt_q;
+  const double *env_img;             /* (env_h, env_w, 3) */
+  double env_c0[3], env_c1[3], env_c2[3];
+  double env_q, eps, diag;
+  double bbox_min[3], bbox_inv_ext[3];
+  const double *bvh_lo, *bvh_hi;
+  const int32_t *bvh_a, *bvh_b, *bvh_prim;
+} nirc_scene_t;
+
+/* Two-level estimator knobs; mirrors EstimatorConfig
+ * (pkg/src/nirclab/estimators.py:49-84) as consumed by render_kernel
+ * (pkg/src/nirclab/kernels.py:723-759). */
+typedef struct nirc_render_cfg {
+  int32_t mode;          /* 0 = pt, 1 = two-level */
+  int32_t spp;
+  int32_t cache_on;      /* 0: cache skipped (is_zero and not forced) */
+  int32_t max_cv;
+  int32_t nc[8];         /* nc[:max_cv], each 0..28 */
+  double rough_cut;
+  double rr_survive;     /* 1 - EstimatorConfig.rr */
+  uint64_t seed, frame;
+  int32_t width, height; /* camera resolution */
+  int32_t row0, row1;    /* pixel-row band [row0, row1) rendered by this call */
+} nirc_render_cfg_t;
+
+/* ---- library / introspection ------------------------------------------ */
+const char* nirc_version(void);
+int nirc_last_error(char* buf, int buflen);
+int nirc_device_sm_count(void);
+
+/* ---- encoding (pkg/src/nirclab/encoding.py) ----------------------------- */
+/* encode_batch (encoding.py:111-157): X (n,in_dim) f32, entries (n,levels,8)
+ * i64 slots, weights (n,levels,8) f32.  entries/weights may be NULL. */
+int nirc_encode(const nirc_spec_t* spec, const float* theta,
+                const double* pos, const double* normal, const double* albedo,
+                const double* rough, const double* dirs, int64_t n,
+                float* X, int64_t* entries, float* weights, void* stream);
+
+/* scatter_grid_grad (encoding.py:160-167): grad[slot*F+f] += w * dX[:, l*F+f]. */
+int nirc_scatter_grid_grad(const nirc_spec_t* spec, float* grad,
+                           const int64_t* entries, const float* weights,
+                           const float* dX, int64_t n, int64_t dx_stride,
+                           void* stream);
+
+/* ---- network (pkg/src/nirclab/mlp.py) ----------------------------------- */
+/* mlp_forward (mlp.py:102-122), fp32 SIMT twin.  zs (n, sum(dims[1:])) f32 is
+ * the training cache (pre-activations per layer), NULL for inference.
+ * finite_flag (i32, may be NULL) is set to 1 when theta holds a non-finite
+ * value (DivergenceError in the reference). */
+int nirc_mlp_forward(const nirc_spec_t* spec, const float* theta,
+                     const float* X, int64_t n, float* Y, float* zs,
+                     int32_t* nonfinite_flag, void* stream);
+
+/* mlp_backward (mlp.py:125-154) without the grid scatter: accumulates dW, db
+ * into grad (congruent to theta, caller-zeroed) and writes dX (n, in_dim). */
+int nirc_mlp_backward(const nirc_spec_t* spec, const float* theta,
+                      const float* X, const float* zs, const float* dY,
+                      int64_t n, float* grad, float* dX, float* scratch,
+                      void* stream);
+
+/* full_forward (mlp.py:216-224) = encode_batch + mlp_forward fused in one
+ * persistent sm_100a kernel: hash-grid + SH + aux encoding written straight
+ * into the SMEM A-tile, every layer a 3xTF32 tcgen05.mma with the fp32
+ * accumulator in TMEM.  precision: 0 = tcgen05 3xTF32, 1 = fp32 SIMT twin. */
+int nirc_full_forward(const nirc_spec_t* spec, const float* theta,
+                      const double* pos, const double* normal,
+                      const double* albedo, const double* rough,
+                      const double* dirs, int64_t n, float* Y,
+                      int32_t precision, void* stream);
+
+/* ---- losses (pkg/src/nirclab/losses.py) --------------------------------- */
+/* kind: 0 l2, 1 relative_l2, 2 variance, 3 bce.  Y (n,3) f32, target (n,3)
+ * f64, pdf (n,) f64 (unused for bce), running_mean (3,) f64 (variance).
+ * dY (n,3) f32 = the reference gradient cast to f32; loss_out (1,) f64 = the
+ * mean.  status_flags[0] |= 1 on pdf <= 0 (InvalidSampleError),
+ * |= 2 on a non-finite loss (DivergenceError). */
+int nirc_loss(int32_t kind, const float* Y, const double* target,
+              const double* pdf, const double* running_mean, double eps,
+              int64_t n, float* dY, double* loss_out, int32_t* status_flags,
+              double* scratch, void* stream);
+
+/* ---- optimizer (pkg/src/nirclab/adam.py:20-33) -------------------------- */
+/* Dense Adam over theta_len params.  t (i64) and skipped (i64) live on the
+ * device; a non-finite grad skips the step without touching t.  When
+ * gate_flags is non-NULL and *gate_flags != 0 the call is a no-op (a prior
+ * divergence). */
+int nirc_adam_step(float* theta, float* m, float* v, const float* grad,
+                   int64_t n, int64_t* t, int64_t* skipped, double lr,
+                   double beta1, double beta2, double eps,
+                   const int32_t* gate_flags, int32_t* scratch, void* stream);
+
+/* ---- online training (pkg/src/nirclab/caches.py:310-354) ---------------- */
+/* One optimizer step of train_frame on device-resident records (SoA f64):
+ * batch selection from the splitmix64 shuffle stream
+ * (uniform_array(seed, P_SHUFFLE, frame, n, offset=step*n) + stable argsort,
+ * caches.py:327-329), encode, forward, loss, backward + hash-grid scatter,
+ * dense Adam.  Records: pos, ns, alb (n,3), rough (n,), dirs (n,3),
+ * target (n,3), pdf (n,).  loss_out receives the step's loss (f64).
+ * status_flags as in nirc_loss; once a divergence flag is set, later steps are
+ * no-ops (state equals the reference at the raise). */
+typedef struct nirc_records {
+  const double *pos, *ns, *alb, *rough, *dirs, *target, *pdf;
+  int64_t n;
+} nirc_records_t;
+
+int nirc_train_step(const nirc_spec_t* spec, float* theta, float* m, float* v,
+                    int64_t* t, int64_t* skipped, const nirc_records_t* rec,
+                    uint64_t seed, int64_t frame, int32_t step,
+                    int32_t batch_cap, int32_t loss_kind, double loss_eps,
+                    double lr, double* running_mean, double* loss_out,
+                    int32_t* status_flags, int64_t* batch_idx_out,
+                    void* workspace, int64_t workspace_bytes, void* stream);
+int64_t nirc_train_workspace_bytes(const nirc_spec_t* spec, int64_t n_records,
+                                   int32_t batch_cap);
+
+/* ---- rendering (pkg/src/nirclab/kernels.py:451-759) --------------------- */
+/* render_kernel for MODE_PT / MODE_TL: per-pixel sums img, img2 (h,w,3) f64
+ * and term (h,w) f64 are ACCUMULATED (caller zeroes).  The two-level cache
+ * integral + residual is evaluated by the deferred NIRC inference pipeline
+ * (trace -> fused encode/tcgen05 MLP/combine -> accumulate).
+ * queries_out (i64, may be NULL) receives the executed-query count. */
+int nirc_render(const nirc_scene_t* scene, const double* cam,
+                const nirc_render_cfg_t* cfg, const nirc_spec_t* spec,
+                const float* theta, double* img, double* img2, double* term,
+                int64_t* queries_out, void* workspace, int64_t workspace_bytes,
+                void* stream);
+int64_t nirc_render_workspace_bytes(const nirc_render_cfg_t* cfg);
+
+/* ---- training records (pkg/src/nirclab/kernels.py:85-311,
+ *      caches.py:87-131) ------------------------------------------------- */
+/* collect_training_records, kind "nirc" (0) or "nirc_full" (1): traces
+ * `count` recording paths and writes the records in the reference's row
+ * order (path-major, vertex-minor).  out_* hold `cap` rows; n_out (i64,
+ * device) receives the record count. */
+typedef struct nirc_records_out {
+  double *pos, *ns, *alb, *rough, *dirs, *target, *pdf;
+  int64_t cap;
+} nirc_records_out_t;
+
+int nirc_collect(const nirc_scene_t* scene, const double* cam, uint64_t seed,
+                 uint64_t frame, int64_t count, int32_t kind,
+                 const nirc_records_out_t* out, int64_t* n_out,
+                 void* workspace, int64_t workspace_bytes, void* stream);
+int64_t nirc_collect_workspace_bytes(int64_t count);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NIRC_B200_H */

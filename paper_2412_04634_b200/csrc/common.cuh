@@ -1,0 +1,220 @@
+// Shared device building blocks for the NIRC hot path on sm_100a.
+//
+// Everything that must be BIT-EXACT against the reference lives here and is
+// written with explicit round-to-nearest intrinsics (__fmul_rn, __dadd_rn,
+// ...) so nvcc can never contract it into FMAs:
+//   * splitmix64 counter RNG          pkg/src/nirclab/rng.py:59-106
+//   * real SH, no Condon-Shortley     pkg/src/nirclab/sh.py:36-127
+//   * XOR-primes hash + trilinear     pkg/src/nirclab/encoding.py:38-157
+//   * cosine sampling / ONB           pkg/src/nirclab/core.py:39-74
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/nirc_b200.h"
+
+#define NIRC_HD __host__ __device__ __forceinline__
+#define NIRC_D __device__ __forceinline__
+
+namespace nirc {
+
+// ---------------------------------------------------------------- rng ----
+// rng.py:23-31 constants, :59-64 mix64, :67-73 stream_key, :76-89 draws.
+constexpr uint64_t GAMMA = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t M1 = 0xBF58476D1CE4E5B9ull;
+constexpr uint64_t M2 = 0x94D049BB133111EBull;
+constexpr uint64_t P_RENDER = 0x01, P_TRAIN = 0x02, P_INIT = 0x03,
+                   P_SHUFFLE = 0x04, P_BASELINE = 0x05, P_MEASURE = 0x06;
+// rng.py:45-56 per-vertex dimension layout
+constexpr int DIM_JITTER_X = 0, DIM_JITTER_Y = 1, VERTEX_DIM_BASE = 8,
+              DIMS_PER_VERTEX = 64, OFF_LIGHT_PICK = 0, OFF_LIGHT_U = 1,
+              OFF_LIGHT_V = 2, OFF_BSDF_U = 3, OFF_BSDF_V = 4, OFF_RR = 5,
+              OFF_TERM = 6, OFF_CACHE = 8;
+
+NIRC_HD uint64_t mix64(uint64_t x) {
+  x += GAMMA;
+  x = (x ^ (x >> 30)) * M1;
+  x = (x ^ (x >> 27)) * M2;
+  return x ^ (x >> 31);
+}
+NIRC_HD uint64_t stream_key(uint64_t seed, uint64_t purpose, uint64_t frame,
+                            uint64_t pixel, uint64_t sample) {
+  uint64_t k = mix64(seed ^ purpose);
+  k = mix64(k ^ frame);
+  k = mix64(k ^ pixel);
+  return mix64(k ^ sample);
+}
+NIRC_HD uint64_t rand_u64(uint64_t key, uint64_t dim) {
+  return mix64(key + GAMMA * dim);
+}
+// (u64 >> 11) * 2^-53: both steps are exact in f64.
+NIRC_HD double rand_uniform(uint64_t key, uint64_t dim) {
+  return (double)(rand_u64(key, dim) >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// ----------------------------------------------------- exact f64 helpers --
+NIRC_D double dmul(double a, double b) { return __dmul_rn(a, b); }
+NIRC_D double dadd(double a, double b) { return __dadd_rn(a, b); }
+NIRC_D double dsub(double a, double b) { return __dsub_rn(a, b); }
+NIRC_D double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+NIRC_D double dsqrt(double a) { return __dsqrt_rn(a); }
+
+// ------------------------------------------------------------------ SH ---
+// sh.py:36-76 (scalar, numba) and :89-127 (batch, numpy).  The two differ in
+// one association: the batch path advances P_m^m as (pmm*(2m-1))*s, the
+// scalar path as pmm*((2m-1)*s).  `BatchOrder` selects which one to follow.
+// The Legendre recurrences and the K*P*cos products are otherwise identical.
+template <bool BatchOrder, typename Store>
+NIRC_D void sh_eval(double x, double y, double z, int bands,
+                    const double* __restrict__ sh_k, Store store) {
+  const double s = dsqrt(dadd(dmul(x, x), dmul(y, y)));
+  double cphi = 1.0, sphi = 0.0;
+  if (s > 0.0) {
+    cphi = ddiv(x, s);
+    sphi = ddiv(y, s);
+  }
+  double cm = 1.0, sm = 0.0, pmm = 1.0;
+  for (int m = 0; m < bands; ++m) {
+    if (m > 0) {
+      const double f = (double)(2 * m - 1);
+      pmm = BatchOrder ? dmul(dmul(pmm, f), s) : dmul(pmm, dmul(f, s));
+      const double cn = dsub(dmul(cm, cphi), dmul(sm, sphi));
+      const double sn = dadd(dmul(sm, cphi), dmul(cm, sphi));
+      cm = cn;
+      sm = sn;
+    }
+    double p_lm2 = 0.0, p_lm1 = 0.0;
+    for (int l = m; l < bands; ++l) {
+      double p;
+      if (l == m) {
+        p = pmm;
+      } else if (l == m + 1) {
+        p = dmul(dmul(z, (double)(2 * m + 1)), pmm);
+      } else {
+        const double a = dmul(dmul((double)(2 * l - 1), z), p_lm1);
+        const double b = dmul((double)(l + m - 1), p_lm2);
+        p = ddiv(dsub(a, b), (double)(l - m));
+      }
+      p_lm2 = p_lm1;
+      p_lm1 = p;
+      const int base = l * l + l;
+      if (m == 0) {
+        store(base, dmul(sh_k[l * 8], p));
+      } else {
+        const double k = dmul(sh_k[l * 8 + m], p);
+        store(base + m, dmul(k, cm));
+        store(base - m, dmul(k, sm));
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------- hash grid ---
+// encoding.py:38-42: (x*1 ^ y*P1 ^ z*P2) & (T-1).  The mask is < 2^32 so
+// the low 32 bits of the u64 products decide the slot; u32 math is exact.
+constexpr uint32_t P1 = 2654435761u;
+constexpr uint32_t P2 = 805459861u;
+
+NIRC_HD uint32_t hash3(uint32_t x, uint32_t y, uint32_t z, uint32_t mask) {
+  return (x ^ (y * P1) ^ (z * P2)) & mask;
+}
+
+// Position normalisation, encoding.py:49-66 / :126-127: f64 affine into the
+// padded scene box, clamp to [0,1], then round to f32.
+NIRC_D float norm_coord(double p, double lo, double inv) {
+  double u = dmul(dsub(p, lo), inv);
+  u = u < 0.0 ? 0.0 : (u > 1.0 ? 1.0 : u);
+  return __double2float_rn(u);
+}
+
+struct LevelCell {
+  int32_t ix, iy, iz;
+  float wx, wy, wz;
+};
+
+// encoding.py:129-131: s = u * f32(res) (f32 RN), i = floor, w = s - i.
+NIRC_D LevelCell level_cell(float ux, float uy, float uz, int res) {
+  const float r = (float)res;
+  const float sx = __fmul_rn(ux, r), sy = __fmul_rn(uy, r), sz = __fmul_rn(uz, r);
+  LevelCell c;
+  c.ix = (int32_t)floorf(sx);
+  c.iy = (int32_t)floorf(sy);
+  c.iz = (int32_t)floorf(sz);
+  c.wx = __fsub_rn(sx, (float)c.ix);
+  c.wy = __fsub_rn(sy, (float)c.iy);
+  c.wz = __fsub_rn(sz, (float)c.iz);
+  return c;
+}
+
+// Corner c: x = bit0, y = bit1, z = bit2; w = ((wx|1-wx)*(wy|1-wy))*(wz|1-wz)
+// in f32 (encoding.py:81-85, :140-143).
+NIRC_D float corner_weight(const LevelCell& c, int corner) {
+  const float ax = (corner & 1) ? c.wx : __fsub_rn(1.0f, c.wx);
+  const float ay = (corner & 2) ? c.wy : __fsub_rn(1.0f, c.wy);
+  const float az = (corner & 4) ? c.wz : __fsub_rn(1.0f, c.wz);
+  return __fmul_rn(__fmul_rn(ax, ay), az);
+}
+NIRC_D uint32_t corner_hash(const LevelCell& c, int corner, uint32_t mask) {
+  return hash3((uint32_t)(c.ix + (corner & 1)), (uint32_t)(c.iy + ((corner >> 1) & 1)),
+               (uint32_t)(c.iz + ((corner >> 2) & 1)), mask);
+}
+
+// Hash-grid features of one level for feats == 2 (the NIRC default):
+// x[f] = sum_{c=0..7} (w_c * theta[slot_c*2+f]) accumulated in corner order
+// from 0.0f, f32 RN (encoding.py:144-151).  The 8 gathers are issued before
+// the dependent accumulation so they overlap in the memory system.
+NIRC_D float2 level_features2(const float* __restrict__ table, const LevelCell& c,
+                              uint32_t mask) {
+  float2 g[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    g[k] = __ldg(reinterpret_cast<const float2*>(table) + corner_hash(c, k, mask));
+  float x0 = 0.0f, x1 = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float w = corner_weight(c, k);
+    x0 = __fadd_rn(x0, __fmul_rn(w, g[k].x));
+    x1 = __fadd_rn(x1, __fmul_rn(w, g[k].y));
+  }
+  return make_float2(x0, x1);
+}
+
+// ------------------------------------------------------ sampling frames --
+// core.py:39-54 onb_s (Duff et al.), :57-65 cosine_dir_s.  Used by the render
+// and collection kernels (compiled with -fmad=false).
+struct Onb {
+  double tx, ty, tz, bx, by, bz;
+};
+__device__ inline Onb onb(double nx, double ny, double nz) {
+  const double s = nz >= 0.0 ? 1.0 : -1.0;
+  const double a = -1.0 / (s + nz);
+  const double b = nx * ny * a;
+  Onb o;
+  o.tx = 1.0 + s * nx * nx * a;
+  o.ty = s * b;
+  o.tz = -s * nx;
+  o.bx = b;
+  o.by = s + ny * ny * a;
+  o.bz = -ny;
+  return o;
+}
+
+}  // namespace nirc
+
+// ------------------------------------------------------------- errors ----
+namespace nirc {
+void set_last_error(const char* fmt, ...);
+int check_cuda(cudaError_t e, const char* what);
+}  // namespace nirc
+
+#define NIRC_CUDA_TRY(expr)                                        \
+  do {                                                             \
+    cudaError_t _e = (expr);                                       \
+    if (_e != cudaSuccess) return nirc::check_cuda(_e, #expr);     \
+  } while (0)
+
+#define NIRC_LAUNCH_CHECK(what)                                    \
+  do {                                                             \
+    cudaError_t _e = cudaGetLastError();                           \
+    if (_e != cudaSuccess) return nirc::check_cuda(_e, what);      \
+  } while (0)

@@ -1,0 +1,241 @@
+// full_forward (pkg/src/nirclab/mlp.py:216-224 = encode_batch + mlp_forward)
+// as ONE persistent sm_100a kernel: every thread encodes its query row
+// (12-level hash grid, 8-corner gathers from the L2-resident tables, f64
+// SH, aux) straight into the SMEM A tile, then the group runs the network
+// on tcgen05 (tc_mlp.cuh).  No X, entries or weights ever touch HBM.
+#include <mutex>
+#include "common.cuh"
+#include "tc_mlp.cuh"
+
+namespace nirc {
+
+// The default NIRC input layout (test_default_layout_dimensions,
+// tests/test_neural.py:81-88): 12 levels x 2 feats, 4 SH bands, 7 aux.
+constexpr int kL = 12, kF = 2, kBands = 4, kIn = 47, kK0 = 48;
+
+__host__ __device__ inline bool is_default_layout(const nirc_spec_t& sp) {
+  return sp.levels == kL && sp.feats == kF && sp.bands == kBands && sp.in_dim == kIn &&
+         sp.dims[0] == kIn;
+}
+
+// Encodes one query row into x[48] (x[47] = 0 pad), bit-identical to
+// encode_batch (encoding.py:111-157).
+__device__ __forceinline__ void encode_default(const nirc_spec_t& sp,
+                                               const float* __restrict__ theta, const double* p,
+                                               const double* nrm, const double* alb,
+                                               double rough, const double* d, float* x) {
+  const float ux = norm_coord(p[0], sp.bb_min[0], sp.bb_inv[0]);
+  const float uy = norm_coord(p[1], sp.bb_min[1], sp.bb_inv[1]);
+  const float uz = norm_coord(p[2], sp.bb_min[2], sp.bb_inv[2]);
+  const uint32_t T = 1u << sp.table_log2;
+#pragma unroll
+  for (int lvl = 0; lvl < kL; ++lvl) {
+    const LevelCell c = level_cell(ux, uy, uz, sp.res[lvl]);
+    const float2 f = level_features2(theta + (size_t)lvl * T * kF, c, T - 1u);
+    x[2 * lvl] = f.x;
+    x[2 * lvl + 1] = f.y;
+  }
+  sh_eval<true>(d[0], d[1], d[2], kBands, sp.sh_k,
+                [&](int i, double v) { x[24 + i] = __double2float_rn(v); });
+  x[40] = __double2float_rn(dmul(dadd(nrm[0], 1.0), 0.5));
+  x[41] = __double2float_rn(dmul(dadd(nrm[1], 1.0), 0.5));
+  x[42] = __double2float_rn(dmul(dadd(nrm[2], 1.0), 0.5));
+  x[43] = __double2float_rn(alb[0]);
+  x[44] = __double2float_rn(alb[1]);
+  x[45] = __double2float_rn(alb[2]);
+  x[46] = __double2float_rn(rough);
+  x[47] = 0.0f;
+}
+
+template <int NG>
+__global__ void __launch_bounds__(NG * 128, 1)
+    k_full_forward_tc(nirc_spec_t sp, tc::TcNet net, tc::TcSmem L,
+                      const float* __restrict__ theta, const uint8_t* __restrict__ wimg,
+                      const float* __restrict__ bias_g, const double* __restrict__ pos,
+                      const double* __restrict__ nrm, const double* __restrict__ alb,
+                      const double* __restrict__ rough, const double* __restrict__ dirs,
+                      int64_t n, float* __restrict__ Y) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint32_t tmem_base;
+  tc::tc_prologue(smem, L, net, NG, wimg, bias_g, tmem_base);
+  const uint32_t s0 = tc::smem_u32(smem);
+  const int group = threadIdx.x >> 7;
+  const int tg = threadIdx.x & 127;
+  const uint32_t a_hi = s0 + L.a_off + group * tc::kABufBytes;
+  const uint32_t a_lo = a_hi + tc::kAImageBytes;
+  const uint32_t mbar = s0 + L.bar_off + 8 * (1 + group);
+  const uint32_t tmem_d = tmem_base + group * 64;
+  const float* s_bias = reinterpret_cast<const float*>(smem + L.bias_off);
+  const int dout = sp.dims[sp.n_layers];
+  uint32_t phase = 0;
+  const int64_t ntiles = (n + tc::kTileRows - 1) / tc::kTileRows;
+  for (int64_t tile = (int64_t)blockIdx.x * NG + group; tile < ntiles;
+       tile += (int64_t)gridDim.x * NG) {
+    const int64_t row = tile * tc::kTileRows + tg;
+    float x[kK0];
+    if (row < n) {
+      encode_default(sp, theta, pos + 3 * row, nrm + 3 * row, alb + 3 * row, rough[row],
+                     dirs + 3 * row, x);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kK0; ++k) x[k] = 0.0f;
+    }
+    tc::write_a_row<kK0>(a_hi, a_lo, tg, x);
+    float y[4];
+    tc::run_chain(net, s0 + L.w_off, s_bias, group, tg, a_hi, a_lo, tmem_d, mbar, phase, y);
+    if (row < n)
+      for (int j = 0; j < dout; ++j) Y[row * dout + j] = y[j];
+  }
+  tc::tc_epilogue(tmem_base, NG);
+}
+
+// fp32 SIMT twin of the same fusion (precision == 1): weights in smem,
+// one thread per row, the reference's accuracy class.
+__global__ void k_full_forward_simt(nirc_spec_t sp, const float* __restrict__ theta,
+                                    const double* __restrict__ pos, const double* __restrict__ nrm,
+                                    const double* __restrict__ alb,
+                                    const double* __restrict__ rough,
+                                    const double* __restrict__ dirs, int64_t n,
+                                    float* __restrict__ Y) {
+  extern __shared__ float smem_f[];
+  const int np = (int)(sp.theta_len - sp.grid_len);
+  float* W = smem_f;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) W[i] = __ldg(theta + sp.grid_len + i);
+  __syncthreads();
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  float a[64], b[64];
+  encode_default(sp, theta, pos + 3 * row, nrm + 3 * row, alb + 3 * row, rough[row],
+                 dirs + 3 * row, a);
+  for (int l = 0; l < sp.n_layers; ++l) {
+    const int din = sp.dims[l], dout = sp.dims[l + 1];
+    const float* w = W + (sp.w_off[l] - sp.grid_len);
+    const float* bias = W + (sp.b_off[l] - sp.grid_len);
+    const bool last = l == sp.n_layers - 1;
+#pragma unroll 4
+    for (int j = 0; j < dout; ++j) {
+      float acc = 0.0f;
+#pragma unroll 8
+      for (int i = 0; i < din; ++i) acc = fmaf(a[i], w[j * din + i], acc);
+      const float z = acc + bias[j];
+      b[j] = (!last || sp.out_act == 0) ? (z > 0.0f ? z : 0.0f) : 1.0f / (1.0f + expf(-z));
+    }
+    for (int j = 0; j < dout; ++j) a[j] = b[j];
+  }
+  const int dout = sp.dims[sp.n_layers];
+  for (int j = 0; j < dout; ++j) Y[row * dout + j] = a[j];
+}
+
+// Per-device cache of packed weight images (the library's only state).
+struct WeightCache {
+  uint8_t* img = nullptr;
+  float* bias = nullptr;
+};
+static WeightCache g_wcache[16];
+static std::mutex g_wmutex;
+
+int get_weight_cache(uint8_t** img, float** bias) {
+  int dev = 0;
+  NIRC_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 16) return NIRC_E_CUDA;
+  std::lock_guard<std::mutex> lk(g_wmutex);
+  WeightCache& c = g_wcache[dev];
+  if (!c.img) {
+    NIRC_CUDA_TRY(cudaMalloc(&c.img, 160 * 1024));
+    NIRC_CUDA_TRY(cudaMalloc(&c.bias, tc::kMaxTcLayers * 64 * 4));
+  }
+  *img = c.img;
+  *bias = c.bias;
+  return NIRC_OK;
+}
+
+int pack_weights(const nirc_spec_t& sp, const tc::TcNet& net, const float* theta,
+                 cudaStream_t s, uint8_t** img, float** bias) {
+  int st = get_weight_cache(img, bias);
+  if (st) return st;
+  int total = 0;
+  for (int l = 0; l < net.nl; ++l) total += net.N[l] * net.K[l];
+  total = total > net.nl * 64 ? total : net.nl * 64;
+  tc::k_pack_weights<<<(total + 255) / 256, 256, 0, s>>>(sp, net, theta, *img, *bias);
+  NIRC_LAUNCH_CHECK("k_pack_weights");
+  return NIRC_OK;
+}
+
+int sm_count() {
+  static int cached[16] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return 148;
+  if (!cached[dev]) {
+    int c = 0;
+    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = c > 0 ? c : 148;
+  }
+  return cached[dev];
+}
+
+// Chooses the number of 128-row groups per CTA that fit in shared memory.
+int tc_groups_for(const tc::TcNet& net, uint32_t extra_per_cta) {
+  for (int g = 2; g >= 1; --g)
+    if (tc::tc_smem_layout(net, g, extra_per_cta).total <= 227u * 1024u) return g;
+  return 0;
+}
+
+}  // namespace nirc
+
+using namespace nirc;
+
+extern "C" int nirc_device_sm_count(void) { return sm_count(); }
+
+extern "C" int nirc_full_forward(const nirc_spec_t* spec, const float* theta, const double* pos,
+                                 const double* normal, const double* albedo, const double* rough,
+                                 const double* dirs, int64_t n, float* Y, int32_t precision,
+                                 void* stream) {
+  if (!spec) return NIRC_E_CONFIG;
+  if (n <= 0) return NIRC_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!is_default_layout(*spec)) {
+    set_last_error("fused forward needs the default 12x2 hash + 4-band SH layout");
+    return NIRC_E_UNSUPPORTED;
+  }
+  if (precision == 1) {
+    const size_t sm = (size_t)(spec->theta_len - spec->grid_len) * 4;
+    if (sm > 200 * 1024 || spec->dims[1] > 64) return NIRC_E_UNSUPPORTED;
+    NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)k_full_forward_simt,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_full_forward_simt<<<(int)((n + 127) / 128), 128, sm, s>>>(*spec, theta, pos, normal, albedo,
+                                                               rough, dirs, n, Y);
+    NIRC_LAUNCH_CHECK("k_full_forward_simt");
+    return NIRC_OK;
+  }
+  tc::TcNet net;
+  if (!tc::tc_net_for(*spec, &net)) {
+    set_last_error("network shape not supported by the tcgen05 path");
+    return NIRC_E_UNSUPPORTED;
+  }
+  const int ng = tc_groups_for(net, 0);
+  if (ng == 0) {
+    set_last_error("network too large for the tcgen05 shared-memory plan");
+    return NIRC_E_UNSUPPORTED;
+  }
+  uint8_t* img;
+  float* bias;
+  int st = pack_weights(*spec, net, theta, s, &img, &bias);
+  if (st) return st;
+  const tc::TcSmem L = tc::tc_smem_layout(net, ng, 0);
+  const int64_t ntiles = (n + tc::kTileRows - 1) / tc::kTileRows;
+  const int64_t want = (ntiles + ng - 1) / ng;
+  const int grid = (int)(want < sm_count() ? want : sm_count());
+  if (ng == 2) {
+    NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)k_full_forward_tc<2>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+    k_full_forward_tc<2><<<grid, 256, L.total, s>>>(*spec, net, L, theta, img, bias, pos, normal,
+                                                    albedo, rough, dirs, n, Y);
+  } else {
+    NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)k_full_forward_tc<1>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+    k_full_forward_tc<1><<<grid, 128, L.total, s>>>(*spec, net, L, theta, img, bias, pos, normal,
+                                                    albedo, rough, dirs, n, Y);
+  }
+  NIRC_LAUNCH_CHECK("k_full_forward_tc");
+  return NIRC_OK;
+}

@@ -1,0 +1,888 @@
+// NIRC neural substrate on sm_100a: encoding, fp32 SIMT network twin,
+// losses, backward + hash-grid scatter, dense Adam, and the fused online
+// training step.  Reference: pkg/src/nirclab/{encoding,mlp,losses,adam,
+// caches}.py (file:line cited per function).
+#include <cstdio>
+#include <cstring>
+#include <cmath>
+#include <climits>
+#include "common.cuh"
+
+namespace nirc {
+
+constexpr int kRowsPerBlock = 128;
+
+// ----------------------------------------------------------------------
+// Encoding of one row into a caller-provided store functor.
+// encode_batch (encoding.py:111-157): hash block [0, L*F), SH block
+// [L*F, L*F+bands^2), aux block (n+1)/2, albedo, rough.
+// ----------------------------------------------------------------------
+template <typename StoreX>
+__device__ void encode_row(const nirc_spec_t& sp, const float* __restrict__ theta,
+                           const double* p, const double* nrm, const double* alb,
+                           double rough, const double* d, StoreX store,
+                           int64_t* __restrict__ ent, float* __restrict__ wts) {
+  const float ux = norm_coord(p[0], sp.bb_min[0], sp.bb_inv[0]);
+  const float uy = norm_coord(p[1], sp.bb_min[1], sp.bb_inv[1]);
+  const float uz = norm_coord(p[2], sp.bb_min[2], sp.bb_inv[2]);
+  const uint32_t T = 1u << sp.table_log2;
+  const uint32_t mask = T - 1u;
+  const int F = sp.feats;
+  for (int lvl = 0; lvl < sp.levels; ++lvl) {
+    const LevelCell c = level_cell(ux, uy, uz, sp.res[lvl]);
+    const float* table = theta + (int64_t)lvl * T * F;
+    if (F == 2 && ent == nullptr) {
+      const float2 x = level_features2(table, c, mask);
+      store(lvl * 2, x.x);
+      store(lvl * 2 + 1, x.y);
+    } else {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int k = 0; k < 8; ++k) {
+        const float w = corner_weight(c, k);
+        const uint32_t h = corner_hash(c, k, mask);
+        if (ent) {
+          ent[lvl * 8 + k] = (int64_t)lvl * T + h;
+          wts[lvl * 8 + k] = w;
+        }
+        for (int f = 0; f < F && f < 4; ++f)
+          acc[f] = __fadd_rn(acc[f], __fmul_rn(w, __ldg(table + (int64_t)h * F + f)));
+      }
+      for (int f = 0; f < F && f < 4; ++f) store(lvl * F + f, acc[f]);
+    }
+  }
+  const int g = sp.levels * F;
+  sh_eval<true>(d[0], d[1], d[2], sp.bands, sp.sh_k,
+                [&](int i, double v) { store(g + i, __double2float_rn(v)); });
+  const int a0 = g + sp.bands * sp.bands;
+  store(a0 + 0, __double2float_rn(dmul(dadd(nrm[0], 1.0), 0.5)));
+  store(a0 + 1, __double2float_rn(dmul(dadd(nrm[1], 1.0), 0.5)));
+  store(a0 + 2, __double2float_rn(dmul(dadd(nrm[2], 1.0), 0.5)));
+  store(a0 + 3, __double2float_rn(alb[0]));
+  store(a0 + 4, __double2float_rn(alb[1]));
+  store(a0 + 5, __double2float_rn(alb[2]));
+  store(a0 + 6, __double2float_rn(rough));
+}
+
+__global__ void k_encode(nirc_spec_t sp, const float* __restrict__ theta,
+                         const double* __restrict__ pos, const double* __restrict__ nrm,
+                         const double* __restrict__ alb, const double* __restrict__ rough,
+                         const double* __restrict__ dirs, int64_t n, float* __restrict__ X,
+                         int64_t* __restrict__ entries, float* __restrict__ weights) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float* xr = X + i * sp.in_dim;
+  encode_row(sp, theta, pos + 3 * i, nrm + 3 * i, alb + 3 * i, rough[i], dirs + 3 * i,
+             [&](int k, float v) { xr[k] = v; },
+             entries ? entries + i * sp.levels * 8 : nullptr,
+             weights ? weights + i * sp.levels * 8 : nullptr);
+}
+
+// scatter_grid_grad (encoding.py:160-167).  np.add.at accumulates
+// (w * dG) in row order; the device sums the same f32 products with
+// atomics (order-free, tolerance stated in DESIGN.md).
+__global__ void k_scatter(nirc_spec_t sp, float* __restrict__ grad,
+                          const int64_t* __restrict__ entries, const float* __restrict__ weights,
+                          const float* __restrict__ dX, int64_t n, int64_t stride) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = n * sp.levels * 8;
+  if (t >= total) return;
+  const int64_t row = t / (sp.levels * 8);
+  const int lvl = (int)((t / 8) % sp.levels);
+  const int64_t slot = entries[t];
+  const float w = weights[t];
+  for (int f = 0; f < sp.feats; ++f)
+    atomicAdd(grad + slot * sp.feats + f, __fmul_rn(w, dX[row * stride + lvl * sp.feats + f]));
+}
+
+// ----------------------------------------------------------------------
+// fp32 SIMT network twin: one thread per row, weights in shared memory,
+// activations in a padded per-thread shared slab (stride dmax+1 words ->
+// conflict-free).  mlp_forward (mlp.py:102-122) / mlp_forward_s
+// (mlp.py:160-192): z = a W^T + b, ReLU hidden, ReLU or sigmoid output.
+// ----------------------------------------------------------------------
+__host__ __device__ inline int net_param_count(const nirc_spec_t& sp) {
+  return (int)(sp.theta_len - sp.grid_len);
+}
+__host__ __device__ inline int net_dmax(const nirc_spec_t& sp) {
+  int m = 0;
+  for (int l = 0; l <= sp.n_layers; ++l) m = sp.dims[l] > m ? sp.dims[l] : m;
+  return m;
+}
+__host__ __device__ inline int zs_width(const nirc_spec_t& sp) {
+  int s = 0;
+  for (int l = 1; l <= sp.n_layers; ++l) s += sp.dims[l];
+  return s;
+}
+inline size_t simt_smem_bytes(const nirc_spec_t& sp) {
+  return (size_t)net_param_count(sp) * 4 + (size_t)2 * kRowsPerBlock * (net_dmax(sp) + 1) * 4;
+}
+
+// Runs the network on the activation slab `a` (dmax+1 stride per thread)
+// and returns the output in a (first dims[nl] entries).  W is the smem copy
+// of theta[grid_len:].  zs (optional) receives every pre-activation.
+__device__ inline void simt_forward_row(const nirc_spec_t& sp, const float* __restrict__ W,
+                                        float* a, float* b, int stride, float* zs_row) {
+  int zoff = 0;
+  for (int l = 0; l < sp.n_layers; ++l) {
+    const int din = sp.dims[l], dout = sp.dims[l + 1];
+    const float* w = W + (sp.w_off[l] - sp.grid_len);
+    const float* bias = W + (sp.b_off[l] - sp.grid_len);
+    const bool last = (l == sp.n_layers - 1);
+    for (int j = 0; j < dout; ++j) {
+      const float* wr = w + j * din;
+      float acc = 0.0f;
+      for (int i = 0; i < din; ++i) acc = fmaf(a[i * stride], wr[i], acc);
+      const float z = acc + bias[j];
+      if (zs_row) zs_row[zoff + j] = z;
+      float y;
+      if (!last || sp.out_act == 0) y = z > 0.0f ? z : 0.0f;
+      else y = 1.0f / (1.0f + expf(-z));
+      b[j * stride] = y;
+    }
+    zoff += dout;
+    float* t = a; a = b; b = t;
+  }
+  // the output sits in the caller's `b` slab for odd depth, `a` for even
+}
+
+__device__ inline void stage_params(const nirc_spec_t& sp, const float* __restrict__ theta,
+                                    float* W) {
+  const int np = net_param_count(sp);
+  const float* src = theta + sp.grid_len;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) W[i] = __ldg(src + i);
+}
+
+__global__ void k_mlp_forward(nirc_spec_t sp, const float* __restrict__ theta,
+                              const float* __restrict__ X, int64_t n, float* __restrict__ Y,
+                              float* __restrict__ zs, int32_t* __restrict__ nonfinite) {
+  extern __shared__ float smem[];
+  float* W = smem;
+  stage_params(sp, theta, W);
+  if (nonfinite) {  // mlp.py:104-105 raises DivergenceError on any non-finite theta
+    int bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sp.theta_len;
+         i += (int64_t)gridDim.x * blockDim.x)
+      bad |= !isfinite(theta[i]);
+    if (bad) atomicExch(nonfinite, 1);
+  }
+  const int dmax = net_dmax(sp);
+  // thread t owns column t of two [dmax+1][128] slabs: a[i*128 + t]
+  float* a = W + net_param_count(sp) + threadIdx.x;
+  float* b = a + (dmax + 1) * kRowsPerBlock;
+  __syncthreads();
+  const int64_t row = (int64_t)blockIdx.x * kRowsPerBlock + threadIdx.x;
+  if (row >= n) return;
+  for (int i = 0; i < sp.in_dim; ++i) a[i * kRowsPerBlock] = X[row * sp.in_dim + i];
+  simt_forward_row(sp, W, a, b, kRowsPerBlock, zs ? zs + row * zs_width(sp) : nullptr);
+  const float* out = (sp.n_layers % 2 == 1) ? b : a;
+  const int dout = sp.dims[sp.n_layers];
+  for (int j = 0; j < dout; ++j) Y[row * dout + j] = out[j * kRowsPerBlock];
+}
+
+// ----------------------------------------------------------------------
+// Losses (losses.py:23-70).  Computed in f64 from the f32 prediction,
+// exactly the reference's promotions: the relative-L2 denominator is
+// f32(f32(y*y) + f32(eps)) (numpy NEP-50 weak scalar), everything else f64.
+// Gradient = reference gradient cast to f32 (caches.py:349).
+// ----------------------------------------------------------------------
+constexpr int kLossThreads = 256;
+
+__device__ inline double loss_elem(int kind, float yf, double t, double p, double rm,
+                                   double eps, double n_total, float* dy) {
+  const double y = (double)yf;
+  switch (kind) {
+    case 0: {  // loss_l2 :23-30
+      const double diff = dsub(y, t);
+      *dy = __double2float_rn(ddiv(ddiv(dmul(2.0, diff), p), n_total));
+      return ddiv(dmul(diff, diff), p);
+    }
+    case 1: {  // loss_relative_l2 :33-42
+      const float den32 = __fadd_rn(__fmul_rn(yf, yf), (float)eps);
+      const double den = dmul(p, (double)den32);
+      const double diff = dsub(y, t);
+      *dy = __double2float_rn(ddiv(ddiv(dmul(2.0, diff), den), n_total));
+      return ddiv(dmul(diff, diff), den);
+    }
+    case 2: {  // loss_variance :50-61
+      const double dev = dsub(ddiv(dsub(t, y), p), rm);
+      *dy = __double2float_rn(ddiv(ddiv(dmul(-2.0, dev), p), n_total));
+      return dmul(dev, dev);
+    }
+    default: {  // loss_bce :64-70
+      double q = y < 1e-6 ? 1e-6 : (y > 1.0 - 1e-6 ? 1.0 - 1e-6 : y);
+      const double v = -(dadd(dmul(t, log(q)), dmul(dsub(1.0, t), log(dsub(1.0, q)))));
+      *dy = __double2float_rn(ddiv(ddiv(dsub(q, t), dmul(q, dsub(1.0, q))), n_total));
+      return v;
+    }
+  }
+}
+
+// Pass 1: per-block partial sums of the loss (and, for the variance loss,
+// of (t - y)/pdf per channel when `dev_partial` is set).
+__global__ void k_loss(int kind, const float* __restrict__ Y, const double* __restrict__ T,
+                       const double* __restrict__ pdf, const double* __restrict__ rmean,
+                       double eps, int64_t n, float* __restrict__ dY,
+                       double* __restrict__ partial, int32_t* __restrict__ flags,
+                       const int64_t* __restrict__ idx, int dev_pass) {
+  __shared__ double red[kLossThreads][3];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double acc[3] = {0.0, 0.0, 0.0};
+  if (flags && (flags[0] & 2)) return;  // an earlier step diverged
+  if (i < n) {
+    const int64_t r = idx ? idx[i] : i;
+    const double p = kind == 3 ? 1.0 : pdf[r];
+    if (kind != 3 && !(p > 0.0)) atomicOr(flags, 1);
+    for (int c = 0; c < 3; ++c) {
+      if (dev_pass) {
+        acc[c] = ddiv(dsub(T[r * 3 + c], (double)Y[i * 3 + c]), p);
+      } else {
+        float g;
+        acc[c] = loss_elem(kind, Y[i * 3 + c], T[r * 3 + c], p, rmean ? rmean[c] : 0.0, eps,
+                           (double)(n * 3), &g);
+        dY[i * 3 + c] = g;
+      }
+    }
+  }
+  for (int c = 0; c < 3; ++c) red[threadIdx.x][c] = acc[c];
+  __syncthreads();
+  for (int s = kLossThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+      for (int c = 0; c < 3; ++c) red[threadIdx.x][c] += red[threadIdx.x + s][c];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int c = 0; c < 3; ++c) partial[blockIdx.x * 3 + c] = red[0][c];
+}
+
+// Pass 2 (one block): fold the partials in block order (deterministic).
+// mode 0: loss mean -> out[0], non-finite -> flags |= 2.
+// mode 1: variance EMA  rm = 0.95 rm + 0.05 mean((t-y)/pdf) (caches.py:340-343).
+__global__ void k_loss_final(const double* __restrict__ partial, int nblk, int64_t n,
+                             double* __restrict__ out, int32_t* __restrict__ flags,
+                             double* __restrict__ rmean, int mode) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (flags && (flags[0] & 2)) return;
+  double s[3] = {0.0, 0.0, 0.0};
+  for (int b = 0; b < nblk; ++b)
+    for (int c = 0; c < 3; ++c) s[c] += partial[b * 3 + c];
+  if (mode == 0) {
+    const double v = (s[0] + s[1] + s[2]) / (double)(n * 3);
+    out[0] = v;
+    if (!isfinite(v)) atomicOr(flags, 2);
+  } else {
+    for (int c = 0; c < 3; ++c)
+      rmean[c] = dadd(dmul(0.95, rmean[c]), dmul(dsub(1.0, 0.95), s[c] / (double)n));
+  }
+}
+
+// ----------------------------------------------------------------------
+// Backward (mlp.py:125-154).  ReLU' uses (z >= 0) for hidden AND output
+// layers (:134-138, :149).  Row pass: dz per layer (stored for the weight
+// gradient), dX = dz0 W0.  Weight pass: dW = dz^T a_prev, db = sum dz.
+// ----------------------------------------------------------------------
+__device__ inline float act_of(const nirc_spec_t& sp, int layer, float z) {
+  // activation applied to the pre-activation of `layer`
+  if (layer < sp.n_layers - 1 || sp.out_act == 0) return z > 0.0f ? z : 0.0f;
+  return 1.0f / (1.0f + expf(-z));
+}
+
+__global__ void k_backward_rows(nirc_spec_t sp, const float* __restrict__ theta,
+                                const float* __restrict__ zs, const float* __restrict__ dY,
+                                int64_t n, float* __restrict__ dzs, float* __restrict__ dX,
+                                const int32_t* __restrict__ flags) {
+  extern __shared__ float smem[];
+  if (flags && (flags[0] & 3)) return;
+  float* W = smem;
+  stage_params(sp, theta, W);
+  const int dmax = net_dmax(sp);
+  float* cur = W + net_param_count(sp) + threadIdx.x;
+  float* nxt = cur + (dmax + 1) * kRowsPerBlock;
+  __syncthreads();
+  const int64_t row = (int64_t)blockIdx.x * kRowsPerBlock + threadIdx.x;
+  if (row >= n) return;
+  const int zw = zs_width(sp);
+  int zoff[NIRC_MAX_LAYERS + 1];
+  zoff[0] = 0;
+  for (int l = 0; l < sp.n_layers; ++l) zoff[l + 1] = zoff[l] + sp.dims[l + 1];
+  const float* zr = zs + row * zw;
+  float* dzr = dzs + row * zw;
+  const int L = sp.n_layers - 1;
+  const int dout = sp.dims[sp.n_layers];
+  for (int j = 0; j < dout; ++j) {
+    const float z = zr[zoff[L] + j];
+    float g;
+    if (sp.out_act == 0) {
+      g = z >= 0.0f ? dY[row * dout + j] : 0.0f;
+    } else {
+      const float s = 1.0f / (1.0f + expf(-z));
+      g = dY[row * dout + j] * s * (1.0f - s);
+    }
+    cur[j * kRowsPerBlock] = g;
+    dzr[zoff[L] + j] = g;
+  }
+  for (int l = L; l >= 0; --l) {
+    const int din = sp.dims[l], do_ = sp.dims[l + 1];
+    const float* w = W + (sp.w_off[l] - sp.grid_len);
+    for (int i = 0; i < din; ++i) {
+      float acc = 0.0f;
+      for (int j = 0; j < do_; ++j) acc = fmaf(cur[j * kRowsPerBlock], w[j * din + i], acc);
+      if (l > 0) {
+        const float z = zr[zoff[l - 1] + i];
+        const float g = z >= 0.0f ? acc : 0.0f;
+        nxt[i * kRowsPerBlock] = g;
+        dzr[zoff[l - 1] + i] = g;
+      } else {
+        dX[row * sp.in_dim + i] = acc;
+      }
+    }
+    float* t = cur; cur = nxt; nxt = t;
+  }
+}
+
+// dW_l[j][i] = sum_b dz_l[b][j] * a_{l-1}[b][i]; db_l[j] = sum_b dz_l[b][j].
+// grid = (chunks, layers); each block reduces kDwRows rows of one layer in
+// registers then adds its partial into grad with one atomic per weight.
+constexpr int kDwRows = 256;
+constexpr int kDwThreads = 256;
+
+__global__ void k_weight_grad(nirc_spec_t sp, const float* __restrict__ X,
+                              const float* __restrict__ zs, const float* __restrict__ dzs,
+                              int64_t n, float* __restrict__ grad,
+                              const int32_t* __restrict__ flags) {
+  if (flags && (flags[0] & 3)) return;
+  const int l = blockIdx.y;
+  const int din = sp.dims[l], dout = sp.dims[l + 1];
+  const int zw = zs_width(sp);
+  int zoff_l = 0, zoff_prev = 0;
+  for (int k = 0; k < l; ++k) zoff_l += sp.dims[k + 1];
+  zoff_prev = zoff_l - (l > 0 ? sp.dims[l] : 0);
+  __shared__ float s_a[32][129];
+  __shared__ float s_dz[32][129];
+  const int64_t r0 = (int64_t)blockIdx.x * kDwRows;
+  const int64_t r1 = (n < r0 + kDwRows) ? n : r0 + kDwRows;
+  const int nw = dout * (din + 1);  // +1 column: bias
+  if (blockIdx.z * 32 * kDwThreads >= nw) return;
+  // each thread owns up to 32 (j,i) pairs
+  float acc[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) acc[k] = 0.0f;
+  for (int64_t rb = r0; rb < r1; rb += 32) {
+    const int nr = (int)((r1 - rb) < 32 ? (r1 - rb) : 32);
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * 128; e += blockDim.x) {
+      const int rr = e / 128, c = e % 128;
+      if (rr < nr) {
+        const int64_t row = rb + rr;
+        if (c < din) {
+          float a;
+          if (l == 0) a = X[row * sp.in_dim + c];
+          else a = act_of(sp, l - 1, zs[row * zw + zoff_prev + c]);
+          s_a[rr][c] = a;
+        }
+        if (c < dout) s_dz[rr][c] = dzs[row * zw + zoff_l + c];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const int e = blockIdx.z * 32 * kDwThreads + threadIdx.x + k * kDwThreads;
+      if (e < nw) {
+        const int j = e / (din + 1), i = e % (din + 1);
+        float s = acc[k];
+        for (int rr = 0; rr < nr; ++rr) s = fmaf(s_dz[rr][j], i < din ? s_a[rr][i] : 1.0f, s);
+        acc[k] = s;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const int e = blockIdx.z * 32 * kDwThreads + threadIdx.x + k * kDwThreads;
+    if (e < nw) {
+      const int j = e / (din + 1), i = e % (din + 1);
+      float* dst = (i < din) ? grad + sp.w_off[l] + j * din + i : grad + sp.b_off[l] + j;
+      atomicAdd(dst, acc[k]);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------
+// Dense Adam (adam.py:20-33).  All arithmetic is the reference's f32
+// sequence: m += f32(1-b1)*(g-m); v += f32(1-b2)*(g*g-v);
+// theta -= (f32(lr)*(m/f32(1-b1^t))) / (sqrt(v/f32(1-b2^t)) + f32(eps)).
+// Pass 1 flags any non-finite gradient; pass 2 applies or counts a skip.
+// ----------------------------------------------------------------------
+__global__ void k_adam_check(const float* __restrict__ g, int64_t n, int32_t* __restrict__ bad,
+                             const int32_t* __restrict__ gate) {
+  if (gate && gate[0]) return;
+  int found = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    found |= !isfinite(g[i]);
+  found = __syncthreads_or(found);
+  if (found && threadIdx.x == 0) atomicExch(bad, 1);
+}
+
+__global__ void k_adam_apply(float* __restrict__ theta, float* __restrict__ m,
+                             float* __restrict__ v, const float* __restrict__ g, int64_t n,
+                             int64_t* __restrict__ t, int64_t* __restrict__ skipped, float lr,
+                             double b1, double b2, float eps, const int32_t* __restrict__ bad,
+                             const int32_t* __restrict__ gate) {
+  if (gate && gate[0]) return;
+  if (bad[0]) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) skipped[0] += 1;
+    return;
+  }
+  const int64_t tn = t[0] + 1;  // read before block 0 publishes (see k_adam_tick)
+  const float c1 = (float)(1.0 - b1);
+  const float c2 = (float)(1.0 - b2);
+  const float bc1 = (float)(1.0 - pow(b1, (double)tn));
+  const float bc2 = (float)(1.0 - pow(b2, (double)tn));
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    float mi = m[i], vi = v[i];
+    mi = __fadd_rn(mi, __fmul_rn(c1, __fsub_rn(gi, mi)));
+    vi = __fadd_rn(vi, __fmul_rn(c2, __fsub_rn(__fmul_rn(gi, gi), vi)));
+    m[i] = mi;
+    v[i] = vi;
+    const float mh = __fdiv_rn(mi, bc1);
+    const float vh = __fdiv_rn(vi, bc2);
+    const float upd = __fdiv_rn(__fmul_rn(lr, mh), __fadd_rn(__fsqrt_rn(vh), eps));
+    theta[i] = __fsub_rn(theta[i], upd);
+  }
+}
+
+__global__ void k_adam_tick(int64_t* __restrict__ t, const int32_t* __restrict__ bad,
+                            const int32_t* __restrict__ gate) {
+  if (gate && gate[0]) return;
+  if (!bad[0]) t[0] += 1;
+}
+
+// ----------------------------------------------------------------------
+// Batch selection (caches.py:327-329): keys x_i = mix64(K + G*(step*n+i))>>11
+// with K = stream_key(seed, P_SHUFFLE, 0, frame, 0) (rng.py:100-106 puts
+// the stream in the pixel slot); idx = stable argsort(x)[:min(cap, n)].
+// One CTA: radix-select the cap-th key (11-bit digits over 53 bits), then a
+// bitonic sort of the selected (key, index) pairs in shared memory.
+// ----------------------------------------------------------------------
+constexpr int kSelThreads = 1024;
+constexpr int kSelMax = 16384;
+
+__device__ inline uint64_t shuffle_key(uint64_t K, uint64_t dim) {
+  return rand_u64(K, dim) >> 11;
+}
+
+__global__ void __launch_bounds__(kSelThreads, 1)
+k_select(uint64_t K, uint64_t offset, int64_t n, int cap, int64_t* __restrict__ idx_out,
+         const int32_t* __restrict__ flags) {
+  extern __shared__ unsigned char sel_smem[];
+  uint64_t* keys = reinterpret_cast<uint64_t*>(sel_smem);
+  int32_t* ids = reinterpret_cast<int32_t*>(keys + kSelMax);
+  __shared__ uint32_t hist[2048];
+  __shared__ uint64_t s_prefix;
+  __shared__ int64_t s_rank;   // rank of the wanted element within the bucket
+  __shared__ int s_count, s_eq_taken;
+  __shared__ int warp_eq[kSelThreads / 32];
+  if (flags && (flags[0] & 3)) return;
+  const int tid = threadIdx.x;
+  const int B = (int)(n < cap ? n : cap);
+  int P = 1;
+  while (P < B) P <<= 1;
+  if (n <= cap) {
+    for (int i = tid; i < P; i += kSelThreads) {
+      keys[i] = i < n ? shuffle_key(K, offset + i) : ~0ull;
+      ids[i] = i < n ? i : INT_MAX;
+    }
+  } else {
+    // radix select: find the exact key of rank B-1 (0-based) among n keys.
+    uint64_t prefix = 0;
+    int64_t rank = B - 1;
+    int shift = 53;
+    if (tid == 0) { s_prefix = 0; s_rank = rank; }
+    while (shift > 0) {
+      const int bits = shift >= 11 ? 11 : shift;
+      shift -= bits;
+      for (int i = tid; i < 2048; i += kSelThreads) hist[i] = 0;
+      __syncthreads();
+      prefix = s_prefix;
+      rank = s_rank;
+      const uint64_t hi_mask = (shift + bits >= 64) ? 0 : (~0ull << (shift + bits));
+      for (int64_t i = tid; i < n; i += kSelThreads) {
+        const uint64_t k = shuffle_key(K, offset + i);
+        if ((k & hi_mask) == prefix) atomicAdd(&hist[(k >> shift) & ((1u << bits) - 1)], 1u);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int64_t acc = 0;
+        for (int d = 0; d < (1 << bits); ++d) {
+          if (acc + hist[d] > rank) {
+            s_prefix = prefix | ((uint64_t)d << shift);
+            s_rank = rank - acc;
+            break;
+          }
+          acc += hist[d];
+        }
+      }
+      __syncthreads();
+    }
+    const uint64_t thr = s_prefix;   // key of rank B-1
+    const int64_t eq_need = s_rank + 1;  // how many keys == thr are taken (stable: lowest ids)
+    if (tid == 0) { s_count = 0; s_eq_taken = 0; }
+    __syncthreads();
+    for (int64_t base = 0; base < n; base += kSelThreads) {
+      const int64_t i = base + tid;
+      uint64_t k = 0;
+      bool less = false, eq = false;
+      if (i < n) {
+        k = shuffle_key(K, offset + i);
+        less = k < thr;
+        eq = k == thr;
+      }
+      // equal keys are taken in index order: rank them within this chunk
+      const unsigned eq_ballot = __ballot_sync(0xffffffffu, eq);
+      const int lane = tid & 31, wid = tid >> 5;
+      if (lane == 0) warp_eq[wid] = __popc(eq_ballot);
+      __syncthreads();
+      int before = s_eq_taken;
+      for (int w = 0; w < wid; ++w) before += warp_eq[w];
+      before += __popc(eq_ballot & ((1u << lane) - 1u));
+      const bool take = less || (eq && before < eq_need);
+      if (take) {
+        const int pos = atomicAdd(&s_count, 1);
+        keys[pos] = k;
+        ids[pos] = (int32_t)i;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int tot = 0;
+        for (int w = 0; w < kSelThreads / 32; ++w) tot += warp_eq[w];
+        s_eq_taken += tot;
+      }
+      __syncthreads();
+    }
+    for (int i = B + tid; i < P; i += kSelThreads) {
+      keys[i] = ~0ull;
+      ids[i] = INT_MAX;
+    }
+  }
+  __syncthreads();
+  // bitonic sort ascending by (key, id)
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < P; i += kSelThreads) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool up = (i & k) == 0;
+          const uint64_t ka = keys[i], kb = keys[ixj];
+          const int32_t ia = ids[i], ib = ids[ixj];
+          const bool gt = (ka > kb) || (ka == kb && ia > ib);
+          if (gt == up) {
+            keys[i] = kb; keys[ixj] = ka;
+            ids[i] = ib; ids[ixj] = ia;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = tid; i < B; i += kSelThreads) idx_out[i] = ids[i];
+}
+
+// Gather + encode + forward for the training batch: row i of the batch is
+// record idx[i] (caches.py:330-333).
+__global__ void k_train_forward(nirc_spec_t sp, const float* __restrict__ theta,
+                                nirc_records_t rec, const int64_t* __restrict__ idx, int64_t B,
+                                float* __restrict__ X, float* __restrict__ zs,
+                                float* __restrict__ Y, const int32_t* __restrict__ flags) {
+  extern __shared__ float smem[];
+  if (flags && (flags[0] & 3)) return;
+  float* W = smem;
+  stage_params(sp, theta, W);
+  const int dmax = net_dmax(sp);
+  float* a = W + net_param_count(sp) + threadIdx.x;
+  float* b = a + (dmax + 1) * kRowsPerBlock;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * kRowsPerBlock + threadIdx.x;
+  if (i >= B) return;
+  const int64_t r = idx[i];
+  float* xr = X + i * sp.in_dim;
+  encode_row(sp, theta, rec.pos + 3 * r, rec.ns + 3 * r, rec.alb + 3 * r, rec.rough[r],
+             rec.dirs + 3 * r,
+             [&](int k, float v) {
+               xr[k] = v;
+               a[k * kRowsPerBlock] = v;
+             },
+             nullptr, nullptr);
+  simt_forward_row(sp, W, a, b, kRowsPerBlock, zs + i * zs_width(sp));
+  const float* out = (sp.n_layers % 2 == 1) ? b : a;
+  const int dout = sp.dims[sp.n_layers];
+  for (int j = 0; j < dout; ++j) Y[i * dout + j] = out[j * kRowsPerBlock];
+}
+
+// Hash-grid scatter for the training batch: slots and weights are recomputed
+// from the record position (bit-identical to encode_batch's entries/weights)
+// instead of being stored.  One thread per (row, level).
+__global__ void k_train_scatter(nirc_spec_t sp, nirc_records_t rec,
+                                const int64_t* __restrict__ idx, int64_t B,
+                                const float* __restrict__ dX, float* __restrict__ grad,
+                                const int32_t* __restrict__ flags) {
+  if (flags && (flags[0] & 3)) return;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B * sp.levels) return;
+  const int64_t i = t / sp.levels;
+  const int lvl = (int)(t % sp.levels);
+  const int64_t r = idx[i];
+  const double* p = rec.pos + 3 * r;
+  const float ux = norm_coord(p[0], sp.bb_min[0], sp.bb_inv[0]);
+  const float uy = norm_coord(p[1], sp.bb_min[1], sp.bb_inv[1]);
+  const float uz = norm_coord(p[2], sp.bb_min[2], sp.bb_inv[2]);
+  const LevelCell c = level_cell(ux, uy, uz, sp.res[lvl]);
+  const uint32_t T = 1u << sp.table_log2;
+  const int F = sp.feats;
+  float* gl = grad + (int64_t)lvl * T * F;
+  for (int f = 0; f < F; ++f) {
+    const float d = dX[i * sp.in_dim + lvl * F + f];
+    if (d == 0.0f) continue;
+    for (int k = 0; k < 8; ++k)
+      atomicAdd(gl + (int64_t)corner_hash(c, k, T - 1u) * F + f, __fmul_rn(corner_weight(c, k), d));
+  }
+}
+
+}  // namespace nirc
+
+using namespace nirc;
+
+// ======================================================================
+// C ABI
+// ======================================================================
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+static inline int blocks_for(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+static int check_spec(const nirc_spec_t* sp) {
+  if (!sp) { set_last_error("spec is NULL"); return NIRC_E_CONFIG; }
+  if (sp->levels < 1 || sp->levels > NIRC_MAX_LEVELS || sp->feats < 1 || sp->feats > 4 ||
+      sp->bands < 1 || sp->bands > NIRC_MAX_BANDS || sp->n_layers < 1 ||
+      sp->n_layers > NIRC_MAX_LAYERS || sp->table_log2 < 1 || sp->table_log2 > 30) {
+    set_last_error("unsupported spec (levels=%d feats=%d bands=%d layers=%d)", sp->levels,
+                   sp->feats, sp->bands, sp->n_layers);
+    return NIRC_E_CONFIG;
+  }
+  if (net_dmax(*sp) > 128) {
+    set_last_error("layer width %d > 128 unsupported", net_dmax(*sp));
+    return NIRC_E_UNSUPPORTED;
+  }
+  if (simt_smem_bytes(*sp) > 200 * 1024) {
+    set_last_error("network too large for the shared-memory SIMT path");
+    return NIRC_E_UNSUPPORTED;
+  }
+  return NIRC_OK;
+}
+
+static unsigned dw_zsplit(const nirc_spec_t& sp) {
+  int mx = 0;
+  for (int l = 0; l < sp.n_layers; ++l) {
+    const int nw = sp.dims[l + 1] * (sp.dims[l] + 1);
+    mx = nw > mx ? nw : mx;
+  }
+  return (unsigned)((mx + 32 * kDwThreads - 1) / (32 * kDwThreads));
+}
+
+static int set_smem(const void* fn, size_t bytes) {
+  NIRC_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return NIRC_OK;
+}
+
+extern "C" int nirc_encode(const nirc_spec_t* spec, const float* theta, const double* pos,
+                           const double* normal, const double* albedo, const double* rough,
+                           const double* dirs, int64_t n, float* X, int64_t* entries,
+                           float* weights, void* stream) {
+  int st = check_spec(spec);
+  if (st) return st;
+  if (n <= 0) return NIRC_OK;
+  k_encode<<<blocks_for(n, 128), 128, 0, S(stream)>>>(*spec, theta, pos, normal, albedo, rough,
+                                                     dirs, n, X, entries, weights);
+  NIRC_LAUNCH_CHECK("k_encode");
+  return NIRC_OK;
+}
+
+extern "C" int nirc_scatter_grid_grad(const nirc_spec_t* spec, float* grad,
+                                      const int64_t* entries, const float* weights,
+                                      const float* dX, int64_t n, int64_t dx_stride,
+                                      void* stream) {
+  int st = check_spec(spec);
+  if (st) return st;
+  const int64_t total = n * spec->levels * 8;
+  if (total <= 0) return NIRC_OK;
+  k_scatter<<<blocks_for(total, 256), 256, 0, S(stream)>>>(*spec, grad, entries, weights, dX, n,
+                                                          dx_stride);
+  NIRC_LAUNCH_CHECK("k_scatter");
+  return NIRC_OK;
+}
+
+extern "C" int nirc_mlp_forward(const nirc_spec_t* spec, const float* theta, const float* X,
+                                int64_t n, float* Y, float* zs, int32_t* nonfinite_flag,
+                                void* stream) {
+  int st = check_spec(spec);
+  if (st) return st;
+  if (n <= 0) return NIRC_OK;
+  const size_t sm = simt_smem_bytes(*spec);
+  if ((st = set_smem((const void*)k_mlp_forward, sm))) return st;
+  k_mlp_forward<<<blocks_for(n, kRowsPerBlock), kRowsPerBlock, sm, S(stream)>>>(
+      *spec, theta, X, n, Y, zs, nonfinite_flag);
+  NIRC_LAUNCH_CHECK("k_mlp_forward");
+  return NIRC_OK;
+}
+
+extern "C" int nirc_mlp_backward(const nirc_spec_t* spec, const float* theta, const float* X,
+                                 const float* zs, const float* dY, int64_t n, float* grad,
+                                 float* dX, float* scratch, void* stream) {
+  int st = check_spec(spec);
+  if (st) return st;
+  if (n <= 0) return NIRC_OK;
+  const size_t sm = simt_smem_bytes(*spec);
+  if ((st = set_smem((const void*)k_backward_rows, sm))) return st;
+  k_backward_rows<<<blocks_for(n, kRowsPerBlock), kRowsPerBlock, sm, S(stream)>>>(
+      *spec, theta, zs, dY, n, scratch, dX, nullptr);
+  NIRC_LAUNCH_CHECK("k_backward_rows");
+  dim3 g(blocks_for(n, kDwRows), spec->n_layers, dw_zsplit(*spec));
+  k_weight_grad<<<g, kDwThreads, 0, S(stream)>>>(*spec, X, zs, scratch, n, grad, nullptr);
+  NIRC_LAUNCH_CHECK("k_weight_grad");
+  return NIRC_OK;
+}
+
+extern "C" int nirc_loss(int32_t kind, const float* Y, const double* target, const double* pdf,
+                         const double* running_mean, double eps, int64_t n, float* dY,
+                         double* loss_out, int32_t* status_flags, double* scratch,
+                         void* stream) {
+  if (kind < 0 || kind > 3) { set_last_error("unknown loss kind %d", kind); return NIRC_E_CONFIG; }
+  if (n <= 0) return NIRC_OK;
+  const int nb = blocks_for(n, kLossThreads);
+  k_loss<<<nb, kLossThreads, 0, S(stream)>>>(kind, Y, target, pdf, running_mean, eps, n, dY,
+                                             scratch, status_flags, nullptr, 0);
+  NIRC_LAUNCH_CHECK("k_loss");
+  k_loss_final<<<1, 32, 0, S(stream)>>>(scratch, nb, n, loss_out, status_flags, nullptr, 0);
+  NIRC_LAUNCH_CHECK("k_loss_final");
+  return NIRC_OK;
+}
+
+extern "C" int nirc_adam_step(float* theta, float* m, float* v, const float* grad, int64_t n,
+                              int64_t* t, int64_t* skipped, double lr, double beta1,
+                              double beta2, double eps, const int32_t* gate_flags,
+                              int32_t* scratch, void* stream) {
+  if (n <= 0) return NIRC_OK;
+  NIRC_CUDA_TRY(cudaMemsetAsync(scratch, 0, sizeof(int32_t), S(stream)));
+  const int nb = 148 * 4;
+  k_adam_check<<<nb, 256, 0, S(stream)>>>(grad, n, scratch, gate_flags);
+  NIRC_LAUNCH_CHECK("k_adam_check");
+  k_adam_apply<<<nb, 256, 0, S(stream)>>>(theta, m, v, grad, n, t, skipped, (float)lr, beta1,
+                                          beta2, (float)eps, scratch, gate_flags);
+  NIRC_LAUNCH_CHECK("k_adam_apply");
+  k_adam_tick<<<1, 1, 0, S(stream)>>>(t, scratch, gate_flags);
+  NIRC_LAUNCH_CHECK("k_adam_tick");
+  return NIRC_OK;
+}
+
+// ---------------------------------------------------------------- train --
+namespace {
+struct TrainWs {
+  int64_t* idx;
+  float *X, *zs, *Y, *dY, *dzs, *dX, *grad;
+  double* partial;
+  int32_t* adam_bad;
+  size_t bytes;
+};
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+TrainWs carve_train(const nirc_spec_t& sp, int64_t B, void* base) {
+  TrainWs w{};
+  char* p = reinterpret_cast<char*>(base);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* r = p ? p + off : nullptr;
+    off += align_up(bytes);
+    return r;
+  };
+  const int zw = zs_width(sp);
+  w.idx = (int64_t*)take(B * 8);
+  w.X = (float*)take(B * sp.in_dim * 4);
+  w.zs = (float*)take(B * zw * 4);
+  w.Y = (float*)take(B * 3 * 4 + 16);
+  w.dY = (float*)take(B * 3 * 4 + 16);
+  w.dzs = (float*)take(B * zw * 4);
+  w.dX = (float*)take(B * sp.in_dim * 4);
+  w.grad = (float*)take(sp.theta_len * 4);
+  w.partial = (double*)take((B / kLossThreads + 2) * 3 * 8);
+  w.adam_bad = (int32_t*)take(16);
+  w.bytes = off;
+  return w;
+}
+}  // namespace
+
+extern "C" int64_t nirc_train_workspace_bytes(const nirc_spec_t* spec, int64_t n_records,
+                                              int32_t batch_cap) {
+  const int64_t B = n_records < batch_cap ? n_records : batch_cap;
+  return (int64_t)carve_train(*spec, B, nullptr).bytes;
+}
+
+extern "C" int nirc_train_step(const nirc_spec_t* spec, float* theta, float* m, float* v,
+                               int64_t* t, int64_t* skipped, const nirc_records_t* rec,
+                               uint64_t seed, int64_t frame, int32_t step, int32_t batch_cap,
+                               int32_t loss_kind, double loss_eps, double lr,
+                               double* running_mean, double* loss_out, int32_t* status_flags,
+                               int64_t* batch_idx_out, void* workspace,
+                               int64_t workspace_bytes, void* stream) {
+  int st = check_spec(spec);
+  if (st) return st;
+  const int64_t n = rec->n;
+  if (n <= 0) { set_last_error("cannot train on an empty record set"); return NIRC_E_CONFIG; }
+  if (batch_cap < 1) { set_last_error("batch must be positive"); return NIRC_E_CONFIG; }
+  if (batch_cap > kSelMax && n > kSelMax) {
+    set_last_error("batch cap %d > %d unsupported", batch_cap, kSelMax);
+    return NIRC_E_UNSUPPORTED;
+  }
+  if (n > INT_MAX) { set_last_error("too many records"); return NIRC_E_UNSUPPORTED; }
+  const int64_t B = n < batch_cap ? n : batch_cap;
+  TrainWs w = carve_train(*spec, B, workspace);
+  if ((int64_t)w.bytes > workspace_bytes) {
+    set_last_error("train workspace too small (%lld < %lld)", (long long)workspace_bytes,
+                   (long long)w.bytes);
+    return NIRC_E_CONFIG;
+  }
+  cudaStream_t s = S(stream);
+  const uint64_t K = stream_key(seed, P_SHUFFLE, 0, (uint64_t)frame, 0);
+  const size_t sel_smem = kSelMax * (8 + 4);
+  if ((st = set_smem((const void*)k_select, sel_smem))) return st;
+  k_select<<<1, kSelThreads, sel_smem, s>>>(K, (uint64_t)step * (uint64_t)n, n, (int)B,
+                                            w.idx, status_flags);
+  NIRC_LAUNCH_CHECK("k_select");
+  if (batch_idx_out)
+    NIRC_CUDA_TRY(cudaMemcpyAsync(batch_idx_out, w.idx, B * 8, cudaMemcpyDeviceToDevice, s));
+  const size_t sm = simt_smem_bytes(*spec);
+  if ((st = set_smem((const void*)k_train_forward, sm))) return st;
+  k_train_forward<<<blocks_for(B, kRowsPerBlock), kRowsPerBlock, sm, s>>>(
+      *spec, theta, *rec, w.idx, B, w.X, w.zs, w.Y, status_flags);
+  NIRC_LAUNCH_CHECK("k_train_forward");
+  const int nb = blocks_for(B, kLossThreads);
+  if (loss_kind == 2) {  // variance: EMA of the residual mean first (caches.py:340-343)
+    k_loss<<<nb, kLossThreads, 0, s>>>(loss_kind, w.Y, rec->target, rec->pdf, running_mean,
+                                        loss_eps, B, w.dY, w.partial, status_flags, w.idx, 1);
+    k_loss_final<<<1, 32, 0, s>>>(w.partial, nb, B, loss_out, status_flags, running_mean, 1);
+  }
+  k_loss<<<nb, kLossThreads, 0, s>>>(loss_kind, w.Y, rec->target, rec->pdf, running_mean,
+                                      loss_eps, B, w.dY, w.partial, status_flags, w.idx, 0);
+  NIRC_LAUNCH_CHECK("k_loss");
+  k_loss_final<<<1, 32, 0, s>>>(w.partial, nb, B, loss_out, status_flags, nullptr, 0);
+  NIRC_LAUNCH_CHECK("k_loss_final");
+  NIRC_CUDA_TRY(cudaMemsetAsync(w.grad, 0, spec->theta_len * 4, s));
+  if ((st = set_smem((const void*)k_backward_rows, sm))) return st;
+  k_backward_rows<<<blocks_for(B, kRowsPerBlock), kRowsPerBlock, sm, s>>>(
+      *spec, theta, w.zs, w.dY, B, w.dzs, w.dX, status_flags);
+  NIRC_LAUNCH_CHECK("k_backward_rows");
+  dim3 g(blocks_for(B, kDwRows), spec->n_layers, dw_zsplit(*spec));
+  k_weight_grad<<<g, kDwThreads, 0, s>>>(*spec, w.X, w.zs, w.dzs, B, w.grad, status_flags);
+  NIRC_LAUNCH_CHECK("k_weight_grad");
+  k_train_scatter<<<blocks_for(B * spec->levels, 256), 256, 0, s>>>(*spec, *rec, w.idx, B, w.dX,
+                                                                   w.grad, status_flags);
+  NIRC_LAUNCH_CHECK("k_train_scatter");
+  return nirc_adam_step(theta, m, v, w.grad, spec->theta_len, t, skipped, lr, 0.9, 0.99, 1e-8,
+                        status_flags, w.adam_bad, stream);
+}

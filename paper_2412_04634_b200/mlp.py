@@ -1,0 +1,167 @@
+"""Tiny fully connected networks over one flat parameter vector
+(drop-in for pkg/src/nirclab/mlp.py).
+
+The parameter layout, ``make_spec`` and ``init_theta`` are host-side and
+identical to the reference (same numpy Generator calls, so the same theta
+for the same seed).  ``mlp_forward`` / ``mlp_backward`` / ``full_forward``
+run on the B200 through the C ABI:
+
+* ``full_forward`` is the fused persistent kernel (encode + tcgen05 3xTF32
+  MLP, activations only in SMEM/TMEM) -- the NIRC inference hot path;
+* ``mlp_forward`` / ``mlp_backward`` are the fp32 SIMT twin used for the
+  reference's batch API and the training step.
+"""
+
+from __future__ import annotations
+
+from collections import namedtuple
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+from .encoding import AUX_DIM, encode_batch, level_resolutions, scatter_grid_grad
+from .errors import DivergenceError
+
+ACT_RELU = 0
+ACT_SIGMOID = 1
+
+PRECISION_TF32X3 = 0   # tcgen05.mma kind::tf32, hi/lo split operands
+PRECISION_FP32 = 1     # SIMT fp32 twin
+
+NetSpec = namedtuple(
+    "NetSpec",
+    ["levels", "table", "feats", "res", "bb_min", "bb_inv", "bands", "in_dim", "nl",
+     "w_off", "b_off", "dims", "out_act", "grid_len", "theta_len"],
+)
+
+
+def make_spec(levels=12, table=2 ** 15, feats=2, base_res=4, max_res=256, bands=4,
+              depth=4, width=64, out_dim=3, out_act=ACT_RELU, bb_min=None, bb_ext=None):
+    """Layout of theta: hash tables, then per layer W (dout x din) and b
+    (mlp.py:36-62)."""
+    bb_min = np.zeros(3) if bb_min is None else np.asarray(bb_min, float)
+    bb_ext = np.ones(3) if bb_ext is None else np.asarray(bb_ext, float)
+    in_dim = levels * feats + bands * bands + AUX_DIM
+    dims = [in_dim] + [width] * depth + [out_dim]
+    grid_len = levels * table * feats
+    w_off, b_off = [], []
+    cursor = grid_len
+    for din, dout in zip(dims[:-1], dims[1:]):
+        w_off.append(cursor)
+        cursor += din * dout
+        b_off.append(cursor)
+        cursor += dout
+    return NetSpec(levels=levels, table=table, feats=feats,
+                   res=level_resolutions(levels, base_res, max_res),
+                   bb_min=bb_min, bb_inv=1.0 / bb_ext, bands=bands, in_dim=in_dim,
+                   nl=len(dims) - 1, w_off=np.array(w_off, np.int64),
+                   b_off=np.array(b_off, np.int64), dims=np.array(dims, np.int64),
+                   out_act=out_act, grid_len=grid_len, theta_len=cursor)
+
+
+def init_theta(spec, seed=0, dtype=np.float32, out_scale=0.0):
+    """Uniform(+-1e-4) grid, He-normal hidden layers, zero biases, zero (or
+    N(0, out_scale)) output layer -- the same Generator draws as
+    mlp.py:65-85."""
+    gen = np.random.default_rng(seed)
+    theta = np.zeros(spec.theta_len, dtype)
+    theta[: spec.grid_len] = gen.uniform(-1e-4, 1e-4, spec.grid_len)
+    for layer in range(spec.nl):
+        din = int(spec.dims[layer])
+        dout = int(spec.dims[layer + 1])
+        w = int(spec.w_off[layer])
+        if layer == spec.nl - 1:
+            if out_scale > 0.0:
+                theta[w: w + din * dout] = gen.normal(0.0, out_scale, din * dout)
+        else:
+            theta[w: w + din * dout] = gen.normal(0.0, np.sqrt(2.0 / din), din * dout)
+    return theta
+
+
+def weight_view(spec, theta, layer):
+    w = int(spec.w_off[layer])
+    din = int(spec.dims[layer])
+    dout = int(spec.dims[layer + 1])
+    return theta[w: w + din * dout].reshape(dout, din)
+
+
+def bias_view(spec, theta, layer):
+    b = int(spec.b_off[layer])
+    return theta[b: b + int(spec.dims[layer + 1])]
+
+
+def _zs_width(spec):
+    return int(sum(int(d) for d in spec.dims[1:]))
+
+
+def mlp_forward(spec, theta, X, training=False):
+    """Batch forward (mlp.py:102-122).  Returns Y, or (Y, cache) when
+    training; the cache holds X and every pre-activation for mlp_backward.
+    Raises DivergenceError if theta holds a non-finite value."""
+    host = _dev.is_host(X)
+    th = _dev.dev(theta, torch.float32)
+    x = _dev.dev(X, torch.float32)
+    if x.dim() == 1:
+        x = x.reshape(1, -1)
+    n = int(x.shape[0])
+    dout = int(spec.dims[-1])
+    Y = _dev.empty((n, dout), torch.float32)
+    zs = _dev.empty((n, _zs_width(spec)), torch.float32) if training else None
+    flag = _dev.zeros((1,), torch.int32)
+    lib = _lib.load()
+    _lib.check(lib.nirc_mlp_forward(_lib.make_c_spec(spec), _dev.ptr(th), _dev.ptr(x), n,
+                                    _dev.ptr(Y), _dev.ptr(zs), _dev.ptr(flag), _dev.stream()),
+               "nirc_mlp_forward")
+    if int(flag.item()) != 0:
+        raise DivergenceError("non-finite network parameter")
+    if training:
+        return _dev.out(Y, host), (x, zs)
+    return _dev.out(Y, host)
+
+
+def mlp_backward(spec, theta, cache, dY, entries=None, weights=None):
+    """Reverse mode (mlp.py:125-154); ReLU' is (z >= 0) on every layer.
+    Returns a gradient congruent to theta."""
+    X, zs = cache
+    host = _dev.is_host(dY)
+    th = _dev.dev(theta, torch.float32)
+    dy = _dev.dev(dY, torch.float32)
+    n = int(X.shape[0])
+    g = _dev.zeros((spec.theta_len,), torch.float32)
+    dX = _dev.empty((n, spec.in_dim), torch.float32)
+    scratch = _dev.empty((n, _zs_width(spec)), torch.float32)
+    lib = _lib.load()
+    _lib.check(lib.nirc_mlp_backward(_lib.make_c_spec(spec), _dev.ptr(th), _dev.ptr(X),
+                                     _dev.ptr(zs), _dev.ptr(dy), n, _dev.ptr(g), _dev.ptr(dX),
+                                     _dev.ptr(scratch), _dev.stream()),
+               "nirc_mlp_backward")
+    if entries is not None:
+        scatter_grid_grad(spec, g, _dev.dev(entries, torch.int64),
+                          _dev.dev(weights, torch.float32), dX)
+    return _dev.out(g, host)
+
+
+def full_forward(spec, theta, pos, normal, albedo, rough, dirs, training=False,
+                 precision=PRECISION_TF32X3):
+    """encode_batch + mlp_forward (mlp.py:216-224).  Inference runs the fused
+    tcgen05 kernel; training returns the reference tuple via the SIMT path."""
+    if training:
+        X, entries, weights = encode_batch(spec, theta, pos, normal, albedo, rough, dirs)
+        Y, cache = mlp_forward(spec, theta, X, training=True)
+        return Y, cache, entries, weights
+    host = _dev.is_host(pos)
+    th = _dev.dev(theta, torch.float32)
+    args = [_dev.dev(a, torch.float64) for a in (pos, normal, albedo, rough, dirs)]
+    n = int(args[0].shape[0])
+    Y = _dev.empty((n, int(spec.dims[-1])), torch.float32)
+    lib = _lib.load()
+    st = lib.nirc_full_forward(_lib.make_c_spec(spec), _dev.ptr(th),
+                               *[_dev.ptr(a) for a in args], n, _dev.ptr(Y), int(precision),
+                               _dev.stream())
+    if st == _lib.NIRC_E_UNSUPPORTED:
+        # non-default layouts (tests' tiny nets) take the generic device path
+        X, _, _ = encode_batch(spec, th, *args)
+        return _dev.out(mlp_forward(spec, th, X), host)
+    _lib.check(st, "nirc_full_forward")
+    return _dev.out(Y, host)

@@ -1,0 +1,215 @@
+"""GPU parity of the neural hot path against the oracle and the reference's
+golden vectors.  Everything runs through the C ABI (libnirc_b200.so).
+
+Tolerances:
+  * slots, trilinear weights, encoded rows, batch indices: bit-exact;
+  * network outputs: 3xTF32 tcgen05 and fp32 SIMT twin rtol 1e-4 / atol 1e-6
+    (the reference's own scalar-vs-batch bar, tests/test_neural.py:174);
+  * Adam: bit-exact given identical gradients;
+  * training steps: loss rtol 1e-4, parameters rtol 1e-3 / atol 1e-5 (the
+    gradient scatter sums in a different order than np.add.at).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import nirc_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nb():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2412_04634_b200 as pkg
+    from paper_2412_04634_b200 import _lib
+
+    _lib.load()
+    return pkg
+
+
+def _spec(depth=2, **kw):
+    from paper_2412_04634_b200.mlp import make_spec
+
+    return make_spec(depth=depth, **kw)
+
+
+def test_encode_bit_exact(nb, golden):
+    from paper_2412_04634_b200.encoding import encode_batch
+    from paper_2412_04634_b200.mlp import init_theta
+
+    g = golden("encode_forward")
+    spec = _spec(2)
+    theta = init_theta(spec, seed=1, out_scale=0.1)
+    X, ent, wts = encode_batch(spec, theta, g["pos"], g["nrm"], g["alb"], g["rough"], g["dirs"])
+    assert np.array_equal(ent, g["entries"].astype(np.int64))
+    assert np.array_equal(wts, g["weights"])
+    assert np.array_equal(X, g["X"])
+
+
+def test_encode_edge_cases(nb):
+    """Positions outside / on the box clamp exactly like the oracle."""
+    from paper_2412_04634_b200.encoding import encode_batch
+    from paper_2412_04634_b200.mlp import init_theta
+
+    spec = _spec(2)
+    theta = init_theta(spec, seed=2)
+    pos = np.array([[-1.0, 0.0, 2.0], [1.0, 1.0, 1.0], [0.0, 0.0, 0.0], [0.5, 1 - 1e-17, 0.25],
+                    [0.999999, 0.5, 1e-300]])
+    n = len(pos)
+    nrm = np.tile([0.0, 0.0, 1.0], (n, 1))
+    dirs = np.array([[0.0, 0.0, 1.0], [0.0, 0.0, -1.0], [1.0, 0.0, 0.0], [0.6, 0.8, 0.0],
+                     [0.0, -1.0, 0.0]])
+    alb = np.full((n, 3), 0.3)
+    rough = np.linspace(0, 1, n)
+    X, ent, wts = encode_batch(spec, theta, pos, nrm, alb, rough, dirs)
+    os_ = O.Spec(depth=2)
+    Xo, eo, wo = O.encode_batch(os_, theta, pos, nrm, alb, rough, dirs)
+    assert np.array_equal(ent, eo) and np.array_equal(wts, wo) and np.array_equal(X, Xo)
+
+
+@pytest.mark.parametrize("depth", [2, 4])
+@pytest.mark.parametrize("precision", [0, 1])
+def test_full_forward_matches_reference(nb, golden, depth, precision):
+    from paper_2412_04634_b200.mlp import full_forward, init_theta
+
+    g = golden("encode_forward")
+    spec = _spec(depth)
+    theta = init_theta(spec, seed=1, out_scale=0.1)
+    Y = full_forward(spec, theta, g["pos"], g["nrm"], g["alb"], g["rough"], g["dirs"],
+                     precision=precision)
+    ref = g[f"Y_d{depth}"]
+    assert Y.shape == ref.shape
+    np.testing.assert_allclose(Y, ref, rtol=1e-4, atol=1e-6)
+
+
+def test_full_forward_tc_large_and_ragged(nb):
+    """Ragged n (not a multiple of 128) and many tiles per CTA; the tensor
+    core path against the fp32 SIMT twin on the same device inputs."""
+    from paper_2412_04634_b200.mlp import full_forward, init_theta
+
+    spec = _spec(2)
+    theta = torch.from_numpy(init_theta(spec, seed=4, out_scale=0.2)).cuda()
+    n = 300_001
+    q = [torch.from_numpy(a).cuda() for a in O.measure_queries(n, seed=9)]
+    Yt = full_forward(spec, theta, *q, precision=0)
+    Ys = full_forward(spec, theta, *q, precision=1)
+    torch.cuda.synchronize()
+    assert torch.isfinite(Yt).all()
+    np.testing.assert_allclose(Yt.cpu().numpy(), Ys.cpu().numpy(), rtol=1e-4, atol=1e-6)
+    # spot rows against the oracle (f32 numpy) too
+    rows = np.array([0, 1, 127, 128, 129, n // 2, n - 2, n - 1])
+    qo = [a[rows] for a in O.measure_queries(n, seed=9)]
+    Yo = O.full_forward(O.Spec(depth=2), theta.cpu().numpy(), *qo)
+    np.testing.assert_allclose(Yt.cpu().numpy()[rows], Yo, rtol=1e-4, atol=1e-6)
+
+
+def test_tiny_nets_take_generic_path(nb):
+    """Non-default layouts (the reference tests' tiny nets) still run on the
+    device through the generic encode + SIMT kernels."""
+    from paper_2412_04634_b200.mlp import full_forward, init_theta, make_spec
+
+    spec = make_spec(levels=2, table=16, feats=2, base_res=2, max_res=4, bands=1, depth=2,
+                     width=8)
+    theta = init_theta(spec, seed=0, out_scale=0.5)
+    rng = np.random.default_rng(1)
+    n = 33
+    pos, alb, rough = rng.random((n, 3)), rng.random((n, 3)), rng.random(n)
+    nrm = rng.normal(size=(n, 3))
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    dirs = rng.normal(size=(n, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    Y = full_forward(spec, theta, pos, nrm, alb, rough, dirs)
+    os_ = O.Spec(levels=2, table=16, base_res=2, max_res=4, bands=1, depth=2, width=8)
+    Yo = O.full_forward(os_, theta, pos, nrm, alb, rough, dirs)
+    np.testing.assert_allclose(Y, Yo, rtol=1e-5, atol=1e-7)
+
+
+def test_grid_vertex_identity(nb):
+    """tests/test_neural.py:52-64: feature at a grid vertex == table entry."""
+    from paper_2412_04634_b200.encoding import encode_batch
+    from paper_2412_04634_b200.mlp import init_theta, make_spec
+
+    spec = make_spec(levels=1, table=64, feats=2, base_res=4, max_res=4, bands=1, depth=1,
+                     width=4)
+    theta = init_theta(spec, seed=1)
+    theta[: spec.grid_len] = np.random.default_rng(1).random(spec.grid_len)
+    X, _, _ = encode_batch(spec, theta, np.array([[0.25, 0.5, 0.75]]), np.array([[0.0, 0, 1]]),
+                           np.full((1, 3), 0.5), np.ones(1), np.array([[0.0, 0, 1]]))
+    h = (1 * 1 ^ 2 * 2654435761 ^ 3 * 805459861) & 63
+    assert X[0, 0] == theta[h * 2] and X[0, 1] == theta[h * 2 + 1]
+
+
+def test_losses_bit_exact(nb, golden):
+    from paper_2412_04634_b200.losses import loss_l2, loss_relative_l2
+
+    g = golden("losses_adam")
+    v, gr = loss_relative_l2(g["y"], g["t"], g["pdf"])
+    assert v == pytest.approx(float(g["rel_val"]), rel=1e-13)
+    assert np.array_equal(gr, g["rel_grad"].astype(np.float32))
+    v, gr = loss_l2(g["y"], g["t"], g["pdf"])
+    assert v == pytest.approx(float(g["l2_val"]), rel=1e-13)
+    assert np.array_equal(gr, g["l2_grad"].astype(np.float32))
+
+
+def test_loss_rejects_bad_pdf(nb):
+    from paper_2412_04634_b200.errors import InvalidSampleError
+    from paper_2412_04634_b200.losses import loss_l2
+
+    with pytest.raises(InvalidSampleError):
+        loss_l2(np.ones((2, 3), np.float32), np.ones((2, 3)), np.array([1.0, 0.0]))
+
+
+def test_adam_bit_exact(nb, golden):
+    from paper_2412_04634_b200.adam import AdamState, adam_step
+
+    g = golden("losses_adam")
+    theta = torch.from_numpy(g["theta0"].copy()).cuda()
+    st = AdamState(theta)
+    for k, gr in enumerate(g["grads"]):
+        ok = adam_step(st, theta, torch.from_numpy(gr).cuda())
+        assert ok == bool(np.all(np.isfinite(gr)))
+        assert np.array_equal(theta.cpu().numpy(), g["thetas"][k]), k
+    assert st.t == int(g["t_final"]) and st.skipped == int(g["skipped"])
+
+
+def test_mlp_backward_matches_oracle(nb):
+    from paper_2412_04634_b200.mlp import full_forward, init_theta, mlp_backward
+
+    spec = _spec(4, table=2 ** 12)
+    theta = init_theta(spec, seed=5, out_scale=0.3)
+    n = 1000
+    q = O.measure_queries(n, seed=3)
+    Y, cache, ent, wts = full_forward(spec, theta, *q, training=True)
+    dY = (np.random.default_rng(0).normal(size=(n, 3)) / n).astype(np.float32)
+    g = mlp_backward(spec, theta, cache, dY, ent, wts)
+    os_ = O.Spec(table=2 ** 12, depth=4)
+    X, eo, wo = O.encode_batch(os_, theta, *q)
+    yo, co = O.mlp_forward(os_, theta, X, training=True)
+    go = O.mlp_backward(os_, theta, co, dY, eo, wo)
+    np.testing.assert_allclose(Y, yo, rtol=1e-5, atol=1e-7)
+    cos = float(np.dot(g, go) / (np.linalg.norm(g) * np.linalg.norm(go)))
+    assert cos > 0.999999
+    np.testing.assert_allclose(g, go, rtol=2e-3, atol=1e-7 * np.abs(go).max())
+
+
+@pytest.mark.parametrize("tag,n", [("small", 3000), ("big", 20000)])
+def test_train_steps_match_reference(nb, golden, tag, n):
+    from paper_2412_04634_b200.caches import Records, train_frame_device
+
+    g = golden("train_step")
+    rec = O.synth_records(n, seed=5)
+    spec = _spec(4, table=2 ** 12)
+    from paper_2412_04634_b200.mlp import init_theta
+
+    theta = torch.from_numpy(init_theta(spec, seed=3)).cuda()
+    res = train_frame_device(spec, theta, Records(kind="nirc", frame=2, **rec), seed=7, frame=2,
+                             steps=2, return_idx=True)
+    for s in range(2):
+        assert np.array_equal(res.batch_idx[s], g[f"{tag}_idx{s}"]), s
+    np.testing.assert_allclose(res.trace, g[f"{tag}_trace"], rtol=1e-4)
+    th = theta.cpu().numpy()
+    np.testing.assert_allclose(th, g[f"{tag}_theta"], rtol=1e-3, atol=1e-5)
+    assert res.adam.t == int(g[f"{tag}_t"])
