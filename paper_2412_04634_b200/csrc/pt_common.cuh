@@ -1,0 +1,484 @@
+// fp64 path-tracing building blocks (device).  Compiled with -fmad=false so
+// every expression follows the reference's operation order:
+//   geometry   pkg/src/nirclab/geometry.py:19-210
+//   bsdf       pkg/src/nirclab/bsdf.py:27-154
+//   lights     pkg/src/nirclab/lights.py:20-216
+//   NEE        pkg/src/nirclab/kernels.py:44-82
+#pragma once
+#include "common.cuh"
+
+namespace nirc {
+namespace pt {
+
+constexpr double T_FAR = 1.0e30;
+constexpr double INV_PI = 1.0 / 3.141592653589793;
+constexpr double PI = 3.141592653589793;
+constexpr double TWO_PI = 2.0 * 3.141592653589793;
+constexpr double FOUR_PI = 4.0 * 3.141592653589793;
+constexpr double ALPHA_MIN = 1e-3;
+constexpr int MAT_LAMBERT = 0, MAT_CONDUCTOR = 1, MAT_MIRROR = 2;
+constexpr int LIGHT_TRI = 0, LIGHT_SPHERE = 1, LIGHT_ENV = 2;
+constexpr int ENV_NONE = 0, ENV_CONSTANT = 1, ENV_SKY = 2, ENV_LATLONG = 3;
+constexpr int MAXB = 64;
+constexpr double RR_SURVIVE = 0.9;
+constexpr int RR_START = 1;
+
+struct V3 {
+  double x, y, z;
+};
+__device__ inline V3 ld3(const double* a, int i) { return {a[3 * i], a[3 * i + 1], a[3 * i + 2]}; }
+__device__ inline double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+
+// ---------------------------------------------------------- geometry ----
+__device__ inline double ray_tri(V3 o, V3 d, V3 v0, V3 e1, V3 e2) {
+  const double px = d.y * e2.z - d.z * e2.y;
+  const double py = d.z * e2.x - d.x * e2.z;
+  const double pz = d.x * e2.y - d.y * e2.x;
+  const double det = e1.x * px + e1.y * py + e1.z * pz;
+  if (det > -1e-12 && det < 1e-12) return -1.0;
+  const double inv = 1.0 / det;
+  const double tx = o.x - v0.x, ty = o.y - v0.y, tz = o.z - v0.z;
+  const double u = (tx * px + ty * py + tz * pz) * inv;
+  if (u < -1e-9 || u > 1.0 + 1e-9) return -1.0;
+  const double qx = ty * e1.z - tz * e1.y;
+  const double qy = tz * e1.x - tx * e1.z;
+  const double qz = tx * e1.y - ty * e1.x;
+  const double v = (d.x * qx + d.y * qy + d.z * qz) * inv;
+  if (v < -1e-9 || u + v > 1.0 + 1e-9) return -1.0;
+  const double t = (e2.x * qx + e2.y * qy + e2.z * qz) * inv;
+  if (t <= 0.0) return -1.0;
+  return t;
+}
+
+__device__ inline double ray_sph(V3 o, V3 d, V3 c, double r) {
+  const double lx = o.x - c.x, ly = o.y - c.y, lz = o.z - c.z;
+  const double b = d.x * lx + d.y * ly + d.z * lz;
+  const double cc = lx * lx + ly * ly + lz * lz - r * r;
+  const double disc = b * b - cc;
+  if (disc < 0.0) return -1.0;
+  const double sq = sqrt(disc);
+  const double t0 = -b - sq;
+  if (t0 > 0.0) return t0;
+  const double t1 = -b + sq;
+  if (t1 > 0.0) return t1;
+  return -1.0;
+}
+
+__device__ inline bool box_hit(V3 o, V3 d, const double* lo, const double* hi, double t_best) {
+  double t0 = 0.0, t1 = t_best;
+  const double oo[3] = {o.x, o.y, o.z}, dd[3] = {d.x, d.y, d.z};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (dd[a] > -1e-30 && dd[a] < 1e-30) {
+      if (oo[a] < lo[a] || oo[a] > hi[a]) return false;
+    } else {
+      const double inv = 1.0 / dd[a];
+      double ta = (lo[a] - oo[a]) * inv;
+      double tb = (hi[a] - oo[a]) * inv;
+      if (ta > tb) {
+        const double s = ta;
+        ta = tb;
+        tb = s;
+      }
+      if (ta > t0) t0 = ta;
+      if (tb < t1) t1 = tb;
+      if (t0 > t1) return false;
+    }
+  }
+  return true;
+}
+
+struct Hit {
+  int kind, prim, mid;
+  double t;
+  V3 p, n;
+};
+
+// intersect_bvh (geometry.py:153-202): nearest hit with t in (eps, t_max).
+// any_hit stops at the first accepted primitive (occlusion queries only
+// need the boolean, which is identical).
+template <bool AnyHit>
+__device__ inline Hit intersect(const nirc_scene_t& s, V3 o, V3 d, double t_max) {
+  const double eps = s.eps;
+  double best = t_max;
+  int kind = -1, prim = -1;
+  int stack[64];
+  int top = 0;
+  stack[top++] = 0;
+  while (top > 0) {
+    const int node = stack[--top];
+    if (!box_hit(o, d, s.bvh_lo + 3 * node, s.bvh_hi + 3 * node, best)) continue;
+    const int count = s.bvh_b[node];
+    if (count > 0) {
+      const int first = s.bvh_a[node];
+      for (int k = first; k < first + count; ++k) {
+        const int pid = s.bvh_prim[k];
+        if (pid < s.n_tri) {
+          const double t = ray_tri(o, d, ld3(s.tri_v0, pid), ld3(s.tri_e1, pid),
+                                   ld3(s.tri_e2, pid));
+          if (t > eps && t < best) {
+            best = t;
+            kind = 0;
+            prim = pid;
+          }
+        } else {
+          const int j = pid - s.n_tri;
+          const double t = ray_sph(o, d, ld3(s.sph_c, j), s.sph_r[j]);
+          if (t > eps && t < best) {
+            best = t;
+            kind = 1;
+            prim = j;
+          }
+        }
+        if (AnyHit && kind >= 0) {
+          Hit h;
+          h.kind = kind;
+          return h;
+        }
+      }
+    } else if (count == 0 && s.bvh_a[node] != node) {
+      stack[top++] = s.bvh_a[node];
+      stack[top++] = node + 1;
+    }
+  }
+  Hit h;
+  h.kind = kind;
+  h.prim = prim;
+  h.mid = -1;
+  h.t = -1.0;
+  if (kind < 0) return h;
+  h.t = best;
+  h.p = {o.x + d.x * best, o.y + d.y * best, o.z + d.z * best};
+  if (kind == 0) {
+    h.n = ld3(s.tri_ng, prim);
+    h.mid = s.tri_mat[prim];
+  } else {
+    const double inv = 1.0 / s.sph_r[prim];
+    const V3 c = ld3(s.sph_c, prim);
+    h.n = {(h.p.x - c.x) * inv, (h.p.y - c.y) * inv, (h.p.z - c.z) * inv};
+    h.mid = s.sph_mat[prim];
+  }
+  return h;
+}
+
+__device__ inline bool occluded(const nirc_scene_t& s, V3 o, V3 d, double t_max) {
+  return intersect<true>(s, o, d, t_max).kind >= 0;
+}
+
+// ------------------------------------------------------------- frames ---
+struct Cosine {
+  double x, y, z, pdf;
+};
+// core.py:57-65
+__device__ inline Cosine cosine_dir(double u1, double u2) {
+  const double r = sqrt(u1);
+  const double phi = TWO_PI * u2;
+  Cosine c;
+  c.x = r * cos(phi);
+  c.y = r * sin(phi);
+  const double t = 1.0 - u1;
+  c.z = sqrt(t > 0.0 ? t : 0.0);
+  c.pdf = c.z * INV_PI;
+  return c;
+}
+
+// ---------------------------------------------------------------- BSDF --
+__device__ inline double ggx_d(double alpha, double ch) {
+  const double a2 = alpha * alpha;
+  const double d = ch * ch * (a2 - 1.0) + 1.0;
+  return a2 / (PI * d * d);
+}
+__device__ inline double ggx_g1(double alpha, double cv) {
+  const double a2 = alpha * alpha;
+  return 2.0 * cv / (cv + sqrt(a2 + (1.0 - a2) * cv * cv));
+}
+
+// bsdf_eval_s (bsdf.py:38-72)
+__device__ inline V3 bsdf_eval(int kind, V3 a, double rough, V3 n, V3 wo, V3 wi) {
+  const double ci = n.x * wi.x + n.y * wi.y + n.z * wi.z;
+  const double co = n.x * wo.x + n.y * wo.y + n.z * wo.z;
+  if (ci <= 0.0 || co <= 0.0 || kind == MAT_MIRROR) return {0.0, 0.0, 0.0};
+  if (kind == MAT_LAMBERT) return {a.x * INV_PI, a.y * INV_PI, a.z * INV_PI};
+  const double alpha = rough > ALPHA_MIN ? rough : ALPHA_MIN;
+  double hx = wi.x + wo.x, hy = wi.y + wo.y, hz = wi.z + wo.z;
+  const double hl = sqrt(hx * hx + hy * hy + hz * hz);
+  if (hl < 1e-12) return {0.0, 0.0, 0.0};
+  hx /= hl;
+  hy /= hl;
+  hz /= hl;
+  const double ch = n.x * hx + n.y * hy + n.z * hz;
+  if (ch <= 0.0) return {0.0, 0.0, 0.0};
+  const double D = ggx_d(alpha, ch);
+  const double G = ggx_g1(alpha, ci) * ggx_g1(alpha, co);
+  double cd = wo.x * hx + wo.y * hy + wo.z * hz;
+  if (cd < 0.0) cd = 0.0;
+  double s5 = (1.0 - cd);
+  s5 = s5 * s5 * s5 * s5 * s5;
+  const double scale = D * G / (4.0 * ci * co);
+  return {(a.x + (1.0 - a.x) * s5) * scale, (a.y + (1.0 - a.y) * s5) * scale,
+          (a.z + (1.0 - a.z) * s5) * scale};
+}
+
+// bsdf_pdf_s (bsdf.py:75-100)
+__device__ inline double bsdf_pdf(int kind, double rough, V3 n, V3 wo, V3 wi) {
+  const double ci = n.x * wi.x + n.y * wi.y + n.z * wi.z;
+  const double co = n.x * wo.x + n.y * wo.y + n.z * wo.z;
+  if (ci <= 0.0 || co <= 0.0 || kind == MAT_MIRROR) return 0.0;
+  if (kind == MAT_LAMBERT) return ci * INV_PI;
+  const double alpha = rough > ALPHA_MIN ? rough : ALPHA_MIN;
+  double hx = wi.x + wo.x, hy = wi.y + wo.y, hz = wi.z + wo.z;
+  const double hl = sqrt(hx * hx + hy * hy + hz * hz);
+  if (hl < 1e-12) return 0.0;
+  hx /= hl;
+  hy /= hl;
+  hz /= hl;
+  const double ch = n.x * hx + n.y * hy + n.z * hz;
+  if (ch <= 0.0) return 0.0;
+  const double cd = wo.x * hx + wo.y * hy + wo.z * hz;
+  if (cd < 1e-9) return 0.0;
+  return ggx_d(alpha, ch) * ch / (4.0 * cd);
+}
+
+struct BsdfSample {
+  V3 wi;
+  double pdf;
+  V3 f;
+  int delta;
+};
+
+// bsdf_sample_s (bsdf.py:103-154)
+__device__ inline BsdfSample bsdf_sample(int kind, V3 a, double rough, V3 n, V3 wo, double u1,
+                                         double u2) {
+  BsdfSample r;
+  r.wi = {0.0, 0.0, 1.0};
+  r.pdf = 0.0;
+  r.f = {0.0, 0.0, 0.0};
+  r.delta = 0;
+  if (kind == MAT_MIRROR) {
+    r.delta = 1;
+    const double co = n.x * wo.x + n.y * wo.y + n.z * wo.z;
+    const V3 wi = {2.0 * co * n.x - wo.x, 2.0 * co * n.y - wo.y, 2.0 * co * n.z - wo.z};
+    const double ci = n.x * wi.x + n.y * wi.y + n.z * wi.z;
+    if (ci < 1e-9) return r;
+    const double inv = 1.0 / ci;
+    r.wi = wi;
+    r.pdf = 1.0;
+    r.f = {a.x * inv, a.y * inv, a.z * inv};
+    return r;
+  }
+  if (kind == MAT_LAMBERT) {
+    const Onb b = onb(n.x, n.y, n.z);
+    const Cosine c = cosine_dir(u1, u2);
+    const V3 wi = {b.tx * c.x + b.bx * c.y + n.x * c.z, b.ty * c.x + b.by * c.y + n.y * c.z,
+                   b.tz * c.x + b.bz * c.y + n.z * c.z};
+    const double co = n.x * wo.x + n.y * wo.y + n.z * wo.z;
+    if (co <= 0.0 || c.pdf <= 0.0) return r;
+    r.wi = wi;
+    r.pdf = c.pdf;
+    r.f = {a.x * INV_PI, a.y * INV_PI, a.z * INV_PI};
+    return r;
+  }
+  const double alpha = rough > ALPHA_MIN ? rough : ALPHA_MIN;
+  const double ch = sqrt((1.0 - u1) / (1.0 + (alpha * alpha - 1.0) * u1));
+  const double sh = sqrt(ch < 1.0 ? 1.0 - ch * ch : 0.0);
+  const double phi = TWO_PI * u2;
+  const Onb b = onb(n.x, n.y, n.z);
+  const double hlx = sh * cos(phi), hly = sh * sin(phi);
+  const V3 h = {b.tx * hlx + b.bx * hly + n.x * ch, b.ty * hlx + b.by * hly + n.y * ch,
+                b.tz * hlx + b.bz * hly + n.z * ch};
+  const double cd = wo.x * h.x + wo.y * h.y + wo.z * h.z;
+  if (cd < 1e-9) return r;
+  const V3 wi = {2.0 * cd * h.x - wo.x, 2.0 * cd * h.y - wo.y, 2.0 * cd * h.z - wo.z};
+  const double pdf = ggx_d(alpha, ch) * ch / (4.0 * cd);
+  const V3 f = bsdf_eval(kind, a, rough, n, wo, wi);
+  const double ci = n.x * wi.x + n.y * wi.y + n.z * wi.z;
+  if (ci <= 0.0 || pdf <= 0.0) return r;
+  r.wi = wi;
+  r.pdf = pdf;
+  r.f = f;
+  return r;
+}
+
+// -------------------------------------------------------------- lights --
+// env_eval_s (lights.py:20-58)
+__device__ inline V3 env_eval(const nirc_scene_t& s, V3 d) {
+  if (s.env_kind == ENV_NONE) return {0.0, 0.0, 0.0};
+  if (s.env_kind == ENV_CONSTANT) return {s.env_c0[0], s.env_c0[1], s.env_c0[2]};
+  if (s.env_kind == ENV_SKY) {
+    double t;
+    const double* b;
+    if (d.y >= 0.0) {
+      t = d.y;
+      b = s.env_c0;
+    } else {
+      t = -d.y;
+      b = s.env_c2;
+    }
+    const double* a = s.env_c1;
+    return {a[0] + (b[0] - a[0]) * t, a[1] + (b[1] - a[1]) * t, a[2] + (b[2] - a[2]) * t};
+  }
+  double cy = d.y;
+  if (cy > 1.0) cy = 1.0;
+  else if (cy < -1.0) cy = -1.0;
+  const double v = acos(cy) / PI;
+  const double u = 0.5 + atan2(d.x, -d.z) / TWO_PI;
+  int col = (int)(u * s.env_w);
+  int row = (int)(v * s.env_h);
+  if (col >= s.env_w) col = s.env_w - 1;
+  if (col < 0) col = 0;
+  if (row >= s.env_h) row = s.env_h - 1;
+  if (row < 0) row = 0;
+  const double* px = s.env_img + 3 * ((int64_t)row * s.env_w + col);
+  return {px[0], px[1], px[2]};
+}
+
+struct LightSample {
+  V3 wi;
+  double dist;
+  V3 e;
+  double pdf;
+  int src;
+};
+
+// sample_light_s (lights.py:61-135)
+__device__ inline LightSample sample_light(const nirc_scene_t& s, V3 p, V3 ns, double u_pick,
+                                          double u1, double u2) {
+  LightSample r;
+  r.wi = {0.0, 0.0, 1.0};
+  r.dist = 0.0;
+  r.e = {0.0, 0.0, 0.0};
+  r.pdf = 0.0;
+  r.src = -1;
+  const int n = s.n_light;
+  if (n == 0) return r;
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) / 2;
+    if (s.lt_cdf[mid] < u_pick) lo = mid + 1;
+    else hi = mid;
+  }
+  const double q = s.lt_q[lo];
+  const int kind = s.lt_kind[lo];
+  const int prim = s.lt_prim[lo];
+  if (kind == LIGHT_ENV) {
+    const Onb b = onb(ns.x, ns.y, ns.z);
+    const Cosine c = cosine_dir(u1, u2);
+    const V3 wi = {b.tx * c.x + b.bx * c.y + ns.x * c.z, b.ty * c.x + b.by * c.y + ns.y * c.z,
+                   b.tz * c.x + b.bz * c.y + ns.z * c.z};
+    r.wi = wi;
+    r.dist = T_FAR;
+    r.e = env_eval(s, wi);
+    r.pdf = q * c.pdf;
+    r.src = LIGHT_ENV;
+    return r;
+  }
+  V3 lp, ln;
+  double area;
+  int mid;
+  if (kind == LIGHT_TRI) {
+    const double r1 = sqrt(u1);
+    const double b1 = r1 * (1.0 - u2);
+    const double b2 = r1 * u2;
+    const V3 v0 = ld3(s.tri_v0, prim), e1 = ld3(s.tri_e1, prim), e2 = ld3(s.tri_e2, prim);
+    lp = {v0.x + e1.x * b1 + e2.x * b2, v0.y + e1.y * b1 + e2.y * b2,
+          v0.z + e1.z * b1 + e2.z * b2};
+    ln = ld3(s.tri_ng, prim);
+    area = s.tri_area[prim];
+    mid = s.tri_mat[prim];
+  } else {
+    const double z = 1.0 - 2.0 * u1;
+    const double sn = sqrt(z * z < 1.0 ? 1.0 - z * z : 0.0);
+    const double phi = TWO_PI * u2;
+    ln = {sn * cos(phi), sn * sin(phi), z};
+    const double rr = s.sph_r[prim];
+    const V3 c = ld3(s.sph_c, prim);
+    lp = {c.x + rr * ln.x, c.y + rr * ln.y, c.z + rr * ln.z};
+    area = FOUR_PI * rr * rr;
+    mid = s.sph_mat[prim];
+  }
+  const double dx = lp.x - p.x, dy = lp.y - p.y, dz = lp.z - p.z;
+  const double d2 = dx * dx + dy * dy + dz * dz;
+  const double dist = sqrt(d2);
+  if (dist < 1e-9) return r;
+  const V3 wi = {dx / dist, dy / dist, dz / dist};
+  double cos_l = -(wi.x * ln.x + wi.y * ln.y + wi.z * ln.z);
+  if (cos_l < 0.0) cos_l = -cos_l;
+  if (cos_l < 1e-9 || area < 1e-12) return r;
+  r.wi = wi;
+  r.dist = dist;
+  r.e = ld3(s.mat_emit, mid);
+  r.pdf = q * d2 / (area * cos_l);
+  r.src = kind;
+  return r;
+}
+
+// nee_pdf_for_hit_s (lights.py:138-159)
+__device__ inline double nee_pdf_for_hit(const nirc_scene_t& s, int hit_kind, int prim, double t,
+                                         V3 wi, V3 ln) {
+  double q, area;
+  if (hit_kind == 0) {
+    q = s.tri_lq[prim];
+    area = s.tri_area[prim];
+  } else {
+    q = s.sph_lq[prim];
+    area = FOUR_PI * s.sph_r[prim] * s.sph_r[prim];
+  }
+  if (q <= 0.0 || area < 1e-12) return 0.0;
+  double cos_l = -(wi.x * ln.x + wi.y * ln.y + wi.z * ln.z);
+  if (cos_l < 0.0) cos_l = -cos_l;
+  if (cos_l < 1e-9) return 0.0;
+  return q * t * t / (area * cos_l);
+}
+
+// nee_pdf_for_env_s (lights.py:162-169)
+__device__ inline double nee_pdf_for_env(const nirc_scene_t& s, V3 ns, V3 wi) {
+  if (s.env_q <= 0.0) return 0.0;
+  const double c = ns.x * wi.x + ns.y * wi.y + ns.z * wi.z;
+  if (c <= 0.0) return 0.0;
+  return s.env_q * c / PI;
+}
+
+// camera_ray_s (lights.py:205-216)
+__device__ inline void camera_ray(const double* cam, int ix, int iy, double u, double v, V3& o,
+                                  V3& d) {
+  const double w = cam[14], h = cam[15];
+  const double sx = ((ix + u) / w * 2.0 - 1.0) * cam[12] * cam[13];
+  const double sy = (1.0 - (iy + v) / h * 2.0) * cam[12];
+  const double dx = cam[3] * sx + cam[6] * sy + cam[9];
+  const double dy = cam[4] * sx + cam[7] * sy + cam[10];
+  const double dz = cam[5] * sx + cam[8] * sy + cam[11];
+  const double inv = 1.0 / sqrt(dx * dx + dy * dy + dz * dz);
+  o = {cam[0], cam[1], cam[2]};
+  d = {dx * inv, dy * inv, dz * inv};
+}
+
+// nee_contrib_s (kernels.py:44-82)
+__device__ inline V3 nee_contrib(const nirc_scene_t& s, V3 p, V3 ns, V3 gn, int mkind, V3 alb,
+                                 double rough, V3 wo, double u_pick, double u1, double u2,
+                                 int terminal) {
+  const V3 zero = {0.0, 0.0, 0.0};
+  if (s.n_light == 0) return zero;
+  const LightSample L = sample_light(s, p, ns, u_pick, u1, u2);
+  if (L.pdf <= 0.0) return zero;
+  const double cs = L.wi.x * ns.x + L.wi.y * ns.y + L.wi.z * ns.z;
+  if (cs <= 0.0) return zero;
+  const V3 f = bsdf_eval(mkind, alb, rough, ns, wo, L.wi);
+  if (f.x == 0.0 && f.y == 0.0 && f.z == 0.0) return zero;
+  const double sgn = (gn.x * L.wi.x + gn.y * L.wi.y + gn.z * L.wi.z) > 0.0 ? 1.0 : -1.0;
+  const V3 o = {p.x + sgn * s.eps * gn.x, p.y + sgn * s.eps * gn.y, p.z + sgn * s.eps * gn.z};
+  const double t_lim = L.dist - 2.0 * s.eps;
+  if (t_lim <= 0.0) return zero;
+  if (occluded(s, o, L.wi, t_lim)) return zero;
+  double w;
+  if (terminal != 0) {
+    w = 1.0;
+  } else {
+    const double pb = bsdf_pdf(mkind, rough, ns, wo, L.wi);
+    w = L.pdf / (L.pdf + pb);
+  }
+  const double sc = w * cs / L.pdf;
+  return {f.x * L.e.x * sc, f.y * L.e.y * sc, f.z * L.e.z * sc};
+}
+
+}  // namespace pt
+}  // namespace nirc

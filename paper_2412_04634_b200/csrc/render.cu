@@ -1,0 +1,917 @@
+// Two-level (MLMC) frame estimator and training-record collection on
+// sm_100a.  Compiled with -fmad=false: the fp64 path walks follow the
+// reference's operation order.
+//
+// Frame pipeline (nirc_render, one stream, no host sync):
+//   K5  k_trace       one thread per (pixel, sample): fp64 path tracer
+//                     (trace_sample MODE_PT/MODE_TL, kernels.py:451-608).
+//                     The network output never steers the walk, so the
+//                     two-level terms are DEFERRED: each cache vertex emits a
+//                     record (surface, T, key/base, T', w_cont) and the walk
+//                     continues exactly like plain PT.
+//   K1+K2+K4  k_infer_tc  persistent tcgen05 kernel over cache-vertex tiles:
+//                     shared surface hash encoding once per vertex, N_c BSDF
+//                     directions + the residual direction per vertex encoded
+//                     straight into the SMEM A tile, 3xTF32 MLP, and the MLMC
+//                     combine  T*L_c - T'*n(w_cont)  reduced per vertex in
+//                     deterministic order (cache_lc_s, kernels.py:424-448).
+//   k_accumulate      per pixel: r = PT sum + cache terms; img += r,
+//                     img2 += r*r, term += vertices (render_kernel :753-759).
+#include "common.cuh"
+#include "pt_common.cuh"
+#include "tc_mlp.cuh"
+
+namespace nirc {
+
+int sm_count();
+int pack_weights(const nirc_spec_t& sp, const tc::TcNet& net, const float* theta, cudaStream_t s,
+                 uint8_t** img, float** bias);
+int tc_groups_for(const tc::TcNet& net, uint32_t extra_per_cta);
+bool default_layout(const nirc_spec_t& sp);
+
+using pt::V3;
+
+// One two-level cache vertex (the deferred work of kernels.py:559-601).
+struct CacheVertex {
+  double pos[3], ns[3], alb[3], rough;
+  double wo[3];
+  double T[3];    // throughput when the cache integral is added
+  double Tp[3];   // post-roulette, post-bsdf throughput T' (residual weight)
+  double wc[3];   // continuation direction w_cont
+  uint64_t key;
+  int32_t base, ncq, mkind, has_res;
+  int64_t slot;   // sample * max_cv + cu
+};
+
+struct TraceOut {
+  double* acc;       // (n_samples, 3)
+  int32_t* term;     // (n_samples,)
+  CacheVertex* cv;   // capacity n_samples * max_cv
+  unsigned long long* counters;  // [0] cache vertices, [1] executed queries
+};
+
+// trace_sample for MODE_PT / MODE_TL with deferred cache terms.
+__global__ void k_trace(nirc_scene_t scn, const double* __restrict__ cam, nirc_render_cfg_t cfg,
+                        TraceOut out) {
+  const int W = cfg.width;
+  const int64_t nsamp = (int64_t)(cfg.row1 - cfg.row0) * W * cfg.spp;
+  const int64_t sid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (sid >= nsamp) return;
+  const int s = (int)(sid % cfg.spp);
+  const int64_t lp = sid / cfg.spp;
+  const int ix = (int)(lp % W);
+  const int iy = cfg.row0 + (int)(lp / W);
+  const int64_t pix = (int64_t)iy * W + ix;
+  const uint64_t key = stream_key(cfg.seed, P_RENDER, cfg.frame, (uint64_t)pix, (uint64_t)s);
+  const double jx = rand_uniform(key, DIM_JITTER_X);
+  const double jy = rand_uniform(key, DIM_JITTER_Y);
+  V3 o, d;
+  pt::camera_ray(cam, ix, iy, jx, jy, o, d);
+
+  double ar = 0.0, ag = 0.0, ab = 0.0;
+  double tr = 1.0, tg = 1.0, tb = 1.0;
+  double prev_pdf = -1.0;
+  V3 lns = {0.0, 0.0, 0.0};
+  int cu = 0, term = 0;
+  const bool tl = cfg.mode == 1 && cfg.cache_on == 1;
+  for (int v = 0; v < pt::MAXB; ++v) {
+    const pt::Hit h = pt::intersect<false>(scn, o, d, pt::T_FAR);
+    if (h.kind < 0) {
+      if (scn.env_kind != pt::ENV_NONE) {
+        const V3 e = pt::env_eval(scn, d);
+        double w = 1.0;
+        if (prev_pdf >= 0.0) {
+          const double pn = pt::nee_pdf_for_env(scn, lns, d);
+          w = prev_pdf / (prev_pdf + pn);
+        }
+        ar += tr * w * e.x;
+        ag += tg * w * e.y;
+        ab += tb * w * e.z;
+      }
+      break;
+    }
+    term = v + 1;
+    const V3 wo = {-d.x, -d.y, -d.z};
+    const double flip = (h.n.x * wo.x + h.n.y * wo.y + h.n.z * wo.z) >= 0.0 ? 1.0 : -1.0;
+    const V3 ns = {h.n.x * flip, h.n.y * flip, h.n.z * flip};
+    const V3 em = pt::ld3(scn.mat_emit, h.mid);
+    if (em.x > 0.0 || em.y > 0.0 || em.z > 0.0) {
+      double w = 1.0;
+      if (prev_pdf >= 0.0) {
+        const double pn = pt::nee_pdf_for_hit(scn, h.kind, h.prim, h.t, d, h.n);
+        w = prev_pdf / (prev_pdf + pn);
+      }
+      ar += tr * w * em.x;
+      ag += tg * w * em.y;
+      ab += tb * w * em.z;
+    }
+    const int mkind = scn.mat_kind[h.mid];
+    const V3 alb = pt::ld3(scn.mat_albedo, h.mid);
+    const double rough = scn.mat_rough[h.mid];
+    const int base = VERTEX_DIM_BASE + v * DIMS_PER_VERTEX;
+    if (mkind == pt::MAT_MIRROR) {  // delta vertex, kernels.py:520-548
+      double rr_div = 1.0;
+      if (v >= pt::RR_START) {
+        if (rand_uniform(key, base + OFF_RR) >= cfg.rr_survive) break;
+        rr_div = cfg.rr_survive;
+      }
+      const pt::BsdfSample b = pt::bsdf_sample(mkind, alb, rough, ns, wo,
+                                               rand_uniform(key, base + OFF_BSDF_U),
+                                               rand_uniform(key, base + OFF_BSDF_U + 1));
+      if (b.pdf <= 0.0) break;
+      const double ci = b.wi.x * ns.x + b.wi.y * ns.y + b.wi.z * ns.z;
+      if (ci <= 0.0) break;
+      const double inv = 1.0 / (b.pdf * rr_div);
+      tr *= b.f.x * ci * inv;
+      tg *= b.f.y * ci * inv;
+      tb *= b.f.z * ci * inv;
+      prev_pdf = -1.0;
+      const double sg = (h.n.x * b.wi.x + h.n.y * b.wi.y + h.n.z * b.wi.z) > 0.0 ? 1.0 : -1.0;
+      o = {h.p.x + sg * scn.eps * h.n.x, h.p.y + sg * scn.eps * h.n.y,
+           h.p.z + sg * scn.eps * h.n.z};
+      d = b.wi;
+      lns = ns;
+      continue;
+    }
+    // MODE_PT / MODE_TL (kernels.py:549-608)
+    const V3 q = pt::nee_contrib(scn, h.p, ns, h.n, mkind, alb, rough, wo,
+                                 rand_uniform(key, base + OFF_LIGHT_PICK),
+                                 rand_uniform(key, base + OFF_LIGHT_U),
+                                 rand_uniform(key, base + OFF_LIGHT_U + 1), 0);
+    ar += tr * q.x;
+    ag += tg * q.y;
+    ab += tb * q.z;
+    int pending = 0;
+    CacheVertex rec;
+    if (tl && rough >= cfg.rough_cut && cu < cfg.max_cv) {
+      const int ncq = cfg.nc[cu];
+      cu += 1;
+      if (ncq > 0) {
+        pending = 1;
+        rec.pos[0] = h.p.x; rec.pos[1] = h.p.y; rec.pos[2] = h.p.z;
+        rec.ns[0] = ns.x; rec.ns[1] = ns.y; rec.ns[2] = ns.z;
+        rec.alb[0] = alb.x; rec.alb[1] = alb.y; rec.alb[2] = alb.z;
+        rec.rough = rough;
+        rec.wo[0] = wo.x; rec.wo[1] = wo.y; rec.wo[2] = wo.z;
+        rec.T[0] = tr; rec.T[1] = tg; rec.T[2] = tb;
+        rec.key = key;
+        rec.base = base;
+        rec.ncq = ncq;
+        rec.mkind = mkind;
+        rec.has_res = 0;
+        rec.slot = sid * cfg.max_cv + (cu - 1);
+      }
+    }
+    bool cont = true;
+    double rr_div = 1.0;
+    if (v >= pt::RR_START) {
+      if (rand_uniform(key, base + OFF_RR) >= cfg.rr_survive) cont = false;
+      else rr_div = cfg.rr_survive;
+    }
+    pt::BsdfSample b;
+    double ci = 0.0;
+    if (cont) {
+      b = pt::bsdf_sample(mkind, alb, rough, ns, wo, rand_uniform(key, base + OFF_BSDF_U),
+                          rand_uniform(key, base + OFF_BSDF_U + 1));
+      if (b.pdf <= 0.0) cont = false;
+      else {
+        ci = b.wi.x * ns.x + b.wi.y * ns.y + b.wi.z * ns.z;
+        if (ci <= 0.0) cont = false;
+      }
+    }
+    if (cont) {
+      const double inv = 1.0 / (b.pdf * rr_div);
+      tr *= b.f.x * ci * inv;
+      tg *= b.f.y * ci * inv;
+      tb *= b.f.z * ci * inv;
+      if (pending) {
+        rec.has_res = 1;
+        rec.Tp[0] = tr; rec.Tp[1] = tg; rec.Tp[2] = tb;
+        rec.wc[0] = b.wi.x; rec.wc[1] = b.wi.y; rec.wc[2] = b.wi.z;
+      }
+    }
+    if (pending) {
+      if (!rec.has_res) {
+        rec.Tp[0] = rec.Tp[1] = rec.Tp[2] = 0.0;
+        rec.wc[0] = rec.wc[1] = 0.0;
+        rec.wc[2] = 1.0;
+      }
+      const unsigned long long idx = atomicAdd(out.counters, 1ull);
+      out.cv[idx] = rec;
+      atomicAdd(out.counters + 1, (unsigned long long)(rec.ncq + rec.has_res));
+    }
+    if (!cont) break;
+    prev_pdf = b.pdf;
+    const double sg = (h.n.x * b.wi.x + h.n.y * b.wi.y + h.n.z * b.wi.z) > 0.0 ? 1.0 : -1.0;
+    o = {h.p.x + sg * scn.eps * h.n.x, h.p.y + sg * scn.eps * h.n.y,
+         h.p.z + sg * scn.eps * h.n.z};
+    d = b.wi;
+    lns = ns;
+  }
+  out.acc[3 * sid] = ar;
+  out.acc[3 * sid + 1] = ag;
+  out.acc[3 * sid + 2] = ab;
+  out.term[sid] = term;
+}
+
+// ---------------------------------------------------------------------
+// Row of the amortised inference: direction + weights for query k of a
+// cache vertex (cache_lc_s, kernels.py:432-446) or its residual row.
+struct RowDir {
+  V3 wi;
+  double s;  // ci / pdf for cache rows
+  V3 f;
+  int kind;  // 0 invalid, 1 cache sample, 2 residual
+};
+
+__device__ inline RowDir row_direction(const CacheVertex& r, int k) {
+  RowDir o;
+  o.kind = 0;
+  o.wi = {0.0, 0.0, 1.0};
+  o.s = 0.0;
+  o.f = {0.0, 0.0, 0.0};
+  if (k < r.ncq) {
+    const V3 ns = {r.ns[0], r.ns[1], r.ns[2]};
+    const pt::BsdfSample b = pt::bsdf_sample(
+        r.mkind, {r.alb[0], r.alb[1], r.alb[2]}, r.rough, ns, {r.wo[0], r.wo[1], r.wo[2]},
+        rand_uniform(r.key, r.base + OFF_CACHE + 2 * k),
+        rand_uniform(r.key, r.base + OFF_CACHE + 2 * k + 1));
+    if (b.pdf <= 0.0 || b.delta == 1) return o;
+    const double ci = b.wi.x * ns.x + b.wi.y * ns.y + b.wi.z * ns.z;
+    if (ci <= 0.0) return o;
+    o.kind = 1;
+    o.wi = b.wi;
+    o.s = ci / b.pdf;
+    o.f = b.f;
+  } else if (k == r.ncq && r.has_res) {
+    o.kind = 2;
+    o.wi = {r.wc[0], r.wc[1], r.wc[2]};
+  }
+  return o;
+}
+
+// Encoded input of one inference row: shared surface features (24 floats
+// computed once per vertex), SH of the row direction in the scalar-path
+// order (encode_dir_into -> sh_eval_into, sh.py:36-76), aux block.
+__device__ inline void build_row(const nirc_spec_t& sp, const float* feat, const CacheVertex& r,
+                                 V3 wi, float* x) {
+#pragma unroll
+  for (int i = 0; i < 24; ++i) x[i] = feat[i];
+  sh_eval<false>(wi.x, wi.y, wi.z, 4, sp.sh_k, [&](int i, double v) {
+    x[24 + i] = __double2float_rn(v);
+  });
+  x[40] = __double2float_rn((r.ns[0] + 1.0) * 0.5);
+  x[41] = __double2float_rn((r.ns[1] + 1.0) * 0.5);
+  x[42] = __double2float_rn((r.ns[2] + 1.0) * 0.5);
+  x[43] = __double2float_rn(r.alb[0]);
+  x[44] = __double2float_rn(r.alb[1]);
+  x[45] = __double2float_rn(r.alb[2]);
+  x[46] = __double2float_rn(r.rough);
+  x[47] = 0.0f;
+}
+
+struct InferArgs {
+  const CacheVertex* cv;
+  const unsigned long long* counters;
+  double* result;  // (n_samples * max_cv, 3)
+  double* rowbuf;  // SIMT fallback only: per-row contributions (cap * R, 3)
+  int rows_per_vertex;  // R = max(nc) + 1
+  int verts_per_tile;   // S = 128 / R
+};
+
+constexpr int kMaxVertsPerTile = 64;
+
+template <int NG>
+__global__ void __launch_bounds__(NG * 128, 1)
+    k_infer_tc(nirc_spec_t sp, tc::TcNet net, tc::TcSmem L, const float* __restrict__ theta,
+               const uint8_t* __restrict__ wimg, const float* __restrict__ bias_g, InferArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint32_t tmem_base;
+  tc::tc_prologue(smem, L, net, NG, wimg, bias_g, tmem_base);
+  const uint32_t s0 = tc::smem_u32(smem);
+  const int group = threadIdx.x >> 7;
+  const int tg = threadIdx.x & 127;
+  const uint32_t a_hi = s0 + L.a_off + group * tc::kABufBytes;
+  const uint32_t a_lo = a_hi + tc::kAImageBytes;
+  const uint32_t mbar = s0 + L.bar_off + 8 * (1 + group);
+  const uint32_t tmem_d = tmem_base + group * 64;
+  const float* s_bias = reinterpret_cast<const float*>(smem + L.bias_off);
+  // per-group extra shared memory: surface features + row contributions
+  uint8_t* extra = smem + L.a_off + NG * tc::kABufBytes;
+  float* s_feat = reinterpret_cast<float*>(extra) + group * kMaxVertsPerTile * 24;
+  double* s_con = reinterpret_cast<double*>(extra + NG * kMaxVertsPerTile * 24 * 4) +
+                  group * 128 * 3;
+  const uint32_t T = 1u << sp.table_log2;
+  const int R = a.rows_per_vertex, S = a.verts_per_tile;
+  const int64_t nverts = (int64_t)a.counters[0];
+  const int64_t ntiles = (nverts + S - 1) / S;
+  uint32_t phase = 0;
+  for (int64_t tile = (int64_t)blockIdx.x * NG + group; tile < ntiles;
+       tile += (int64_t)gridDim.x * NG) {
+    const int64_t v0 = tile * S;
+    // 1) shared surface encoding: one thread per (vertex, level)
+    if (tg < S * 12) {
+      const int j = tg / 12, lvl = tg % 12;
+      const int64_t vid = v0 + j;
+      if (vid < nverts) {
+        const CacheVertex& r = a.cv[vid];
+        const float ux = norm_coord(r.pos[0], sp.bb_min[0], sp.bb_inv[0]);
+        const float uy = norm_coord(r.pos[1], sp.bb_min[1], sp.bb_inv[1]);
+        const float uz = norm_coord(r.pos[2], sp.bb_min[2], sp.bb_inv[2]);
+        const LevelCell c = level_cell(ux, uy, uz, sp.res[lvl]);
+        const float2 f = level_features2(theta + (size_t)lvl * T * 2, c, T - 1u);
+        s_feat[j * 24 + 2 * lvl] = f.x;
+        s_feat[j * 24 + 2 * lvl + 1] = f.y;
+      }
+    }
+    tc::named_bar_sync(1 + group, tc::kGroupThreads);
+    // 2) per-row direction sampling + SH straight into the A tile
+    const int j = tg / R, k = tg % R;
+    const int64_t vid = v0 + j;
+    RowDir rd;
+    rd.kind = 0;
+    float x[48];
+    if (j < S && vid < nverts) {
+      const CacheVertex& r = a.cv[vid];
+      rd = row_direction(r, k);
+      build_row(sp, s_feat + j * 24, r, rd.wi, x);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 48; ++i) x[i] = 0.0f;
+    }
+    tc::write_a_row<48>(a_hi, a_lo, tg, x);
+    float y[4];
+    tc::run_chain(net, s0 + L.w_off, s_bias, group, tg, a_hi, a_lo, tmem_d, mbar, phase, y);
+    // 3) MLMC combine: cache rows give n(w)*f*cos/pdf, the residual row n(w_cont)
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+    if (rd.kind == 1) {
+      c0 = (double)y[0] * rd.f.x * rd.s;
+      c1 = (double)y[1] * rd.f.y * rd.s;
+      c2 = (double)y[2] * rd.f.z * rd.s;
+    } else if (rd.kind == 2) {
+      c0 = (double)y[0];
+      c1 = (double)y[1];
+      c2 = (double)y[2];
+    }
+    s_con[3 * tg] = c0;
+    s_con[3 * tg + 1] = c1;
+    s_con[3 * tg + 2] = c2;
+    tc::named_bar_sync(1 + group, tc::kGroupThreads);
+    if (tg < S && v0 + tg < nverts) {
+      const CacheVertex& r = a.cv[v0 + tg];
+      double sr = 0.0, sg = 0.0, sb = 0.0;
+      for (int kk = 0; kk < r.ncq; ++kk) {  // kernels.py:444-446, k order
+        sr += s_con[3 * (tg * R + kk)];
+        sg += s_con[3 * (tg * R + kk) + 1];
+        sb += s_con[3 * (tg * R + kk) + 2];
+      }
+      const double inv = 1.0 / r.ncq;
+      double o0 = r.T[0] * (sr * inv), o1 = r.T[1] * (sg * inv), o2 = r.T[2] * (sb * inv);
+      if (r.has_res) {  // kernels.py:593-601
+        const double* q = s_con + 3 * (tg * R + r.ncq);
+        o0 -= r.Tp[0] * q[0];
+        o1 -= r.Tp[1] * q[1];
+        o2 -= r.Tp[2] * q[2];
+      }
+      a.result[3 * r.slot] = o0;
+      a.result[3 * r.slot + 1] = o1;
+      a.result[3 * r.slot + 2] = o2;
+    }
+    tc::named_bar_sync(1 + group, tc::kGroupThreads);
+  }
+  tc::tc_epilogue(tmem_base, NG);
+}
+
+// Generic-shape fallback of the same stage (any NetSpec): one thread per
+// row, weights in shared memory, fp32 SIMT; rows are reduced per vertex by
+// k_combine_rows in the same k order.
+__global__ void k_infer_simt(nirc_spec_t sp, const float* __restrict__ theta, InferArgs a) {
+  extern __shared__ float wsm[];
+  const int np = (int)(sp.theta_len - sp.grid_len);
+  for (int i = threadIdx.x; i < np; i += blockDim.x) wsm[i] = theta[sp.grid_len + i];
+  __syncthreads();
+  const int64_t nverts = (int64_t)a.counters[0];
+  const int R = a.rows_per_vertex;
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t vid = row / R;
+  const int k = (int)(row % R);
+  if (vid >= nverts) return;
+  const CacheVertex& r = a.cv[vid];
+  const RowDir rd = row_direction(r, k);
+  double* out = a.rowbuf + 3 * row;
+  out[0] = out[1] = out[2] = 0.0;
+  if (rd.kind == 0) return;
+  float act[2][136];
+  float* x = act[0];
+  const int F = sp.feats;
+  const uint32_t T = 1u << sp.table_log2;
+  const float ux = norm_coord(r.pos[0], sp.bb_min[0], sp.bb_inv[0]);
+  const float uy = norm_coord(r.pos[1], sp.bb_min[1], sp.bb_inv[1]);
+  const float uz = norm_coord(r.pos[2], sp.bb_min[2], sp.bb_inv[2]);
+  for (int lvl = 0; lvl < sp.levels; ++lvl) {
+    const LevelCell c = level_cell(ux, uy, uz, sp.res[lvl]);
+    for (int f = 0; f < F; ++f) {
+      float acc = 0.0f;
+      for (int cc = 0; cc < 8; ++cc)
+        acc = __fadd_rn(acc, __fmul_rn(corner_weight(c, cc),
+                                       theta[((size_t)lvl * T + corner_hash(c, cc, T - 1u)) * F + f]));
+      x[lvl * F + f] = acc;
+    }
+  }
+  const int g = sp.levels * F;
+  sh_eval<false>(rd.wi.x, rd.wi.y, rd.wi.z, sp.bands, sp.sh_k,
+                 [&](int i, double v) { x[g + i] = __double2float_rn(v); });
+  const int a0 = g + sp.bands * sp.bands;
+  for (int i = 0; i < 3; ++i) x[a0 + i] = __double2float_rn((r.ns[i] + 1.0) * 0.5);
+  for (int i = 0; i < 3; ++i) x[a0 + 3 + i] = __double2float_rn(r.alb[i]);
+  x[a0 + 6] = __double2float_rn(r.rough);
+  int cur = 0;
+  for (int l = 0; l < sp.n_layers; ++l) {
+    const int din = sp.dims[l], dout = sp.dims[l + 1];
+    const float* w = wsm + (sp.w_off[l] - sp.grid_len);
+    const float* bias = wsm + (sp.b_off[l] - sp.grid_len);
+    const bool last = l == sp.n_layers - 1;
+    for (int jj = 0; jj < dout; ++jj) {
+      float acc = 0.0f;
+      for (int i = 0; i < din; ++i) acc = fmaf(act[cur][i], w[jj * din + i], acc);
+      const float z = acc + bias[jj];
+      act[1 - cur][jj] =
+          (!last || sp.out_act == 0) ? (z > 0.0f ? z : 0.0f) : 1.0f / (1.0f + expf(-z));
+    }
+    cur = 1 - cur;
+  }
+  const float* y = act[cur];
+  if (rd.kind == 1) {
+    out[0] = (double)y[0] * rd.f.x * rd.s;
+    out[1] = (double)y[1] * rd.f.y * rd.s;
+    out[2] = (double)y[2] * rd.f.z * rd.s;
+  } else {
+    out[0] = y[0];
+    out[1] = y[1];
+    out[2] = y[2];
+  }
+}
+
+__global__ void k_combine_rows(InferArgs a) {
+  const int64_t vid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (vid >= (int64_t)a.counters[0]) return;
+  const CacheVertex& r = a.cv[vid];
+  const int R = a.rows_per_vertex;
+  const double* rb = a.rowbuf + 3 * vid * R;
+  double sr = 0.0, sg = 0.0, sb = 0.0;
+  for (int k = 0; k < r.ncq; ++k) {
+    sr += rb[3 * k];
+    sg += rb[3 * k + 1];
+    sb += rb[3 * k + 2];
+  }
+  const double inv = 1.0 / r.ncq;
+  double o0 = r.T[0] * (sr * inv), o1 = r.T[1] * (sg * inv), o2 = r.T[2] * (sb * inv);
+  if (r.has_res) {
+    o0 -= r.Tp[0] * rb[3 * r.ncq];
+    o1 -= r.Tp[1] * rb[3 * r.ncq + 1];
+    o2 -= r.Tp[2] * rb[3 * r.ncq + 2];
+  }
+  a.result[3 * r.slot] = o0;
+  a.result[3 * r.slot + 1] = o1;
+  a.result[3 * r.slot + 2] = o2;
+}
+
+// render_kernel accumulation (kernels.py:753-759): per pixel, samples in
+// order s = 0..spp-1; r = PT sum + sum over cache vertices (cu order).
+__global__ void k_accumulate(nirc_render_cfg_t cfg, const double* __restrict__ acc,
+                             const int32_t* __restrict__ term, const double* __restrict__ res,
+                             int use_res, double* __restrict__ img, double* __restrict__ img2,
+                             double* __restrict__ tsum) {
+  const int W = cfg.width;
+  const int64_t lp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (lp >= (int64_t)(cfg.row1 - cfg.row0) * W) return;
+  const int64_t pix = (int64_t)cfg.row0 * W + lp;
+  double i0 = img[3 * pix], i1 = img[3 * pix + 1], i2 = img[3 * pix + 2];
+  double q0 = img2[3 * pix], q1 = img2[3 * pix + 1], q2 = img2[3 * pix + 2];
+  double ts = tsum[pix];
+  for (int s = 0; s < cfg.spp; ++s) {
+    const int64_t sid = lp * cfg.spp + s;
+    double r = acc[3 * sid], g = acc[3 * sid + 1], b = acc[3 * sid + 2];
+    if (use_res) {
+      for (int c = 0; c < cfg.max_cv; ++c) {
+        const double* q = res + 3 * (sid * cfg.max_cv + c);
+        r += q[0];
+        g += q[1];
+        b += q[2];
+      }
+    }
+    i0 += r;
+    i1 += g;
+    i2 += b;
+    q0 += r * r;
+    q1 += g * g;
+    q2 += b * b;
+    ts += term[sid];
+  }
+  img[3 * pix] = i0;
+  img[3 * pix + 1] = i1;
+  img[3 * pix + 2] = i2;
+  img2[3 * pix] = q0;
+  img2[3 * pix + 1] = q1;
+  img2[3 * pix + 2] = q2;
+  tsum[pix] = ts;
+}
+
+// ---------------------------------------------------------------------
+// Training records: walk_record (kernels.py:85-286) driven by
+// collect_paths_kernel (:289-311).  Pass 1 walks every path, keeps its
+// per-vertex rows in a vertex-major staging area and runs the backward
+// sweep; a single-CTA scan turns per-path record counts into offsets; pass 3
+// compacts the records in (path, vertex) order -- the reference's row order.
+struct Stage {
+  // vertex-major: field[v * count + p]
+  double *pos, *ns, *alb, *rough, *wi, *pdf, *tgt, *tfull;
+  uint8_t* keep;
+  int32_t* nrec;   // per path
+  int32_t* nvert;  // per path
+  int64_t count;
+};
+
+__global__ void k_walk_record(nirc_scene_t scn, const double* __restrict__ cam, uint64_t seed,
+                              uint64_t frame, Stage st) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= st.count) return;
+  const int64_t C = st.count;
+  const uint64_t key = stream_key(seed, P_TRAIN, frame, (uint64_t)p, 0);
+  const double w = cam[14], h = cam[15];
+  const double sx = rand_uniform(key, DIM_JITTER_X) * w;
+  const double sy = rand_uniform(key, DIM_JITTER_Y) * h;
+  const int ix = (int)sx, iy = (int)sy;
+  V3 o, d;
+  pt::camera_ray(cam, ix, iy, sx - ix, sy - iy, o, d);
+  // per-vertex backward-sweep inputs live in local memory
+  double mise[pt::MAXB][3], emit[pt::MAXB][3], nee[pt::MAXB][3], fcp[pt::MAXB][3];
+  int n = 0, esc = 0;
+  double env_m[3] = {0.0, 0.0, 0.0}, env_r[3] = {0.0, 0.0, 0.0};
+  double prev_pdf = -1.0;
+  V3 lns = {0.0, 0.0, 0.0};
+  for (int v = 0; v < pt::MAXB; ++v) {
+    const pt::Hit hh = pt::intersect<false>(scn, o, d, pt::T_FAR);
+    if (hh.kind < 0) {
+      if (scn.env_kind != pt::ENV_NONE) {
+        const V3 e = pt::env_eval(scn, d);
+        env_r[0] = e.x; env_r[1] = e.y; env_r[2] = e.z;
+        double wgt = 1.0;
+        if (prev_pdf >= 0.0) {
+          const double pn = pt::nee_pdf_for_env(scn, lns, d);
+          wgt = prev_pdf / (prev_pdf + pn);
+        }
+        env_m[0] = wgt * e.x; env_m[1] = wgt * e.y; env_m[2] = wgt * e.z;
+      }
+      esc = 1;
+      break;
+    }
+    const V3 wo = {-d.x, -d.y, -d.z};
+    const double flip = (hh.n.x * wo.x + hh.n.y * wo.y + hh.n.z * wo.z) >= 0.0 ? 1.0 : -1.0;
+    const V3 ns = {hh.n.x * flip, hh.n.y * flip, hh.n.z * flip};
+    const V3 em = pt::ld3(scn.mat_emit, hh.mid);
+    if (em.x > 0.0 || em.y > 0.0 || em.z > 0.0) {
+      double wgt = 1.0;
+      if (prev_pdf >= 0.0) {
+        const double pn = pt::nee_pdf_for_hit(scn, hh.kind, hh.prim, hh.t, d, hh.n);
+        wgt = prev_pdf / (prev_pdf + pn);
+      }
+      mise[v][0] = wgt * em.x; mise[v][1] = wgt * em.y; mise[v][2] = wgt * em.z;
+      emit[v][0] = em.x; emit[v][1] = em.y; emit[v][2] = em.z;
+    } else {
+      mise[v][0] = mise[v][1] = mise[v][2] = 0.0;
+      emit[v][0] = emit[v][1] = emit[v][2] = 0.0;
+    }
+    const int mkind = scn.mat_kind[hh.mid];
+    const int delta = mkind == pt::MAT_MIRROR ? 1 : 0;
+    const V3 alb = pt::ld3(scn.mat_albedo, hh.mid);
+    const double rough = scn.mat_rough[hh.mid];
+    const int64_t at = (int64_t)v * C + p;
+    st.pos[3 * at] = hh.p.x; st.pos[3 * at + 1] = hh.p.y; st.pos[3 * at + 2] = hh.p.z;
+    st.ns[3 * at] = ns.x; st.ns[3 * at + 1] = ns.y; st.ns[3 * at + 2] = ns.z;
+    st.alb[3 * at] = alb.x; st.alb[3 * at + 1] = alb.y; st.alb[3 * at + 2] = alb.z;
+    st.rough[at] = rough;
+    const int base = VERTEX_DIM_BASE + v * DIMS_PER_VERTEX;
+    V3 q = {0.0, 0.0, 0.0};
+    if (delta == 0)
+      q = pt::nee_contrib(scn, hh.p, ns, hh.n, mkind, alb, rough, wo,
+                          rand_uniform(key, base + OFF_LIGHT_PICK),
+                          rand_uniform(key, base + OFF_LIGHT_U),
+                          rand_uniform(key, base + OFF_LIGHT_U + 1), 0);
+    nee[v][0] = q.x; nee[v][1] = q.y; nee[v][2] = q.z;
+    int alive = 1;
+    double rr_div = 1.0;
+    if (v >= pt::RR_START) {
+      if (rand_uniform(key, base + OFF_RR) >= pt::RR_SURVIVE) alive = 0;
+      else rr_div = pt::RR_SURVIVE;
+    }
+    int cont = 0;
+    double vpdf = 0.0;
+    V3 vwi = {0.0, 0.0, 0.0};
+    fcp[v][0] = fcp[v][1] = fcp[v][2] = 0.0;
+    if (alive == 1 && v < pt::MAXB - 1) {
+      const pt::BsdfSample b = pt::bsdf_sample(mkind, alb, rough, ns, wo,
+                                               rand_uniform(key, base + OFF_BSDF_U),
+                                               rand_uniform(key, base + OFF_BSDF_U + 1));
+      if (b.pdf > 0.0) {
+        const double ci = b.wi.x * ns.x + b.wi.y * ns.y + b.wi.z * ns.z;
+        if (ci > 0.0) {
+          const double inv = 1.0 / (b.pdf * rr_div);
+          vwi = b.wi;
+          vpdf = b.delta == 1 ? -1.0 : b.pdf;
+          fcp[v][0] = b.f.x * ci * inv;
+          fcp[v][1] = b.f.y * ci * inv;
+          fcp[v][2] = b.f.z * ci * inv;
+          prev_pdf = vpdf;
+          const double sg = (hh.n.x * b.wi.x + hh.n.y * b.wi.y + hh.n.z * b.wi.z) > 0.0 ? 1.0 : -1.0;
+          o = {hh.p.x + sg * scn.eps * hh.n.x, hh.p.y + sg * scn.eps * hh.n.y,
+               hh.p.z + sg * scn.eps * hh.n.z};
+          d = b.wi;
+          lns = ns;
+          cont = 1;
+        }
+      }
+    }
+    st.wi[3 * at] = vwi.x; st.wi[3 * at + 1] = vwi.y; st.wi[3 * at + 2] = vwi.z;
+    st.pdf[at] = vpdf;
+    st.keep[at] = (delta == 0 && vpdf > 0.0) ? 1 : 0;
+    n = v + 1;
+    if (cont == 0) break;
+  }
+  // backward sweep (kernels.py:249-277)
+  double lr = 0.0, lg = 0.0, lb = 0.0;
+  int nrec = 0;
+  for (int v = n - 1; v >= 0; --v) {
+    double cr, cg, cb, qr, qg, qb;
+    if (v == n - 1) {
+      cr = esc ? env_m[0] : 0.0; cg = esc ? env_m[1] : 0.0; cb = esc ? env_m[2] : 0.0;
+      qr = esc ? env_r[0] : 0.0; qg = esc ? env_r[1] : 0.0; qb = esc ? env_r[2] : 0.0;
+    } else {
+      cr = mise[v + 1][0] + lr; cg = mise[v + 1][1] + lg; cb = mise[v + 1][2] + lb;
+      qr = emit[v + 1][0] + lr; qg = emit[v + 1][1] + lg; qb = emit[v + 1][2] + lb;
+    }
+    const int64_t at = (int64_t)v * C + p;
+    st.tgt[3 * at] = cr; st.tgt[3 * at + 1] = cg; st.tgt[3 * at + 2] = cb;
+    st.tfull[3 * at] = qr; st.tfull[3 * at + 1] = qg; st.tfull[3 * at + 2] = qb;
+    lr = nee[v][0] + fcp[v][0] * cr;
+    lg = nee[v][1] + fcp[v][1] * cg;
+    lb = nee[v][2] + fcp[v][2] * cb;
+    nrec += st.keep[at];
+  }
+  st.nrec[p] = nrec;
+  st.nvert[p] = n;
+}
+
+// Exclusive scan of per-path record counts (one CTA; count is ~5e4).
+__global__ void k_scan_counts(const int32_t* __restrict__ cnt, int64_t n, int64_t* __restrict__ off,
+                              int64_t* __restrict__ total) {
+  __shared__ int64_t part[1024];
+  const int tid = threadIdx.x;
+  const int64_t per = (n + blockDim.x - 1) / blockDim.x;
+  const int64_t b = tid * per, e = (b + per < n) ? b + per : n;
+  int64_t s = 0;
+  for (int64_t i = b; i < e; ++i) s += cnt[i];
+  part[tid] = s;
+  __syncthreads();
+  if (tid == 0) {
+    int64_t run = 0;
+    for (int i = 0; i < (int)blockDim.x; ++i) {
+      const int64_t t = part[i];
+      part[i] = run;
+      run += t;
+    }
+    *total = run;
+  }
+  __syncthreads();
+  int64_t run = part[tid];
+  for (int64_t i = b; i < e; ++i) {
+    off[i] = run;
+    run += cnt[i];
+  }
+}
+
+__global__ void k_compact_records(Stage st, const int64_t* __restrict__ off, int kind,
+                                  nirc_records_out_t out) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= st.count) return;
+  int64_t o = off[p];
+  const int n = st.nvert[p];
+  for (int v = 0; v < n; ++v) {
+    const int64_t at = (int64_t)v * st.count + p;
+    if (!st.keep[at]) continue;
+    if (o < out.cap) {
+      for (int c = 0; c < 3; ++c) {
+        out.pos[3 * o + c] = st.pos[3 * at + c];
+        out.ns[3 * o + c] = st.ns[3 * at + c];
+        out.alb[3 * o + c] = st.alb[3 * at + c];
+        out.dirs[3 * o + c] = st.wi[3 * at + c];
+        out.target[3 * o + c] = kind == 1 ? st.tfull[3 * at + c] : st.tgt[3 * at + c];
+      }
+      out.rough[o] = st.rough[at];
+      out.pdf[o] = st.pdf[at];
+    }
+    ++o;
+  }
+}
+
+bool default_layout(const nirc_spec_t& sp) {
+  return sp.levels == 12 && sp.feats == 2 && sp.bands == 4 && sp.in_dim == 47;
+}
+
+}  // namespace nirc
+
+using namespace nirc;
+
+namespace {
+size_t aup(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct RenderWs {
+  double *acc, *result, *rowbuf;
+  int32_t* term;
+  CacheVertex* cv;
+  unsigned long long* counters;
+  size_t bytes;
+};
+
+int rows_per_vertex(const nirc_render_cfg_t& c) {
+  int m = 0;
+  for (int i = 0; i < c.max_cv && i < 8; ++i) m = c.nc[i] > m ? c.nc[i] : m;
+  return m + 1;
+}
+
+RenderWs carve_render(const nirc_render_cfg_t& c, void* base) {
+  RenderWs w{};
+  char* p = reinterpret_cast<char*>(base);
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    char* r = p ? p + off : nullptr;
+    off += aup(b);
+    return r;
+  };
+  const int64_t ns = (int64_t)(c.row1 - c.row0) * c.width * c.spp;
+  const int64_t ncv = c.mode == 1 && c.cache_on ? ns * c.max_cv : 0;
+  w.acc = (double*)take(ns * 24);
+  w.term = (int32_t*)take(ns * 4);
+  w.result = (double*)take(ncv * 24 + 24);
+  w.cv = (CacheVertex*)take(ncv * sizeof(CacheVertex) + 16);
+  w.counters = (unsigned long long*)take(64);
+  w.rowbuf = (double*)take(0);  // sized on demand for the SIMT fallback
+  w.bytes = off;
+  return w;
+}
+}  // namespace
+
+extern "C" int64_t nirc_render_workspace_bytes(const nirc_render_cfg_t* cfg) {
+  return (int64_t)carve_render(*cfg, nullptr).bytes;
+}
+
+extern "C" int nirc_render(const nirc_scene_t* scene, const double* cam,
+                           const nirc_render_cfg_t* cfg, const nirc_spec_t* spec,
+                           const float* theta, double* img, double* img2, double* term,
+                           int64_t* queries_out, void* workspace, int64_t workspace_bytes,
+                           void* stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const nirc_render_cfg_t& c = *cfg;
+  if (c.mode != 0 && c.mode != 1) {
+    set_last_error("nirc_render supports the pt and two-level modes");
+    return NIRC_E_UNSUPPORTED;
+  }
+  if (c.spp < 1 || c.row0 < 0 || c.row1 > c.height || c.row0 >= c.row1 || c.max_cv > 8) {
+    set_last_error("bad render configuration");
+    return NIRC_E_CONFIG;
+  }
+  for (int i = 0; i < c.max_cv; ++i)
+    if (c.nc[i] < 0 || c.nc[i] > 28) {
+      set_last_error("nc entry outside 0..28");
+      return NIRC_E_CONFIG;
+    }
+  RenderWs w = carve_render(c, workspace);
+  if ((int64_t)w.bytes > workspace_bytes) {
+    set_last_error("render workspace too small");
+    return NIRC_E_CONFIG;
+  }
+  const bool tl = c.mode == 1 && c.cache_on;
+  const int64_t ns = (int64_t)(c.row1 - c.row0) * c.width * c.spp;
+  NIRC_CUDA_TRY(cudaMemsetAsync(w.counters, 0, 64, s));
+  if (tl) NIRC_CUDA_TRY(cudaMemsetAsync(w.result, 0, ns * c.max_cv * 24, s));
+  TraceOut to{w.acc, w.term, w.cv, w.counters};
+  k_trace<<<(int)((ns + 127) / 128), 128, 0, s>>>(*scene, cam, c, to);
+  NIRC_LAUNCH_CHECK("k_trace");
+  if (tl) {
+    if (!spec || !theta) return NIRC_E_CONFIG;
+    const int R = rows_per_vertex(c);
+    InferArgs a{w.cv, w.counters, w.result, nullptr, R, 128 / R};
+    tc::TcNet net;
+    const bool tc_ok = default_layout(*spec) && tc::tc_net_for(*spec, &net);
+    const uint32_t extra = 0;
+    int ng = tc_ok ? tc_groups_for(net, extra) : 0;
+    if (ng > 0) {
+      const uint32_t ex = ng * (kMaxVertsPerTile * 24 * 4 + 128 * 3 * 8);
+      ng = tc_groups_for(net, ex);
+      if (ng > 0) {
+        uint8_t* img_w;
+        float* bias;
+        int st = pack_weights(*spec, net, theta, s, &img_w, &bias);
+        if (st) return st;
+        const tc::TcSmem L = tc::tc_smem_layout(net, ng, ng * (kMaxVertsPerTile * 24 * 4 + 128 * 3 * 8));
+        const int grid = sm_count();
+        if (ng == 2) {
+          NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)k_infer_tc<2>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+          k_infer_tc<2><<<grid, 256, L.total, s>>>(*spec, net, L, theta, img_w, bias, a);
+        } else {
+          NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)k_infer_tc<1>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+          k_infer_tc<1><<<grid, 128, L.total, s>>>(*spec, net, L, theta, img_w, bias, a);
+        }
+        NIRC_LAUNCH_CHECK("k_infer_tc");
+      }
+    }
+    if (ng == 0) {
+      // generic layouts: SIMT rows into a row buffer, then per-vertex combine
+      const int64_t cap = ns * c.max_cv;
+      double* rowbuf = nullptr;
+      NIRC_CUDA_TRY(cudaMallocAsync((void**)&rowbuf, (size_t)cap * R * 24 + 24, s));
+      a.rowbuf = rowbuf;
+      const size_t sm = (size_t)(spec->theta_len - spec->grid_len) * 4;
+      NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)k_infer_simt,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      k_infer_simt<<<(int)((cap * R + 127) / 128), 128, sm, s>>>(*spec, theta, a);
+      NIRC_LAUNCH_CHECK("k_infer_simt");
+      k_combine_rows<<<(int)((cap + 127) / 128), 128, 0, s>>>(a);
+      NIRC_LAUNCH_CHECK("k_combine_rows");
+      NIRC_CUDA_TRY(cudaFreeAsync(rowbuf, s));
+    }
+  }
+  const int64_t npix = (int64_t)(c.row1 - c.row0) * c.width;
+  k_accumulate<<<(int)((npix + 127) / 128), 128, 0, s>>>(c, w.acc, w.term, w.result, tl ? 1 : 0,
+                                                        img, img2, term);
+  NIRC_LAUNCH_CHECK("k_accumulate");
+  if (queries_out)
+    NIRC_CUDA_TRY(cudaMemcpyAsync(queries_out, w.counters + 1, 8, cudaMemcpyDeviceToDevice, s));
+  return NIRC_OK;
+}
+
+namespace {
+Stage carve_stage(int64_t count, void* base, size_t* bytes) {
+  Stage st{};
+  char* p = reinterpret_cast<char*>(base);
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    char* r = p ? p + off : nullptr;
+    off += aup(b);
+    return r;
+  };
+  const int64_t V = (int64_t)pt::MAXB * count;
+  st.pos = (double*)take(V * 24);
+  st.ns = (double*)take(V * 24);
+  st.alb = (double*)take(V * 24);
+  st.rough = (double*)take(V * 8);
+  st.wi = (double*)take(V * 24);
+  st.pdf = (double*)take(V * 8);
+  st.tgt = (double*)take(V * 24);
+  st.tfull = (double*)take(V * 24);
+  st.keep = (uint8_t*)take(V);
+  st.nrec = (int32_t*)take(count * 4);
+  st.nvert = (int32_t*)take(count * 4);
+  take(count * 8);  // offsets
+  st.count = count;
+  *bytes = off;
+  return st;
+}
+}  // namespace
+
+extern "C" int64_t nirc_collect_workspace_bytes(int64_t count) {
+  size_t b = 0;
+  carve_stage(count, nullptr, &b);
+  return (int64_t)b;
+}
+
+extern "C" int nirc_collect(const nirc_scene_t* scene, const double* cam, uint64_t seed,
+                            uint64_t frame, int64_t count, int32_t kind,
+                            const nirc_records_out_t* out, int64_t* n_out, void* workspace,
+                            int64_t workspace_bytes, void* stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (count <= 0) {
+    set_last_error("count must be positive");
+    return NIRC_E_CONFIG;
+  }
+  if (kind != 0 && kind != 1) {
+    set_last_error("record kind %d unsupported on the device (nirc=0, nirc_full=1)", kind);
+    return NIRC_E_UNSUPPORTED;
+  }
+  size_t need = 0;
+  Stage st = carve_stage(count, workspace, &need);
+  if ((int64_t)need > workspace_bytes) {
+    set_last_error("collect workspace too small");
+    return NIRC_E_CONFIG;
+  }
+  int64_t* off = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(st.nvert) + aup(count * 4));
+  k_walk_record<<<(int)((count + 63) / 64), 64, 0, s>>>(*scene, cam, seed, frame, st);
+  NIRC_LAUNCH_CHECK("k_walk_record");
+  k_scan_counts<<<1, 1024, 0, s>>>(st.nrec, count, off, n_out);
+  NIRC_LAUNCH_CHECK("k_scan_counts");
+  k_compact_records<<<(int)((count + 127) / 128), 128, 0, s>>>(st, off, kind, *out);
+  NIRC_LAUNCH_CHECK("k_compact_records");
+  return NIRC_OK;
+}

@@ -53,34 +53,6 @@ inline bool tc_net_for(const nirc_spec_t& sp, TcNet* net) {
   return true;
 }
 
-// Packs theta's layers into hi/lo tf32 images in the canonical K-major layout
-// (N rows, K columns).  One thread per (layer, n, k).
-__global__ void k_pack_weights(nirc_spec_t sp, TcNet net, const float* __restrict__ theta,
-                               uint8_t* __restrict__ img, float* __restrict__ bias) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  int base = 0;
-  for (int l = 0; l < net.nl; ++l) {
-    const int cnt = net.N[l] * net.K[l];
-    if (t >= base && t < base + cnt) {
-      const int e = t - base;
-      const int nrow = e / net.K[l], k = e % net.K[l];
-      const int din = sp.dims[l], dout = sp.dims[l + 1];
-      float w = 0.0f;
-      if (nrow < dout && k < din) w = theta[sp.w_off[l] + (int64_t)nrow * din + k];
-      const float hi = tf32_hi(w);
-      const float lo = w - hi;
-      const uint32_t o = tile_offset(nrow, k, net.N[l]);
-      *reinterpret_cast<float*>(img + net.woff[l] + o) = hi;
-      *reinterpret_cast<float*>(img + net.woff[l] + net.N[l] * net.K[l] * 4 + o) = lo;
-    }
-    base += cnt;
-  }
-  if (t < net.nl * 64) {
-    const int l = t / 64, j = t % 64;
-    bias[t] = j < sp.dims[l + 1] ? theta[sp.b_off[l] + j] : 0.0f;
-  }
-}
-
 // Writes one row (K values, K % 4 == 0) of an A tile as tf32 hi/lo images.
 template <int K>
 __device__ __forceinline__ void write_a_row(uint32_t a_hi, uint32_t a_lo, int r, const float* x) {

@@ -1,0 +1,171 @@
+"""Rendering estimators on the B200 (drop-in for the plain and two-level
+modes of pkg/src/nirclab/estimators.py).
+
+``render`` / ``render_two_level`` run the device frame pipeline
+(C-ABI ``nirc_render``): fp64 path tracing with deferred cache vertices,
+the fused tcgen05 inference + MLMC combine, and per-pixel accumulation.
+The biased early-stop modes are outside the MLMC hot path
+and raise NotImplementedError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+from .errors import ConfigError
+
+MODES = {"pt": 0, "two-level": 1, "biased-nirc-bth": 2, "biased-nirc-sph": 3,
+         "biased-nrc-sph": 4}
+MAX_DIRS = 28  # OFF_CACHE leaves room for 28 direction pairs per vertex
+
+
+@dataclass
+class EstimatorConfig:
+    """Render-mode knobs (estimators.py:49-84)."""
+
+    mode: str = "pt"
+    nc: tuple = (15, 5, 5)
+    nbias: int = 5
+    nr: int = 1
+    max_cache_vertices: int = 3
+    sph_c: float = 0.01
+    rr: float = 0.1
+    roughness_cutoff: float = 0.0625
+
+    def __post_init__(self):
+        if self.mode not in MODES:
+            raise ConfigError(f"unknown estimator mode '{self.mode}'")
+        if len(self.nc) < self.max_cache_vertices:
+            raise ConfigError("nc must cover max_cache_vertices entries")
+        for v in self.nc:
+            if not 0 <= int(v) <= MAX_DIRS:
+                raise ConfigError(f"nc entry {v} outside 0..{MAX_DIRS}")
+        if not 1 <= self.nbias <= MAX_DIRS:
+            raise ConfigError(f"nbias {self.nbias} outside 1..{MAX_DIRS}")
+        if self.nr != 1:
+            raise ConfigError("the walk carries exactly one residual sample per cache vertex")
+        if not 0.0 <= self.rr < 1.0:
+            raise ConfigError(f"roulette probability {self.rr} not in [0,1)")
+        if self.sph_c <= 0.0:
+            raise ConfigError("spread threshold must be positive")
+
+
+@dataclass
+class RenderResult:
+    image: np.ndarray
+    sample_var: np.ndarray
+    path_length: np.ndarray
+    spp: int
+    mode: str
+    queries: int = 0
+
+    @property
+    def avg_path_length(self):
+        return float(np.mean(self.path_length))
+
+    @property
+    def pct_ir_bounces(self):
+        return self.avg_path_length - 1.0
+
+
+class _RenderWs:
+    buf = None
+
+    @classmethod
+    def get(cls, nbytes):
+        if cls.buf is None or cls.buf.numel() < nbytes:
+            cls.buf = _dev.empty((max(int(nbytes), 256),), torch.uint8)
+        return cls.buf
+
+
+def _c_cfg(config, scene, spp, seed, frame, cache_on, rows=None):
+    mode = MODES[config.mode]
+    c = _lib.NircRenderCfg()
+    c.mode = mode
+    c.spp = int(spp)
+    c.cache_on = int(cache_on)
+    c.max_cv = int(config.max_cache_vertices)
+    if c.max_cv > 8:
+        raise ConfigError("at most 8 cache vertices are supported")
+    for i in range(c.max_cv):
+        c.nc[i] = int(config.nc[i])
+    c.rough_cut = float(config.roughness_cutoff)
+    c.rr_survive = 1.0 - float(config.rr)
+    c.seed = int(seed)
+    c.frame = int(frame)
+    c.width = int(scene.camera[14])
+    c.height = int(scene.camera[15])
+    r0, r1 = rows if rows is not None else (0, c.height)
+    c.row0, c.row1 = int(r0), int(r1)
+    return c
+
+
+def render_device(scene, config=None, cache=None, seed=0, spp=1, frame=0, force_cache=False,
+                  rows=None, out=None):
+    """Device-resident render: returns (img, img2, term, queries) CUDA
+    tensors of sums (callers divide by spp).  ``rows`` renders a band of
+    pixel rows (multi-GPU tiles); ``out`` accumulates into given buffers."""
+    if config is None:
+        config = EstimatorConfig()
+    mode = MODES[config.mode]
+    if mode > 1:
+        raise NotImplementedError(f"mode '{config.mode}' is outside the two-level hot path")
+    w, h = int(scene.camera[14]), int(scene.camera[15])
+    cache_on = 0
+    if mode == 1 and cache is not None and (force_cache or not cache.is_zero):
+        cache_on = 1
+    cfg = _c_cfg(config, scene, spp, seed, frame, cache_on, rows)
+    lib = _lib.load()
+    ds = scene.device()
+    if out is None:
+        img = _dev.zeros((h, w, 3), torch.float64)
+        img2 = _dev.zeros((h, w, 3), torch.float64)
+        term = _dev.zeros((h, w), torch.float64)
+    else:
+        img, img2, term = out
+    queries = _dev.zeros((1,), torch.int64)
+    ws = _RenderWs.get(lib.nirc_render_workspace_bytes(C.byref(cfg)))
+    if cache_on:
+        cs = _lib.make_c_spec(cache.spec)
+        spec_p, theta_p = C.byref(cs), _dev.ptr(cache.theta)
+    else:
+        spec_p, theta_p = None, None
+    _lib.check(lib.nirc_render(ds.ptr(), _dev.ptr(ds.cam), C.byref(cfg), spec_p, theta_p,
+                               _dev.ptr(img), _dev.ptr(img2), _dev.ptr(term), _dev.ptr(queries),
+                               _dev.ptr(ws), int(ws.numel()), _dev.stream()), "nirc_render")
+    return img, img2, term, queries
+
+
+def render(scene, config=None, cache=None, seed=0, spp=1, frame=0, v1_map=None,
+           force_cache=False):
+    """Render with the configured estimator (estimators.py:173-217)."""
+    if config is None:
+        config = EstimatorConfig()
+    if v1_map is not None and MODES[config.mode] <= 1:
+        v1_map = None  # only the *_sph modes read it
+    img, img2, term, queries = render_device(scene, config, cache, seed, spp, frame,
+                                             force_cache)
+    img = img.cpu().numpy()
+    img2 = img2.cpu().numpy()
+    term = term.cpu().numpy()
+    mean = img / spp
+    if spp > 1:
+        var = (img2 - img * img / spp) / (spp - 1)
+        np.maximum(var, 0.0, out=var)
+    else:
+        var = np.zeros_like(img)
+    return RenderResult(mean, var, term / spp, spp, config.mode, int(queries.item()))
+
+
+def render_two_level(scene, cache, seed=0, spp=1, frame=0, config=None, force_cache=False):
+    """Cache-plus-residual render; any cache state keeps the mean."""
+    if config is None:
+        config = EstimatorConfig(mode="two-level")
+    if config.mode != "two-level":
+        raise ConfigError(f"config mode '{config.mode}' is not two-level")
+    return render(scene, config, cache, seed, spp, frame, force_cache=force_cache)

@@ -150,3 +150,115 @@ if __name__ == "__main__":
     if "losses" in which:
         golden_losses_adam()
     print("golden fixtures written to", HERE)
+
+
+BOX = """
+camera { position 0.5 0.5 -1.4  look_at 0.5 0.5 0.5  up 0 1 0
+         fov 39  resolution 16 16 }
+material w { kind lambert  albedo 0.7 0.7 0.7 }
+material l { kind lambert  albedo 0 0 0  emit 10 10 10 }
+quad floor   { material w  p0 0 0 0  p1 1 0 0  p2 1 0 1  p3 0 0 1 }
+quad ceiling { material w  p0 0 1 0  p1 0 1 1  p2 1 1 1  p3 1 1 0 }
+quad back    { material w  p0 0 0 1  p1 1 0 1  p2 1 1 1  p3 0 1 1 }
+quad left    { material w  p0 0 0 0  p1 0 0 1  p2 0 1 1  p3 0 1 0 }
+quad right   { material w  p0 1 0 0  p1 1 1 0  p2 1 1 1  p3 1 0 1 }
+quad lamp    { material l  p0 0.35 0.999 0.35  p1 0.65 0.999 0.35
+               p2 0.65 0.999 0.65  p3 0.35 0.999 0.65 }
+"""
+
+# a scene with every material and light kind the device path tracer handles
+MIXED = """
+camera { position 0.5 0.5 -1.6  look_at 0.5 0.45 0.5  up 0 1 0  fov 42  resolution 24 20 }
+material w { kind lambert  albedo 0.7 0.7 0.7 }
+material r { kind lambert  albedo 0.6 0.1 0.1 }
+material m { kind mirror  albedo 0.9 0.9 0.9 }
+material g { kind conductor  albedo 0.9 0.6 0.3  roughness 0.3 }
+material l { kind lambert  albedo 0 0 0  emit 8 7 6 }
+quad floor   { material w  p0 0 0 0  p1 1 0 0  p2 1 0 1  p3 0 0 1 }
+quad back    { material g  p0 0 0 1  p1 1 0 1  p2 1 1 1  p3 0 1 1 }
+quad left    { material r  p0 0 0 0  p1 0 0 1  p2 0 1 1  p3 0 1 0 }
+quad right   { material m  p0 1 0 0  p1 1 1 0  p2 1 1 1  p3 1 0 1 }
+sphere ball  { material w  center 0.35 0.2 0.5  radius 0.2 }
+sphere bulb  { material l  center 0.7 0.85 0.45  radius 0.08 }
+environment { kind sky  zenith 0.3 0.4 0.8  horizon 0.9 0.9 0.9  ground 0.2 0.2 0.2 }
+"""
+
+
+def golden_scenes():
+    """sha1 of every pack array of the builtin scenes and the test scenes."""
+    import hashlib
+    import json
+
+    from nirclab.scene import load_builtin, load_scene
+
+    out = {}
+    scenes = {n: load_builtin(n) for n in ("cornell", "furnace", "occlusion", "teleport")}
+    scenes["teleport@50"] = load_builtin("teleport").at_frame(50)
+    scenes["BOX"] = load_scene(BOX)
+    scenes["MIXED"] = load_scene(MIXED)
+    for name, sc in scenes.items():
+        d = {}
+        for f in sc.pack._fields:
+            a = np.ascontiguousarray(np.asarray(getattr(sc.pack, f)))
+            d[f] = [str(a.dtype), list(a.shape), hashlib.sha1(a.tobytes()).hexdigest()]
+        d["camera"] = hashlib.sha1(np.asarray(sc.camera).tobytes()).hexdigest()
+        out[name] = d
+    with open(os.path.join(HERE, "scene_packs.json"), "w") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+
+
+def golden_render():
+    """PT and two-level renders (images + path lengths) from the reference."""
+    from nirclab.caches import Cache
+    from nirclab.estimators import EstimatorConfig, render, render_two_level
+    from nirclab.scene import load_builtin, load_scene
+
+    out = {}
+    box = load_scene(BOX)
+    mixed = load_scene(MIXED)
+    corn = load_builtin("cornell")
+    jobs = [("box_pt", box, EstimatorConfig(mode="pt"), None, 5, 2),
+            ("mixed_pt", mixed, EstimatorConfig(mode="pt"), None, 3, 2),
+            ("corn_pt", corn, EstimatorConfig(mode="pt"), None, 0, 1)]
+    cbox = Cache.create("nirc", box, seed=9, init="random")
+    cmix = Cache.create("nirc", mixed, seed=2, init="random")
+    ccor = Cache.create("nirc", corn, seed=1, init="random")
+    jobs += [("box_tl", box, EstimatorConfig(mode="two-level", nc=(8, 4, 4)), cbox, 5, 2),
+             ("mixed_tl", mixed, EstimatorConfig(mode="two-level", nc=(6, 3, 2)), cmix, 3, 2),
+             ("corn_tl", corn, EstimatorConfig(mode="two-level", nc=(8,), max_cache_vertices=1),
+              ccor, 0, 1)]
+    for tag, sc, cfg, cache, seed, spp in jobs:
+        r = render(sc, cfg, cache=cache, seed=seed, spp=spp)
+        out[f"{tag}_image"] = r.image
+        out[f"{tag}_var"] = r.sample_var
+        out[f"{tag}_plen"] = r.path_length
+    # zero cache: bit-identical to PT (tests/test_estimators.py:157-166)
+    zc = Cache.create("nirc", box, seed=3)
+    out["box_tl_zero_forced"] = render_two_level(box, zc, seed=5, spp=2, force_cache=True).image
+    np.savez_compressed(os.path.join(HERE, "render.npz"), **out)
+
+
+def golden_collect():
+    """Training records (caches.py:87-131) on the BOX, MIXED and Cornell scenes."""
+    from nirclab.caches import collect_training_records
+    from nirclab.scene import load_builtin, load_scene
+
+    out = {}
+    for tag, sc, count, seed, frame, kind in (
+            ("box", load_scene(BOX), 40, 5, 3, "nirc"),
+            ("boxfull", load_scene(BOX), 40, 5, 3, "nirc_full"),
+            ("mixed", load_scene(MIXED), 60, 2, 1, "nirc"),
+            ("corn", load_builtin("cornell"), 103, 0, 0, "nirc")):
+        rec = collect_training_records(sc, seed, count, kind=kind, frame=frame)
+        for k in ("pos", "ns", "alb", "rough", "dirs", "target", "pdf"):
+            out[f"{tag}_{k}"] = getattr(rec, k)
+    np.savez_compressed(os.path.join(HERE, "collect.npz"), **out)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1:
+    if "scenes" in sys.argv:
+        golden_scenes()
+    if "render" in sys.argv:
+        golden_render()
+    if "collect" in sys.argv:
+        golden_collect()
