@@ -310,8 +310,8 @@ __global__ void __launch_bounds__(NG * 128, 1)
        tile += (int64_t)gridDim.x * NG) {
     const int64_t v0 = tile * S;
     // 1) shared surface encoding: one thread per (vertex, level)
-    if (tg < S * 12) {
-      const int j = tg / 12, lvl = tg % 12;
+    for (int item = tg; item < S * 12; item += tc::kGroupThreads) {
+      const int j = item / 12, lvl = item % 12;
       const int64_t vid = v0 + j;
       if (vid < nverts) {
         const CacheVertex& r = a.cv[vid];
