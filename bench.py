@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n", type=int, default=N_QUERIES)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-frame", action="store_true")
+    ap.add_argument("--frame-steps", type=int, default=10)
     return ap.parse_args()
 
 
@@ -172,6 +174,58 @@ def run_reference(args, rank, world):
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------- frame leg -------
+def frame_bench(frames, warmup, width=1920, height=1080, nc=(16,)):
+    """BASELINE config 3: Cornell at 1920x1080, two-level with nc=(16,) at
+    the first cache vertex, spp 1, D = 4 cache; then collect ceil(0.025 W H)
+    training paths and 4 Adam steps of 16384 records.  Device time per
+    phase with CUDA events; frames after `warmup` are timed."""
+    import torch
+
+    from paper_2412_04634_b200.caches import Cache, default_train_count, train_frame
+    from paper_2412_04634_b200.estimators import render_device
+    from paper_2412_04634_b200.frame import config3
+    from paper_2412_04634_b200.scene import load_builtin
+
+    scene = load_builtin("cornell").with_resolution(width, height)
+    cache = Cache.create("nirc", scene, seed=0, init="random")
+    cfg = config3(nc)
+    stream = torch.cuda.current_stream()
+    phases = {"render": [], "collect": [], "train": [], "frame": []}
+    queries, records = [], []
+    count = default_train_count(scene)
+    for f in range(warmup + frames):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record(stream)
+        _, _, _, q = render_device(scene, cfg, cache, seed=0, spp=1, frame=f)
+        ev[1].record(stream)
+        rec = cache.collect(count=count, frame=f)
+        ev[2].record(stream)
+        train_frame(cache, rec, steps=4)
+        ev[3].record(stream)
+        torch.cuda.synchronize()
+        if f >= warmup:
+            phases["render"].append(ev[0].elapsed_time(ev[1]))
+            phases["collect"].append(ev[1].elapsed_time(ev[2]))
+            phases["train"].append(ev[2].elapsed_time(ev[3]))
+            phases["frame"].append(ev[0].elapsed_time(ev[3]))
+            queries.append(int(q.item()))
+            records.append(len(rec))
+    med = {k: sorted(v)[len(v) // 2] for k, v in phases.items()}
+    return {
+        "metric": "ms_per_frame_1080p", "value": med["frame"], "unit": "ms/frame",
+        "higher_is_better": False, "frames": frames, "warmup": warmup,
+        "render_ms": med["render"], "collect_ms": med["collect"], "train_ms": med["train"],
+        "queries_per_frame": queries[-1], "records_per_frame": records[-1],
+        "train_paths_per_frame": count,
+        "train_samples_per_sec": 4 * min(16384, records[-1]) / (med["train"] * 1e-3),
+        "render_queries_per_sec": queries[-1] / (med["render"] * 1e-3),
+        "config": "cfg3: cornell 1920x1080, two-level nc=(16,), spp 1, D=4 cache, "
+                  "collect 51,840 paths, 4 x 16384 train steps",
+        "reference_cpu_context": "SURVEY.md 6: 122.6 s/frame on 1 core (not re-timed here)",
+    }
 
 
 # ------------------------------------------------------------ GPU leg ----
@@ -304,6 +358,8 @@ def run_b200(args, rank, world, local_rank):
                 "path": "paper_2412_04634_b200.mlp.full_forward, pinned host buffers"},
         "gpu_launches": 2 * args.steps,
     }
+    if world == 1 and not args.no_frame:
+        line["frame_1080p"] = frame_bench(args.frame_steps, 3)
     if world == 1 and not args.no_cpu_baseline:
         rate, nq = cpu_baseline(cores=1, chunks=6, chunk=1 << 15)
         line["cpu_baseline"] = {"value": rate, "unit": "queries/s", "cores": 1, "kind": "port",
