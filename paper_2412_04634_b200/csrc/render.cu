@@ -50,102 +50,106 @@ struct TraceOut {
   unsigned long long* counters;  // [0] cache vertices, [1] executed queries
 };
 
-// trace_sample for MODE_PT / MODE_TL with deferred cache terms.
-__global__ void k_trace(nirc_scene_t scn, const double* __restrict__ cam, nirc_render_cfg_t cfg,
-                        TraceOut out) {
+// Per-lane path state of the persistent tracer.
+struct PathState {
+  V3 o, d, lns;
+  double ar, ag, ab, tr, tg, tb, prev_pdf;
+  uint64_t key;
+  int64_t sid;
+  int v, cu, term;
+};
+
+// Warp-aggregated fetch of the next sample index for the lanes in `want`.
+__device__ inline int64_t fetch_sample(unsigned long long* ctr, bool want) {
+  const unsigned mask = __activemask();
+  const unsigned need = __ballot_sync(mask, want);
+  if (!want) return -1;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(need) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(ctr, (unsigned long long)__popc(need));
+  base = __shfl_sync(need, base, leader);
+  return (int64_t)base + __popc(need & ((1u << lane) - 1u));
+}
+
+__device__ inline void start_path(PathState& p, const double* cam, const nirc_render_cfg_t& cfg,
+                                  int64_t sid) {
   const int W = cfg.width;
-  const int64_t nsamp = (int64_t)(cfg.row1 - cfg.row0) * W * cfg.spp;
-  const int64_t sid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (sid >= nsamp) return;
   const int s = (int)(sid % cfg.spp);
   const int64_t lp = sid / cfg.spp;
   const int ix = (int)(lp % W);
   const int iy = cfg.row0 + (int)(lp / W);
   const int64_t pix = (int64_t)iy * W + ix;
-  const uint64_t key = stream_key(cfg.seed, P_RENDER, cfg.frame, (uint64_t)pix, (uint64_t)s);
-  const double jx = rand_uniform(key, DIM_JITTER_X);
-  const double jy = rand_uniform(key, DIM_JITTER_Y);
-  V3 o, d;
-  pt::camera_ray(cam, ix, iy, jx, jy, o, d);
+  p.sid = sid;
+  p.key = stream_key(cfg.seed, P_RENDER, cfg.frame, (uint64_t)pix, (uint64_t)s);
+  pt::camera_ray(cam, ix, iy, rand_uniform(p.key, DIM_JITTER_X), rand_uniform(p.key, DIM_JITTER_Y),
+                 p.o, p.d);
+  p.ar = p.ag = p.ab = 0.0;
+  p.tr = p.tg = p.tb = 1.0;
+  p.prev_pdf = -1.0;
+  p.lns = {0.0, 0.0, 0.0};
+  p.v = p.cu = p.term = 0;
+}
 
-  double ar = 0.0, ag = 0.0, ab = 0.0;
-  double tr = 1.0, tg = 1.0, tb = 1.0;
-  double prev_pdf = -1.0;
-  V3 lns = {0.0, 0.0, 0.0};
-  int cu = 0, term = 0;
-  const bool tl = cfg.mode == 1 && cfg.cache_on == 1;
-  for (int v = 0; v < pt::MAXB; ++v) {
-    const pt::Hit h = pt::intersect<false>(scn, o, d, pt::T_FAR);
-    if (h.kind < 0) {
-      if (scn.env_kind != pt::ENV_NONE) {
-        const V3 e = pt::env_eval(scn, d);
-        double w = 1.0;
-        if (prev_pdf >= 0.0) {
-          const double pn = pt::nee_pdf_for_env(scn, lns, d);
-          w = prev_pdf / (prev_pdf + pn);
-        }
-        ar += tr * w * e.x;
-        ag += tg * w * e.y;
-        ab += tb * w * e.z;
-      }
-      break;
-    }
-    term = v + 1;
-    const V3 wo = {-d.x, -d.y, -d.z};
-    const double flip = (h.n.x * wo.x + h.n.y * wo.y + h.n.z * wo.z) >= 0.0 ? 1.0 : -1.0;
-    const V3 ns = {h.n.x * flip, h.n.y * flip, h.n.z * flip};
-    const V3 em = pt::ld3(scn.mat_emit, h.mid);
-    if (em.x > 0.0 || em.y > 0.0 || em.z > 0.0) {
+// One vertex of trace_sample (kernels.py:481-608) for MODE_PT / MODE_TL.
+// Returns true when the path ended.  A two-level cache vertex is returned in
+// `rec` (pending == 1) instead of being evaluated inline.
+__device__ inline bool trace_vertex(const nirc_scene_t& scn, const nirc_render_cfg_t& cfg,
+                                    PathState& p, CacheVertex& rec, int& pending) {
+  pending = 0;
+  const int v = p.v;
+  const pt::Hit h = pt::intersect<false>(scn, p.o, p.d, pt::T_FAR);
+  if (h.kind < 0) {
+    if (scn.env_kind != pt::ENV_NONE) {
+      const V3 e = pt::env_eval(scn, p.d);
       double w = 1.0;
-      if (prev_pdf >= 0.0) {
-        const double pn = pt::nee_pdf_for_hit(scn, h.kind, h.prim, h.t, d, h.n);
-        w = prev_pdf / (prev_pdf + pn);
+      if (p.prev_pdf >= 0.0) {
+        const double pn = pt::nee_pdf_for_env(scn, p.lns, p.d);
+        w = p.prev_pdf / (p.prev_pdf + pn);
       }
-      ar += tr * w * em.x;
-      ag += tg * w * em.y;
-      ab += tb * w * em.z;
+      p.ar += p.tr * w * e.x;
+      p.ag += p.tg * w * e.y;
+      p.ab += p.tb * w * e.z;
     }
-    const int mkind = scn.mat_kind[h.mid];
-    const V3 alb = pt::ld3(scn.mat_albedo, h.mid);
-    const double rough = scn.mat_rough[h.mid];
-    const int base = VERTEX_DIM_BASE + v * DIMS_PER_VERTEX;
-    if (mkind == pt::MAT_MIRROR) {  // delta vertex, kernels.py:520-548
-      double rr_div = 1.0;
-      if (v >= pt::RR_START) {
-        if (rand_uniform(key, base + OFF_RR) >= cfg.rr_survive) break;
-        rr_div = cfg.rr_survive;
-      }
-      const pt::BsdfSample b = pt::bsdf_sample(mkind, alb, rough, ns, wo,
-                                               rand_uniform(key, base + OFF_BSDF_U),
-                                               rand_uniform(key, base + OFF_BSDF_U + 1));
-      if (b.pdf <= 0.0) break;
-      const double ci = b.wi.x * ns.x + b.wi.y * ns.y + b.wi.z * ns.z;
-      if (ci <= 0.0) break;
-      const double inv = 1.0 / (b.pdf * rr_div);
-      tr *= b.f.x * ci * inv;
-      tg *= b.f.y * ci * inv;
-      tb *= b.f.z * ci * inv;
-      prev_pdf = -1.0;
-      const double sg = (h.n.x * b.wi.x + h.n.y * b.wi.y + h.n.z * b.wi.z) > 0.0 ? 1.0 : -1.0;
-      o = {h.p.x + sg * scn.eps * h.n.x, h.p.y + sg * scn.eps * h.n.y,
-           h.p.z + sg * scn.eps * h.n.z};
-      d = b.wi;
-      lns = ns;
-      continue;
+    return true;
+  }
+  p.term = v + 1;
+  const V3 wo = {-p.d.x, -p.d.y, -p.d.z};
+  const double flip = (h.n.x * wo.x + h.n.y * wo.y + h.n.z * wo.z) >= 0.0 ? 1.0 : -1.0;
+  const V3 ns = {h.n.x * flip, h.n.y * flip, h.n.z * flip};
+  const V3 em = pt::ld3(scn.mat_emit, h.mid);
+  if (em.x > 0.0 || em.y > 0.0 || em.z > 0.0) {
+    double w = 1.0;
+    if (p.prev_pdf >= 0.0) {
+      const double pn = pt::nee_pdf_for_hit(scn, h.kind, h.prim, h.t, p.d, h.n);
+      w = p.prev_pdf / (p.prev_pdf + pn);
     }
-    // MODE_PT / MODE_TL (kernels.py:549-608)
+    p.ar += p.tr * w * em.x;
+    p.ag += p.tg * w * em.y;
+    p.ab += p.tb * w * em.z;
+  }
+  const int mkind = scn.mat_kind[h.mid];
+  const V3 alb = pt::ld3(scn.mat_albedo, h.mid);
+  const double rough = scn.mat_rough[h.mid];
+  const int base = VERTEX_DIM_BASE + v * DIMS_PER_VERTEX;
+  const uint64_t key = p.key;
+  double rr_div = 1.0;
+  if (mkind == pt::MAT_MIRROR) {  // delta vertex, kernels.py:520-548
+    if (v >= pt::RR_START) {
+      if (rand_uniform(key, base + OFF_RR) >= cfg.rr_survive) return true;
+      rr_div = cfg.rr_survive;
+    }
+  } else {
     const V3 q = pt::nee_contrib(scn, h.p, ns, h.n, mkind, alb, rough, wo,
                                  rand_uniform(key, base + OFF_LIGHT_PICK),
                                  rand_uniform(key, base + OFF_LIGHT_U),
                                  rand_uniform(key, base + OFF_LIGHT_U + 1), 0);
-    ar += tr * q.x;
-    ag += tg * q.y;
-    ab += tb * q.z;
-    int pending = 0;
-    CacheVertex rec;
-    if (tl && rough >= cfg.rough_cut && cu < cfg.max_cv) {
-      const int ncq = cfg.nc[cu];
-      cu += 1;
+    p.ar += p.tr * q.x;
+    p.ag += p.tg * q.y;
+    p.ab += p.tb * q.z;
+    if (cfg.mode == 1 && cfg.cache_on == 1 && rough >= cfg.rough_cut && p.cu < cfg.max_cv) {
+      const int ncq = cfg.nc[p.cu];
+      p.cu += 1;
       if (ncq > 0) {
         pending = 1;
         rec.pos[0] = h.p.x; rec.pos[1] = h.p.y; rec.pos[2] = h.p.z;
@@ -153,65 +157,95 @@ __global__ void k_trace(nirc_scene_t scn, const double* __restrict__ cam, nirc_r
         rec.alb[0] = alb.x; rec.alb[1] = alb.y; rec.alb[2] = alb.z;
         rec.rough = rough;
         rec.wo[0] = wo.x; rec.wo[1] = wo.y; rec.wo[2] = wo.z;
-        rec.T[0] = tr; rec.T[1] = tg; rec.T[2] = tb;
+        rec.T[0] = p.tr; rec.T[1] = p.tg; rec.T[2] = p.tb;
         rec.key = key;
         rec.base = base;
         rec.ncq = ncq;
         rec.mkind = mkind;
         rec.has_res = 0;
-        rec.slot = sid * cfg.max_cv + (cu - 1);
-      }
-    }
-    bool cont = true;
-    double rr_div = 1.0;
-    if (v >= pt::RR_START) {
-      if (rand_uniform(key, base + OFF_RR) >= cfg.rr_survive) cont = false;
-      else rr_div = cfg.rr_survive;
-    }
-    pt::BsdfSample b;
-    double ci = 0.0;
-    if (cont) {
-      b = pt::bsdf_sample(mkind, alb, rough, ns, wo, rand_uniform(key, base + OFF_BSDF_U),
-                          rand_uniform(key, base + OFF_BSDF_U + 1));
-      if (b.pdf <= 0.0) cont = false;
-      else {
-        ci = b.wi.x * ns.x + b.wi.y * ns.y + b.wi.z * ns.z;
-        if (ci <= 0.0) cont = false;
-      }
-    }
-    if (cont) {
-      const double inv = 1.0 / (b.pdf * rr_div);
-      tr *= b.f.x * ci * inv;
-      tg *= b.f.y * ci * inv;
-      tb *= b.f.z * ci * inv;
-      if (pending) {
-        rec.has_res = 1;
-        rec.Tp[0] = tr; rec.Tp[1] = tg; rec.Tp[2] = tb;
-        rec.wc[0] = b.wi.x; rec.wc[1] = b.wi.y; rec.wc[2] = b.wi.z;
-      }
-    }
-    if (pending) {
-      if (!rec.has_res) {
+        rec.slot = p.sid * cfg.max_cv + (p.cu - 1);
         rec.Tp[0] = rec.Tp[1] = rec.Tp[2] = 0.0;
         rec.wc[0] = rec.wc[1] = 0.0;
         rec.wc[2] = 1.0;
       }
-      const unsigned long long idx = atomicAdd(out.counters, 1ull);
-      out.cv[idx] = rec;
-      atomicAdd(out.counters + 1, (unsigned long long)(rec.ncq + rec.has_res));
     }
-    if (!cont) break;
-    prev_pdf = b.pdf;
-    const double sg = (h.n.x * b.wi.x + h.n.y * b.wi.y + h.n.z * b.wi.z) > 0.0 ? 1.0 : -1.0;
-    o = {h.p.x + sg * scn.eps * h.n.x, h.p.y + sg * scn.eps * h.n.y,
-         h.p.z + sg * scn.eps * h.n.z};
-    d = b.wi;
-    lns = ns;
+    if (v >= pt::RR_START) {
+      if (rand_uniform(key, base + OFF_RR) >= cfg.rr_survive) return true;
+      rr_div = cfg.rr_survive;
+    }
   }
-  out.acc[3 * sid] = ar;
-  out.acc[3 * sid + 1] = ag;
-  out.acc[3 * sid + 2] = ab;
-  out.term[sid] = term;
+  const pt::BsdfSample b = pt::bsdf_sample(mkind, alb, rough, ns, wo,
+                                           rand_uniform(key, base + OFF_BSDF_U),
+                                           rand_uniform(key, base + OFF_BSDF_U + 1));
+  if (b.pdf <= 0.0) return true;
+  const double ci = b.wi.x * ns.x + b.wi.y * ns.y + b.wi.z * ns.z;
+  if (ci <= 0.0) return true;
+  const double inv = 1.0 / (b.pdf * rr_div);
+  p.tr *= b.f.x * ci * inv;
+  p.tg *= b.f.y * ci * inv;
+  p.tb *= b.f.z * ci * inv;
+  if (pending) {  // residual along the continuation (kernels.py:593-601)
+    rec.has_res = 1;
+    rec.Tp[0] = p.tr; rec.Tp[1] = p.tg; rec.Tp[2] = p.tb;
+    rec.wc[0] = b.wi.x; rec.wc[1] = b.wi.y; rec.wc[2] = b.wi.z;
+  }
+  p.prev_pdf = mkind == pt::MAT_MIRROR ? -1.0 : b.pdf;
+  const double sg = (h.n.x * b.wi.x + h.n.y * b.wi.y + h.n.z * b.wi.z) > 0.0 ? 1.0 : -1.0;
+  p.o = {h.p.x + sg * scn.eps * h.n.x, h.p.y + sg * scn.eps * h.n.y,
+         h.p.z + sg * scn.eps * h.n.z};
+  p.d = b.wi;
+  p.lns = ns;
+  p.v = v + 1;
+  return p.v >= pt::MAXB;
+}
+
+// K5: persistent path tracer.  Each lane owns one path at a time and pulls
+// the next (pixel, sample) from a global counter as soon as its path ends,
+// so lanes stay busy despite Russian-roulette path-length variance (a plain
+// one-thread-per-sample megakernel idles ~80% of each warp).
+__global__ void __launch_bounds__(128) k_trace(nirc_scene_t scn, const double* __restrict__ cam,
+                                               nirc_render_cfg_t cfg, TraceOut out) {
+  const int64_t nsamp = (int64_t)(cfg.row1 - cfg.row0) * cfg.width * cfg.spp;
+  PathState p;
+  bool active = false;
+  int64_t sid = fetch_sample(out.counters + 2, true);
+  if (sid < nsamp) {
+    start_path(p, cam, cfg, sid);
+    active = true;
+  }
+  while (__any_sync(0xffffffffu, active)) {
+    if (active) {
+      CacheVertex rec;
+      int pending;
+      const bool done = trace_vertex(scn, cfg, p, rec, pending);
+      // warp-aggregated append of the cache-vertex records and query counts
+      const unsigned pm = __ballot_sync(__activemask(), pending);
+      if (pending) {
+        const int lane = threadIdx.x & 31;
+        const int leader = __ffs(pm) - 1;
+        unsigned long long base = 0;
+        const unsigned q = __reduce_add_sync(pm, (unsigned)(rec.ncq + rec.has_res));
+        if (lane == leader) {
+          base = atomicAdd(out.counters, (unsigned long long)__popc(pm));
+          atomicAdd(out.counters + 1, (unsigned long long)q);
+        }
+        base = __shfl_sync(pm, base, leader);
+        out.cv[base + __popc(pm & ((1u << lane) - 1u))] = rec;
+      }
+      if (done) {
+        out.acc[3 * p.sid] = p.ar;
+        out.acc[3 * p.sid + 1] = p.ag;
+        out.acc[3 * p.sid + 2] = p.ab;
+        out.term[p.sid] = p.term;
+        active = false;
+      }
+    }
+    const int64_t nxt = fetch_sample(out.counters + 2, !active);
+    if (!active && nxt < nsamp) {
+      start_path(p, cam, cfg, nxt);
+      active = true;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------
@@ -795,7 +829,16 @@ extern "C" int nirc_render(const nirc_scene_t* scene, const double* cam,
   NIRC_CUDA_TRY(cudaMemsetAsync(w.counters, 0, 64, s));
   if (tl) NIRC_CUDA_TRY(cudaMemsetAsync(w.result, 0, ns * c.max_cv * 24, s));
   TraceOut to{w.acc, w.term, w.cv, w.counters};
-  k_trace<<<(int)((ns + 127) / 128), 128, 0, s>>>(*scene, cam, c, to);
+  static int trace_blocks_per_sm = 0;
+  if (!trace_blocks_per_sm) {
+    NIRC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&trace_blocks_per_sm, k_trace,
+                                                                128, 0));
+    if (trace_blocks_per_sm < 1) trace_blocks_per_sm = 1;
+  }
+  const int64_t tgrid_max = (ns + 127) / 128;
+  const int64_t tgrid_pers = (int64_t)sm_count() * trace_blocks_per_sm;
+  k_trace<<<(int)(tgrid_max < tgrid_pers ? tgrid_max : tgrid_pers), 128, 0, s>>>(*scene, cam, c,
+                                                                                  to);
   NIRC_LAUNCH_CHECK("k_trace");
   if (tl) {
     if (!spec || !theta) return NIRC_E_CONFIG;
