@@ -37,6 +37,7 @@ DEPTH = 2
 FLOPS_PER_QUERY = 2 * (47 * 64 + 64 * 64 + 64 * 3)     # 14,592 for D = 2
 HBM_BYTES_PER_QUERY = 13 * 8 + 3 * 4                  # f64 rows in + f32 rgb out = 116
 L2_GATHER_BYTES_PER_QUERY = 12 * 8 * 2 * 4            # 768
+PRECISION = int(os.environ.get("NIRC_BENCH_PRECISION", "2"))  # 2: tcgen05 2xFP16 split
 
 
 def parse():
@@ -253,7 +254,7 @@ def run_b200(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
 
     def step():
-        _lib.check(lib.nirc_full_forward(cs, _dev.ptr(theta), *ptrs, n, _dev.ptr(Y), 0,
+        _lib.check(lib.nirc_full_forward(cs, _dev.ptr(theta), *ptrs, n, _dev.ptr(Y), PRECISION,
                                          _dev.stream()), "nirc_full_forward")
 
     def barrier():
@@ -292,7 +293,7 @@ def run_b200(args, rank, world, local_rank):
 
     def e2e_step():
         dq = [h.to("cuda", non_blocking=True) for h in host]
-        y = full_forward(spec, theta, *dq)
+        y = full_forward(spec, theta, *dq, precision=PRECISION)
         y_host.copy_(y, non_blocking=True)
 
     for _ in range(2):
@@ -339,7 +340,7 @@ def run_b200(args, rank, world, local_rank):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "cfg2 NIRC inference micro-bench: 2^22 random (pos,dir) queries "
                                "per GPU, fused hash-grid+SH encode + 64-wide 2-hidden-layer MLP "
-                               "(tcgen05 3xTF32)",
+                               f"(tcgen05 {'2xFP16-split' if PRECISION == 2 else '3xTF32'})",
                    "model": "nirc 12x2^15x2 hash + SH4 + 64x2 MLP", "global_batch": world * n,
                    "seq_len": 1, "parallelism": f"dp{world} (independent query shards)",
                    "l2_flush": "inputs (436 MB/step) larger than L2; hash tables L2-resident"},

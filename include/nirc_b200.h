@@ -92,6 +92,9 @@ typedef struct nirc_render_cfg {
   uint64_t seed, frame;
   int32_t width, height; /* camera resolution */
   int32_t row0, row1;    /* pixel-row band [row0, row1) rendered by this call */
+  int32_t precision;     /* network arithmetic: 0 tcgen05 3xTF32, 1 fp32 SIMT,
+                            2 tcgen05 2xFP16 split (default) */
+  int32_t pad;
 } nirc_render_cfg_t;
 
 /* ---- library / introspection ------------------------------------------ */
@@ -132,7 +135,8 @@ int nirc_mlp_backward(const nirc_spec_t* spec, const float* theta,
 /* full_forward (mlp.py:216-224) = encode_batch + mlp_forward fused in one
  * persistent sm_100a kernel: hash-grid + SH + aux encoding written straight
  * into the SMEM A-tile, every layer a 3xTF32 tcgen05.mma with the fp32
- * accumulator in TMEM.  precision: 0 = tcgen05 3xTF32, 1 = fp32 SIMT twin. */
+ * accumulator in TMEM.  precision: 0 = tcgen05 3xTF32, 1 = fp32 SIMT twin,
+ * 2 = tcgen05 2xFP16 split (3 products; |activations| < 65504). */
 int nirc_full_forward(const nirc_spec_t* spec, const float* theta,
                       const double* pos, const double* normal,
                       const double* albedo, const double* rough,

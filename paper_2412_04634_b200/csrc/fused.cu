@@ -9,8 +9,8 @@
 
 namespace nirc {
 namespace tc {
-// Packs theta's layers into hi/lo tf32 images in the canonical K-major layout
-// (N rows, K columns).  One thread per (layer, n, k).
+// Packs theta's layers into hi/lo operand images (tf32 or fp16) in the
+// canonical K-major layout (N rows, K columns).  One thread per (layer, n, k).
 __global__ void k_pack_weights(nirc_spec_t sp, TcNet net, const float* __restrict__ theta,
                                uint8_t* __restrict__ img, float* __restrict__ bias) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -23,11 +23,18 @@ __global__ void k_pack_weights(nirc_spec_t sp, TcNet net, const float* __restric
       const int din = sp.dims[l], dout = sp.dims[l + 1];
       float w = 0.0f;
       if (nrow < dout && k < din) w = theta[sp.w_off[l] + (int64_t)nrow * din + k];
-      const float hi = tf32_hi(w);
-      const float lo = w - hi;
-      const uint32_t o = tile_offset(nrow, k, net.N[l]);
-      *reinterpret_cast<float*>(img + net.woff[l] + o) = hi;
-      *reinterpret_cast<float*>(img + net.woff[l] + net.N[l] * net.K[l] * 4 + o) = lo;
+      if (net.prec == PrecF16x2::kId) {
+        const __half hi = __float2half_rn(w);
+        const __half lo = __float2half_rn(w - __half2float(hi));
+        const uint32_t o = op_offset<PrecF16x2>(nrow, k, net.N[l]);
+        *reinterpret_cast<__half*>(img + net.woff[l] + o) = hi;
+        *reinterpret_cast<__half*>(img + net.woff[l] + net.N[l] * net.K[l] * 2 + o) = lo;
+      } else {
+        const float hi = tf32_hi(w);
+        const uint32_t o = op_offset<PrecTF32x3>(nrow, k, net.N[l]);
+        *reinterpret_cast<float*>(img + net.woff[l] + o) = hi;
+        *reinterpret_cast<float*>(img + net.woff[l] + net.N[l] * net.K[l] * 4 + o) = w - hi;
+      }
     }
     base += cnt;
   }
@@ -77,7 +84,7 @@ __device__ __forceinline__ void encode_default(const nirc_spec_t& sp,
   x[47] = 0.0f;
 }
 
-template <int NG>
+template <class P, int NG>
 __global__ void __launch_bounds__(NG * 128, 1)
     k_full_forward_tc(nirc_spec_t sp, tc::TcNet net, tc::TcSmem L,
                       const float* __restrict__ theta, const uint8_t* __restrict__ wimg,
@@ -91,8 +98,8 @@ __global__ void __launch_bounds__(NG * 128, 1)
   const uint32_t s0 = tc::smem_u32(smem);
   const int group = threadIdx.x >> 7;
   const int tg = threadIdx.x & 127;
-  const uint32_t a_hi = s0 + L.a_off + group * tc::kABufBytes;
-  const uint32_t a_lo = a_hi + tc::kAImageBytes;
+  const uint32_t a_hi = s0 + L.a_off + group * L.abuf_bytes;
+  const uint32_t a_lo = a_hi + L.abuf_bytes / 2;
   const uint32_t mbar = s0 + L.bar_off + 8 * (1 + group);
   const uint32_t tmem_d = tmem_base + group * 64;
   const float* s_bias = reinterpret_cast<const float*>(smem + L.bias_off);
@@ -110,9 +117,9 @@ __global__ void __launch_bounds__(NG * 128, 1)
 #pragma unroll
       for (int k = 0; k < kK0; ++k) x[k] = 0.0f;
     }
-    tc::write_a_row<kK0>(a_hi, a_lo, tg, x);
+    tc::write_a_row<P, kK0>(a_hi, a_lo, tg, x);
     float y[4];
-    tc::run_chain(net, s0 + L.w_off, s_bias, group, tg, a_hi, a_lo, tmem_d, mbar, phase, y);
+    tc::run_chain<P>(net, s0 + L.w_off, s_bias, group, tg, a_hi, a_lo, tmem_d, mbar, phase, y);
     if (row < n)
       for (int j = 0; j < dout; ++j) Y[row * dout + j] = y[j];
   }
@@ -171,7 +178,7 @@ int get_weight_cache(uint8_t** img, float** bias) {
   std::lock_guard<std::mutex> lk(g_wmutex);
   WeightCache& c = g_wcache[dev];
   if (!c.img) {
-    NIRC_CUDA_TRY(cudaMalloc(&c.img, 160 * 1024));
+    NIRC_CUDA_TRY(cudaMalloc(&c.img, 192 * 1024));
     NIRC_CUDA_TRY(cudaMalloc(&c.bias, tc::kMaxTcLayers * 64 * 4));
   }
   *img = c.img;
@@ -204,9 +211,10 @@ int sm_count() {
 }
 
 // Chooses the number of 128-row groups per CTA that fit in shared memory.
-int tc_groups_for(const tc::TcNet& net, uint32_t extra_per_cta) {
-  for (int g = 2; g >= 1; --g)
-    if (tc::tc_smem_layout(net, g, extra_per_cta).total <= 227u * 1024u) return g;
+int tc_groups_for(const tc::TcNet& net, uint32_t extra_per_group) {
+  const int gmax = net.prec == tc::PrecF16x2::kId ? 4 : 2;
+  for (int g = gmax; g >= 1; --g)
+    if (tc::tc_smem_layout(net, g, g * extra_per_group).total <= 227u * 1024u) return g;
   return 0;
 }
 
@@ -237,8 +245,9 @@ extern "C" int nirc_full_forward(const nirc_spec_t* spec, const float* theta, co
     NIRC_LAUNCH_CHECK("k_full_forward_simt");
     return NIRC_OK;
   }
+  const int prec = precision == 2 ? tc::PrecF16x2::kId : tc::PrecTF32x3::kId;
   tc::TcNet net;
-  if (!tc::tc_net_for(*spec, &net)) {
+  if (!tc::tc_net_for(*spec, &net, prec)) {
     set_last_error("network shape not supported by the tcgen05 path");
     return NIRC_E_UNSUPPORTED;
   }
@@ -255,17 +264,23 @@ extern "C" int nirc_full_forward(const nirc_spec_t* spec, const float* theta, co
   const int64_t ntiles = (n + tc::kTileRows - 1) / tc::kTileRows;
   const int64_t want = (ntiles + ng - 1) / ng;
   const int grid = (int)(want < sm_count() ? want : sm_count());
-  if (ng == 2) {
-    NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)k_full_forward_tc<2>,
+  auto launch = [&](auto kern, int threads) -> int {
+    NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)kern,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-    k_full_forward_tc<2><<<grid, 256, L.total, s>>>(*spec, net, L, theta, img, bias, pos, normal,
-                                                    albedo, rough, dirs, n, Y);
+    kern<<<grid, threads, L.total, s>>>(*spec, net, L, theta, img, bias, pos, normal, albedo,
+                                        rough, dirs, n, Y);
+    return NIRC_OK;
+  };
+  if (prec == tc::PrecF16x2::kId) {
+    if (ng == 4) st = launch(k_full_forward_tc<tc::PrecF16x2, 4>, 512);
+    else if (ng == 3) st = launch(k_full_forward_tc<tc::PrecF16x2, 3>, 384);
+    else if (ng == 2) st = launch(k_full_forward_tc<tc::PrecF16x2, 2>, 256);
+    else st = launch(k_full_forward_tc<tc::PrecF16x2, 1>, 128);
   } else {
-    NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)k_full_forward_tc<1>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-    k_full_forward_tc<1><<<grid, 128, L.total, s>>>(*spec, net, L, theta, img, bias, pos, normal,
-                                                    albedo, rough, dirs, n, Y);
+    if (ng == 2) st = launch(k_full_forward_tc<tc::PrecTF32x3, 2>, 256);
+    else st = launch(k_full_forward_tc<tc::PrecTF32x3, 1>, 128);
   }
+  if (st) return st;
   NIRC_LAUNCH_CHECK("k_full_forward_tc");
   return NIRC_OK;
 }

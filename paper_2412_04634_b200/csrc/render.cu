@@ -26,7 +26,7 @@ namespace nirc {
 int sm_count();
 int pack_weights(const nirc_spec_t& sp, const tc::TcNet& net, const float* theta, cudaStream_t s,
                  uint8_t** img, float** bias);
-int tc_groups_for(const tc::TcNet& net, uint32_t extra_per_cta);
+int tc_groups_for(const tc::TcNet& net, uint32_t extra_per_group);
 bool default_layout(const nirc_spec_t& sp);
 
 using pt::V3;
@@ -315,7 +315,7 @@ struct InferArgs {
 
 constexpr int kMaxVertsPerTile = 64;
 
-template <int NG>
+template <class P, int NG>
 __global__ void __launch_bounds__(NG * 128, 1)
     k_infer_tc(nirc_spec_t sp, tc::TcNet net, tc::TcSmem L, const float* __restrict__ theta,
                const uint8_t* __restrict__ wimg, const float* __restrict__ bias_g, InferArgs a) {
@@ -325,13 +325,13 @@ __global__ void __launch_bounds__(NG * 128, 1)
   const uint32_t s0 = tc::smem_u32(smem);
   const int group = threadIdx.x >> 7;
   const int tg = threadIdx.x & 127;
-  const uint32_t a_hi = s0 + L.a_off + group * tc::kABufBytes;
-  const uint32_t a_lo = a_hi + tc::kAImageBytes;
+  const uint32_t a_hi = s0 + L.a_off + group * L.abuf_bytes;
+  const uint32_t a_lo = a_hi + L.abuf_bytes / 2;
   const uint32_t mbar = s0 + L.bar_off + 8 * (1 + group);
   const uint32_t tmem_d = tmem_base + group * 64;
   const float* s_bias = reinterpret_cast<const float*>(smem + L.bias_off);
   // per-group extra shared memory: surface features + row contributions
-  uint8_t* extra = smem + L.a_off + NG * tc::kABufBytes;
+  uint8_t* extra = smem + L.a_off + NG * L.abuf_bytes;
   float* s_feat = reinterpret_cast<float*>(extra) + group * kMaxVertsPerTile * 24;
   double* s_con = reinterpret_cast<double*>(extra + NG * kMaxVertsPerTile * 24 * 4) +
                   group * 128 * 3;
@@ -373,9 +373,9 @@ __global__ void __launch_bounds__(NG * 128, 1)
 #pragma unroll
       for (int i = 0; i < 48; ++i) x[i] = 0.0f;
     }
-    tc::write_a_row<48>(a_hi, a_lo, tg, x);
+    tc::write_a_row<P, 48>(a_hi, a_lo, tg, x);
     float y[4];
-    tc::run_chain(net, s0 + L.w_off, s_bias, group, tg, a_hi, a_lo, tmem_d, mbar, phase, y);
+    tc::run_chain<P>(net, s0 + L.w_off, s_bias, group, tg, a_hi, a_lo, tmem_d, mbar, phase, y);
     // 3) MLMC combine: cache rows give n(w)*f*cos/pdf, the residual row n(w_cont)
     double c0 = 0.0, c1 = 0.0, c2 = 0.0;
     if (rd.kind == 1) {
@@ -844,31 +844,37 @@ extern "C" int nirc_render(const nirc_scene_t* scene, const double* cam,
     if (!spec || !theta) return NIRC_E_CONFIG;
     const int R = rows_per_vertex(c);
     InferArgs a{w.cv, w.counters, w.result, nullptr, R, 128 / R};
+    const int prec = c.precision == 2 ? tc::PrecF16x2::kId : tc::PrecTF32x3::kId;
     tc::TcNet net;
-    const bool tc_ok = default_layout(*spec) && tc::tc_net_for(*spec, &net);
-    const uint32_t extra = 0;
-    int ng = tc_ok ? tc_groups_for(net, extra) : 0;
+    const bool tc_ok =
+        c.precision != 1 && default_layout(*spec) && tc::tc_net_for(*spec, &net, prec);
+    const uint32_t extra = kMaxVertsPerTile * 24 * 4 + 128 * 3 * 8;
+    const int ng = tc_ok ? tc_groups_for(net, extra) : 0;
     if (ng > 0) {
-      const uint32_t ex = ng * (kMaxVertsPerTile * 24 * 4 + 128 * 3 * 8);
-      ng = tc_groups_for(net, ex);
-      if (ng > 0) {
-        uint8_t* img_w;
-        float* bias;
-        int st = pack_weights(*spec, net, theta, s, &img_w, &bias);
-        if (st) return st;
-        const tc::TcSmem L = tc::tc_smem_layout(net, ng, ng * (kMaxVertsPerTile * 24 * 4 + 128 * 3 * 8));
-        const int grid = sm_count();
-        if (ng == 2) {
-          NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)k_infer_tc<2>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-          k_infer_tc<2><<<grid, 256, L.total, s>>>(*spec, net, L, theta, img_w, bias, a);
-        } else {
-          NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)k_infer_tc<1>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-          k_infer_tc<1><<<grid, 128, L.total, s>>>(*spec, net, L, theta, img_w, bias, a);
-        }
-        NIRC_LAUNCH_CHECK("k_infer_tc");
+      uint8_t* img_w;
+      float* bias;
+      int st = pack_weights(*spec, net, theta, s, &img_w, &bias);
+      if (st) return st;
+      const tc::TcSmem L = tc::tc_smem_layout(net, ng, ng * extra);
+      const int grid = sm_count();
+      auto launch = [&](auto kern, int threads) -> int {
+        NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)kern,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)L.total));
+        kern<<<grid, threads, L.total, s>>>(*spec, net, L, theta, img_w, bias, a);
+        return NIRC_OK;
+      };
+      if (prec == tc::PrecF16x2::kId) {
+        if (ng == 4) st = launch(k_infer_tc<tc::PrecF16x2, 4>, 512);
+        else if (ng == 3) st = launch(k_infer_tc<tc::PrecF16x2, 3>, 384);
+        else if (ng == 2) st = launch(k_infer_tc<tc::PrecF16x2, 2>, 256);
+        else st = launch(k_infer_tc<tc::PrecF16x2, 1>, 128);
+      } else {
+        if (ng == 2) st = launch(k_infer_tc<tc::PrecTF32x3, 2>, 256);
+        else st = launch(k_infer_tc<tc::PrecTF32x3, 1>, 128);
       }
+      if (st) return st;
+      NIRC_LAUNCH_CHECK("k_infer_tc");
     }
     if (ng == 0) {
       // generic layouts: SIMT rows into a row buffer, then per-vertex combine

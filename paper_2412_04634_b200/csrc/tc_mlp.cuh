@@ -1,18 +1,27 @@
-// Fully fused tiny-MLP chain on tcgen05 (3xTF32, fp32 accumulate in TMEM).
+// Fully fused tiny-MLP chain on tcgen05 (fp32 accumulate in TMEM).
 //
 // A "group" is 4 consecutive warps (128 threads, thread tg <-> tile row tg
 // <-> TMEM lane tg).  Each group owns one 128-row A tile in shared memory
-// (tf32 hi + lo images, 32 KB each) and 64 TMEM columns.  Per layer the
-// group's thread 0 issues 3 x K/8 tcgen05.mma (hi*hi, hi*lo, lo*hi) into the
-// TMEM accumulator and commits to the group's mbarrier; the 128 threads then
-// tcgen05.ld their row, add bias, apply ReLU, split into tf32 hi/lo and
-// write the next layer's A tile in place.  Activations never leave SMEM /
-// TMEM.  Weights (hi/lo images of every layer) are staged once per CTA by
-// TMA bulk copy and shared by all groups.
+// (hi + lo operand images) and 64 TMEM columns.  Per layer the group's
+// thread 0 issues 3 x K/Kmma tcgen05.mma (lo*hi... hi*hi, split-precision
+// products) into the TMEM accumulator and commits to the group's mbarrier;
+// the 128 threads then tcgen05.ld their row in 16-column chunks, add bias,
+// apply ReLU, split into hi/lo and write the next layer's A tile in place.
+// Activations never leave SMEM / TMEM.  The weight hi/lo images of every
+// layer are staged once per CTA by TMA bulk copy and shared by all groups.
+//
+// Precision policies (operand split x -> hi + lo, products hi*hi + hi*lo +
+// lo*hi accumulated in fp32; ~2^-22 relative per product):
+//   TF32x3 : kind::tf32, 4-byte operands, K = 8 per MMA, full fp32 range;
+//   F16x2  : kind::f16 with fp16 operands, 2-byte operands, K = 16 per MMA:
+//            half the SMEM and half the MMAs, values must stay below the fp16
+//            range (|x| < 65504); entries below 2^-14 keep ~3e-8 absolute
+//            accuracy.
 //
 // Reference semantics: mlp_forward (pkg/src/nirclab/mlp.py:102-122):
 // z = a W^T + b, ReLU hidden layers, ReLU (NIRC/NRC) or sigmoid (NVC) output.
 #pragma once
+#include <cuda_fp16.h>
 #include "common.cuh"
 #include "tc_common.cuh"
 
@@ -22,21 +31,70 @@ namespace tc {
 constexpr int kTileRows = 128;
 constexpr int kMaxTcLayers = 6;
 constexpr int kGroupThreads = 128;
-constexpr uint32_t kAImageBytes = kTileRows * 64 * 4;   // one of hi/lo, K <= 64
-constexpr uint32_t kABufBytes = 2 * kAImageBytes;        // hi + lo
+
+struct PrecTF32x3 {
+  static constexpr int kElemBytes = 4;
+  static constexpr uint32_t kIdescFmt = (1u << 4) | (2u << 7) | (2u << 10);  // f32 <- tf32 x tf32
+  static constexpr int kId = 0;
+  __device__ static inline void split4(const float* x, uint32_t* hi, uint32_t* lo) {
+    // 4 elements -> one 16-byte chunk each of hi and lo
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float h = tf32_hi(x[q]);
+      hi[q] = __float_as_uint(h);
+      lo[q] = __float_as_uint(x[q] - h);
+    }
+  }
+};
+
+struct PrecF16x2 {
+  static constexpr int kElemBytes = 2;
+  static constexpr uint32_t kIdescFmt = (1u << 4);  // f32 <- f16 x f16
+  static constexpr int kId = 2;
+  __device__ static inline void split8(const float* x, uint32_t* hi, uint32_t* lo) {
+    // 8 elements -> one 16-byte chunk each of hi and lo
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const __half h0 = __float2half_rn(x[2 * q]), h1 = __float2half_rn(x[2 * q + 1]);
+      const __half l0 = __float2half_rn(x[2 * q] - __half2float(h0));
+      const __half l1 = __float2half_rn(x[2 * q + 1] - __half2float(h1));
+      hi[q] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+      lo[q] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+    }
+  }
+};
+
+template <class P>
+struct Geo {
+  static constexpr int kEPC = 16 / P::kElemBytes;      // elements per 16-byte chunk
+  static constexpr int kKmma = 2 * kEPC;               // K per MMA instruction (32 B)
+  static constexpr uint32_t kAImageBytes = kTileRows * 64 * P::kElemBytes;
+  static constexpr uint32_t kABufBytes = 2 * kAImageBytes;  // hi + lo
+};
+
+// byte offset of element (r, k) in a canonical K-major no-swizzle operand
+template <class P>
+__host__ __device__ inline uint32_t op_offset(int r, int k, int rows) {
+  constexpr int E = Geo<P>::kEPC;
+  return (uint32_t)((k / E) * (rows * 16) + (r >> 3) * 128 + (r & 7) * 16 +
+                    (k % E) * P::kElemBytes);
+}
 
 struct TcNet {
-  int nl, out_act;
+  int nl, out_act, prec;
   int K[kMaxTcLayers], N[kMaxTcLayers];
   uint32_t woff[kMaxTcLayers];   // byte offset of layer l's hi image; lo follows
   uint32_t wbytes;               // total image bytes
 };
 
-// Host: geometry of the packed weight image for a spec (0 if unsupported).
-inline bool tc_net_for(const nirc_spec_t& sp, TcNet* net) {
+// Host: geometry of the packed weight image for a spec (false if unsupported).
+inline bool tc_net_for(const nirc_spec_t& sp, TcNet* net, int prec) {
   if (sp.n_layers < 2 || sp.n_layers > kMaxTcLayers) return false;
+  const int eb = prec == PrecF16x2::kId ? 2 : 4;
+  const int kstep = prec == PrecF16x2::kId ? 16 : 8;
   net->nl = sp.n_layers;
   net->out_act = sp.out_act;
+  net->prec = prec;
   uint32_t off = 0;
   for (int l = 0; l < sp.n_layers; ++l) {
     const int din = sp.dims[l], dout = sp.dims[l + 1];
@@ -44,39 +102,57 @@ inline bool tc_net_for(const nirc_spec_t& sp, TcNet* net) {
     if (!last && dout != 64) return false;
     if (last && (dout < 1 || dout > 16)) return false;
     if (din > 64) return false;
-    net->K[l] = (din + 7) / 8 * 8;
+    net->K[l] = (din + kstep - 1) / kstep * kstep;
     net->N[l] = last ? 16 : 64;
     net->woff[l] = off;
-    off += 2u * net->N[l] * net->K[l] * 4u;
+    off += 2u * net->N[l] * net->K[l] * eb;
   }
   net->wbytes = off;
   return true;
 }
 
-// Writes one row (K values, K % 4 == 0) of an A tile as tf32 hi/lo images.
-template <int K>
+// Writes one row (K values, K % 16 == 0) of an A tile as hi/lo images.
+template <class P, int K>
 __device__ __forceinline__ void write_a_row(uint32_t a_hi, uint32_t a_lo, int r, const float* x) {
+  constexpr int E = Geo<P>::kEPC;
 #pragma unroll
-  for (int kc = 0; kc < K / 4; ++kc) {
-    float h[4], l[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      h[q] = tf32_hi(x[kc * 4 + q]);
-      l[q] = x[kc * 4 + q] - h[q];
-    }
-    const uint32_t o = tile_offset(r, kc * 4, kTileRows);
-    st_shared_v4(a_hi + o, h[0], h[1], h[2], h[3]);
-    st_shared_v4(a_lo + o, l[0], l[1], l[2], l[3]);
+  for (int kc = 0; kc < K / E; ++kc) {
+    uint32_t h[4], l[4];
+    if constexpr (E == 4) P::split4(x + kc * E, h, l);
+    else P::split8(x + kc * E, h, l);
+    const uint32_t o = op_offset<P>(r, kc * E, kTileRows);
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a_hi + o), "r"(h[0]), "r"(h[1]),
+                 "r"(h[2]), "r"(h[3])
+                 : "memory");
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a_lo + o), "r"(l[0]), "r"(l[1]),
+                 "r"(l[2]), "r"(l[3])
+                 : "memory");
   }
 }
 
-// Issues one layer: D[128 x N] = A[128 x K] . W[N x K]^T in 3xTF32.
+template <class P>
+__device__ __forceinline__ void mma_issue(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                          uint32_t acc) {
+  if constexpr (P::kId == PrecF16x2::kId) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+  } else {
+    mma_tf32(tmem_d, ad, bd, idesc, acc);
+  }
+}
+
+// Issues one layer: D[128 x N] = A[128 x K] . W[N x K]^T, split precision.
+template <class P>
 __device__ __forceinline__ void issue_layer(const TcNet& net, int l, uint32_t w_base,
                                             uint32_t a_hi, uint32_t a_lo, uint32_t tmem_d) {
   const int K = net.K[l], N = net.N[l];
-  const uint32_t idesc = idesc_tf32(kTileRows, N);
+  const uint32_t idesc =
+      P::kIdescFmt | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTileRows >> 4) << 24);
   const uint32_t w_hi = w_base + net.woff[l];
-  const uint32_t w_lo = w_hi + (uint32_t)(N * K * 4);
+  const uint32_t w_lo = w_hi + (uint32_t)(N * K * P::kElemBytes);
   const uint32_t a_lbo = kTileRows * 16, w_lbo = (uint32_t)N * 16;
   uint32_t acc = 0;
   // small cross terms first, the dominant hi*hi term last
@@ -84,10 +160,10 @@ __device__ __forceinline__ void issue_layer(const TcNet& net, int l, uint32_t w_
   for (int term = 0; term < 3; ++term) {
     const uint32_t A = term == 1 ? a_lo : a_hi;
     const uint32_t B = term == 0 ? w_lo : w_hi;
-    for (int kk = 0; kk < K / 8; ++kk) {
+    for (int kk = 0; kk < K / Geo<P>::kKmma; ++kk) {
       const uint64_t ad = sdesc(A + kk * 2 * a_lbo, a_lbo, 128);
       const uint64_t bd = sdesc(B + kk * 2 * w_lbo, w_lbo, 128);
-      mma_tf32(tmem_d, ad, bd, idesc, acc);
+      mma_issue<P>(tmem_d, ad, bd, idesc, acc);
       acc = 1;
     }
   }
@@ -96,6 +172,7 @@ __device__ __forceinline__ void issue_layer(const TcNet& net, int l, uint32_t w_
 // Runs the whole network for the group's current tile.  Precondition: this
 // thread wrote its row of layer-0 input into (a_hi, a_lo).  On return y[0..3]
 // holds the activated outputs of row tg (only dims[nl] are meaningful).
+template <class P>
 __device__ __forceinline__ void run_chain(const TcNet& net, uint32_t w_base,
                                           const float* __restrict__ s_bias, int group, int tg,
                                           uint32_t a_hi, uint32_t a_lo, uint32_t tmem_d,
@@ -106,7 +183,7 @@ __device__ __forceinline__ void run_chain(const TcNet& net, uint32_t w_base,
   named_bar_sync(1 + group, kGroupThreads);
   if (tg == 0) {
     fence_after();
-    issue_layer(net, 0, w_base, a_hi, a_lo, tmem_d);
+    issue_layer<P>(net, 0, w_base, a_hi, a_lo, tmem_d);
     mma_commit(mbar);
   }
   for (int l = 0; l < net.nl; ++l) {
@@ -115,22 +192,38 @@ __device__ __forceinline__ void run_chain(const TcNet& net, uint32_t w_base,
     fence_after();
     const float* b = s_bias + l * 64;
     if (l < net.nl - 1) {
-      float h[64];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) tmem_ld16(tmem_d + lane_off + q * 16, h + q * 16);
-      tmem_wait_ld();
+      for (int q = 0; q < 4; ++q) {
+        float h[16];
+        tmem_ld16(tmem_d + lane_off + q * 16, h);
+        tmem_wait_ld();
 #pragma unroll
-      for (int j = 0; j < 64; ++j) {
-        const float z = h[j] + b[j];
-        h[j] = z > 0.0f ? z : 0.0f;
+        for (int j = 0; j < 16; ++j) {
+          const float z = h[j] + b[q * 16 + j];
+          h[j] = z > 0.0f ? z : 0.0f;
+        }
+        // 16 columns = 4 (tf32) or 2 (f16) operand chunks
+        constexpr int E = Geo<P>::kEPC;
+#pragma unroll
+        for (int c = 0; c < 16 / E; ++c) {
+          uint32_t hh[4], ll[4];
+          if constexpr (E == 4) P::split4(h + c * E, hh, ll);
+          else P::split8(h + c * E, hh, ll);
+          const uint32_t o = op_offset<P>(tg, q * 16 + c * E, kTileRows);
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a_hi + o), "r"(hh[0]),
+                       "r"(hh[1]), "r"(hh[2]), "r"(hh[3])
+                       : "memory");
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a_lo + o), "r"(ll[0]),
+                       "r"(ll[1]), "r"(ll[2]), "r"(ll[3])
+                       : "memory");
+        }
       }
-      write_a_row<64>(a_hi, a_lo, tg, h);
       fence_proxy_async();
       fence_before();
       named_bar_sync(1 + group, kGroupThreads);
       if (tg == 0) {
         fence_after();
-        issue_layer(net, l + 1, w_base, a_hi, a_lo, tmem_d);
+        issue_layer<P>(net, l + 1, w_base, a_hi, a_lo, tmem_d);
         mma_commit(mbar);
       }
     } else {
@@ -149,17 +242,25 @@ __device__ __forceinline__ void run_chain(const TcNet& net, uint32_t w_base,
 
 // Shared-memory carve-up common to the tensor-core kernels.
 struct TcSmem {
-  uint32_t w_off, bias_off, a_off, bar_off, holder_off, total;
+  uint32_t w_off, bias_off, a_off, abuf_bytes, bar_off, holder_off, total;
 };
 __host__ __device__ inline TcSmem tc_smem_layout(const TcNet& net, int ngroups, uint32_t extra) {
   TcSmem s;
   s.w_off = 0;
+  s.abuf_bytes = 2u * kTileRows * 64 * (net.prec == PrecF16x2::kId ? 2u : 4u);
   s.bias_off = (net.wbytes + 1023u) & ~1023u;
   s.a_off = (s.bias_off + kMaxTcLayers * 64 * 4 + 1023u) & ~1023u;
-  s.bar_off = s.a_off + ngroups * kABufBytes + extra;
+  s.bar_off = s.a_off + ngroups * s.abuf_bytes + extra;
   s.holder_off = s.bar_off + 8 * (1 + ngroups);
   s.total = s.holder_off + 16;
   return s;
+}
+
+__host__ __device__ inline uint32_t tmem_cols_for(int ngroups) {
+  const uint32_t need = 64u * (uint32_t)ngroups;
+  uint32_t c = 32;
+  while (c < need) c <<= 1;
+  return c;
 }
 
 // CTA prologue: barriers, TMEM allocation, weight image by TMA bulk copy.
@@ -174,7 +275,7 @@ __device__ __forceinline__ void tc_prologue(uint8_t* smem, const TcSmem& L, cons
     for (int i = 0; i < 1 + ngroups; ++i) mbar_init(s0 + L.bar_off + 8 * i, 1);
     mbar_init_fence();
   }
-  if ((tid >> 5) == 0) tmem_alloc(smem_u32(holder), ngroups == 1 ? 64u : 128u);
+  if ((tid >> 5) == 0) tmem_alloc(smem_u32(holder), tmem_cols_for(ngroups));
   float* s_bias = reinterpret_cast<float*>(smem + L.bias_off);
   for (int i = tid; i < net.nl * 64; i += blockDim.x) s_bias[i] = bias_g[i];
   fence_before();
@@ -197,7 +298,7 @@ __device__ __forceinline__ void tc_epilogue(uint32_t tmem_base, int ngroups) {
   __syncthreads();
   if ((threadIdx.x >> 5) == 0) {
     fence_after();
-    tmem_dealloc(tmem_base, ngroups == 1 ? 64u : 128u);
+    tmem_dealloc(tmem_base, tmem_cols_for(ngroups));
   }
 }
 

@@ -23,6 +23,10 @@ MODES = {"pt": 0, "two-level": 1, "biased-nirc-bth": 2, "biased-nirc-sph": 3,
          "biased-nrc-sph": 4}
 MAX_DIRS = 28  # OFF_CACHE leaves room for 28 direction pairs per vertex
 
+# network arithmetic of the fused inference (include/nirc_b200.h)
+PRECISION_TF32X3, PRECISION_FP32, PRECISION_F16X2 = 0, 1, 2
+DEFAULT_PRECISION = PRECISION_F16X2
+
 
 @dataclass
 class EstimatorConfig:
@@ -83,7 +87,7 @@ class _RenderWs:
         return cls.buf
 
 
-def _c_cfg(config, scene, spp, seed, frame, cache_on, rows=None):
+def _c_cfg(config, scene, spp, seed, frame, cache_on, rows=None, precision=None):
     mode = MODES[config.mode]
     c = _lib.NircRenderCfg()
     c.mode = mode
@@ -102,11 +106,12 @@ def _c_cfg(config, scene, spp, seed, frame, cache_on, rows=None):
     c.height = int(scene.camera[15])
     r0, r1 = rows if rows is not None else (0, c.height)
     c.row0, c.row1 = int(r0), int(r1)
+    c.precision = DEFAULT_PRECISION if precision is None else int(precision)
     return c
 
 
 def render_device(scene, config=None, cache=None, seed=0, spp=1, frame=0, force_cache=False,
-                  rows=None, out=None):
+                  rows=None, out=None, precision=None):
     """Device-resident render: returns (img, img2, term, queries) CUDA
     tensors of sums (callers divide by spp).  ``rows`` renders a band of
     pixel rows (multi-GPU tiles); ``out`` accumulates into given buffers."""
@@ -119,7 +124,7 @@ def render_device(scene, config=None, cache=None, seed=0, spp=1, frame=0, force_
     cache_on = 0
     if mode == 1 and cache is not None and (force_cache or not cache.is_zero):
         cache_on = 1
-    cfg = _c_cfg(config, scene, spp, seed, frame, cache_on, rows)
+    cfg = _c_cfg(config, scene, spp, seed, frame, cache_on, rows, precision)
     lib = _lib.load()
     ds = scene.device()
     if out is None:
@@ -142,14 +147,14 @@ def render_device(scene, config=None, cache=None, seed=0, spp=1, frame=0, force_
 
 
 def render(scene, config=None, cache=None, seed=0, spp=1, frame=0, v1_map=None,
-           force_cache=False):
+           force_cache=False, precision=None):
     """Render with the configured estimator (estimators.py:173-217)."""
     if config is None:
         config = EstimatorConfig()
     if v1_map is not None and MODES[config.mode] <= 1:
         v1_map = None  # only the *_sph modes read it
     img, img2, term, queries = render_device(scene, config, cache, seed, spp, frame,
-                                             force_cache)
+                                             force_cache, precision=precision)
     img = img.cpu().numpy()
     img2 = img2.cpu().numpy()
     term = term.cpu().numpy()

@@ -28,6 +28,7 @@ ACT_SIGMOID = 1
 
 PRECISION_TF32X3 = 0   # tcgen05.mma kind::tf32, hi/lo split operands
 PRECISION_FP32 = 1     # SIMT fp32 twin
+PRECISION_F16X2 = 2    # tcgen05.mma kind::f16, fp16 hi/lo split operands
 
 NetSpec = namedtuple(
     "NetSpec",

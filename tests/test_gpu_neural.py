@@ -71,7 +71,7 @@ def test_encode_edge_cases(nb):
 
 
 @pytest.mark.parametrize("depth", [2, 4])
-@pytest.mark.parametrize("precision", [0, 1])
+@pytest.mark.parametrize("precision", [0, 1, 2])
 def test_full_forward_matches_reference(nb, golden, depth, precision):
     from paper_2412_04634_b200.mlp import full_forward, init_theta
 
@@ -96,9 +96,11 @@ def test_full_forward_tc_large_and_ragged(nb):
     q = [torch.from_numpy(a).cuda() for a in O.measure_queries(n, seed=9)]
     Yt = full_forward(spec, theta, *q, precision=0)
     Ys = full_forward(spec, theta, *q, precision=1)
+    Yh = full_forward(spec, theta, *q, precision=2)
     torch.cuda.synchronize()
     assert torch.isfinite(Yt).all()
     np.testing.assert_allclose(Yt.cpu().numpy(), Ys.cpu().numpy(), rtol=1e-4, atol=1e-6)
+    np.testing.assert_allclose(Yh.cpu().numpy(), Ys.cpu().numpy(), rtol=1e-4, atol=1e-6)
     # spot rows against the oracle (f32 numpy) too
     rows = np.array([0, 1, 127, 128, 129, n // 2, n - 2, n - 1])
     qo = [a[rows] for a in O.measure_queries(n, seed=9)]
