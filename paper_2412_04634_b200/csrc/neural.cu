@@ -462,130 +462,113 @@ __global__ void k_adam_tick(int64_t* __restrict__ t, const int32_t* __restrict__
 // Batch selection (caches.py:327-329): keys x_i = mix64(K + G*(step*n+i))>>11
 // with K = stream_key(seed, P_SHUFFLE, 0, frame, 0) (rng.py:100-106 puts
 // the stream in the pixel slot); idx = stable argsort(x)[:min(cap, n)].
-// One CTA: radix-select the cap-th key (11-bit digits over 53 bits), then a
-// bitonic sort of the selected (key, index) pairs in shared memory.
-// ----------------------------------------------------------------------
-constexpr int kSelThreads = 1024;
-constexpr int kSelMax = 16384;
-
 __device__ inline uint64_t shuffle_key(uint64_t K, uint64_t dim) {
   return rand_u64(K, dim) >> 11;
 }
 
-__global__ void __launch_bounds__(kSelThreads, 1)
-k_select(uint64_t K, uint64_t offset, int64_t n, int cap, int64_t* __restrict__ idx_out,
-         const int32_t* __restrict__ flags) {
-  extern __shared__ unsigned char sel_smem[];
-  uint64_t* keys = reinterpret_cast<uint64_t*>(sel_smem);
-  int32_t* ids = reinterpret_cast<int32_t*>(keys + kSelMax);
-  __shared__ uint32_t hist[2048];
-  __shared__ uint64_t s_prefix;
-  __shared__ int64_t s_rank;   // rank of the wanted element within the bucket
-  __shared__ int s_count, s_eq_taken;
-  __shared__ int warp_eq[kSelThreads / 32];
+// Multi-CTA exact selection (the production path): bucket the 53-bit keys
+// by their top 12 bits, find the bucket holding rank B-1, scatter every key
+// of the buckets up to it into bucket order, then sort each bucket by
+// (key, index) with one thread per bucket (~n/4096 keys each).  The result
+// is exactly argsort(key, stable)[:B] in O(n) work with no single-CTA pass.
+constexpr int kSelBins = 4096;
+constexpr int kSelShift = 53 - 12;
+
+struct SelWs {
+  uint64_t* keys;      // (n,)
+  uint32_t* hist;      // (kSelBins,)
+  uint32_t* fill;      // (kSelBins,)
+  uint32_t* boff;      // (kSelBins + 1,) exclusive offsets
+  int32_t* bstar;      // [0] last bucket taken, [1] staged count
+  uint64_t* skey;      // staged keys (<= n)
+  int64_t* sidx;       // staged indices (<= n) -- the batch is sidx[0:B]
+};
+
+__global__ void k_sel_hist(uint64_t K, uint64_t offset, int64_t n, SelWs w,
+                           const int32_t* __restrict__ flags) {
+  __shared__ uint32_t h[kSelBins];
   if (flags && (flags[0] & 3)) return;
-  const int tid = threadIdx.x;
-  const int B = (int)(n < cap ? n : cap);
-  int P = 1;
-  while (P < B) P <<= 1;
-  if (n <= cap) {
-    for (int i = tid; i < P; i += kSelThreads) {
-      keys[i] = i < n ? shuffle_key(K, offset + i) : ~0ull;
-      ids[i] = i < n ? i : INT_MAX;
-    }
-  } else {
-    // radix select: find the exact key of rank B-1 (0-based) among n keys.
-    uint64_t prefix = 0;
-    int64_t rank = B - 1;
-    int shift = 53;
-    if (tid == 0) { s_prefix = 0; s_rank = rank; }
-    while (shift > 0) {
-      const int bits = shift >= 11 ? 11 : shift;
-      shift -= bits;
-      for (int i = tid; i < 2048; i += kSelThreads) hist[i] = 0;
-      __syncthreads();
-      prefix = s_prefix;
-      rank = s_rank;
-      const uint64_t hi_mask = (shift + bits >= 64) ? 0 : (~0ull << (shift + bits));
-      for (int64_t i = tid; i < n; i += kSelThreads) {
-        const uint64_t k = shuffle_key(K, offset + i);
-        if ((k & hi_mask) == prefix) atomicAdd(&hist[(k >> shift) & ((1u << bits) - 1)], 1u);
-      }
-      __syncthreads();
-      if (tid == 0) {
-        int64_t acc = 0;
-        for (int d = 0; d < (1 << bits); ++d) {
-          if (acc + hist[d] > rank) {
-            s_prefix = prefix | ((uint64_t)d << shift);
-            s_rank = rank - acc;
-            break;
-          }
-          acc += hist[d];
-        }
-      }
-      __syncthreads();
-    }
-    const uint64_t thr = s_prefix;   // key of rank B-1
-    const int64_t eq_need = s_rank + 1;  // how many keys == thr are taken (stable: lowest ids)
-    if (tid == 0) { s_count = 0; s_eq_taken = 0; }
-    __syncthreads();
-    for (int64_t base = 0; base < n; base += kSelThreads) {
-      const int64_t i = base + tid;
-      uint64_t k = 0;
-      bool less = false, eq = false;
-      if (i < n) {
-        k = shuffle_key(K, offset + i);
-        less = k < thr;
-        eq = k == thr;
-      }
-      // equal keys are taken in index order: rank them within this chunk
-      const unsigned eq_ballot = __ballot_sync(0xffffffffu, eq);
-      const int lane = tid & 31, wid = tid >> 5;
-      if (lane == 0) warp_eq[wid] = __popc(eq_ballot);
-      __syncthreads();
-      int before = s_eq_taken;
-      for (int w = 0; w < wid; ++w) before += warp_eq[w];
-      before += __popc(eq_ballot & ((1u << lane) - 1u));
-      const bool take = less || (eq && before < eq_need);
-      if (take) {
-        const int pos = atomicAdd(&s_count, 1);
-        keys[pos] = k;
-        ids[pos] = (int32_t)i;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        int tot = 0;
-        for (int w = 0; w < kSelThreads / 32; ++w) tot += warp_eq[w];
-        s_eq_taken += tot;
-      }
-      __syncthreads();
-    }
-    for (int i = B + tid; i < P; i += kSelThreads) {
-      keys[i] = ~0ull;
-      ids[i] = INT_MAX;
-    }
+  for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = shuffle_key(K, offset + i);
+    w.keys[i] = k;
+    atomicAdd(&h[k >> kSelShift], 1u);
   }
   __syncthreads();
-  // bitonic sort ascending by (key, id)
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < P; i += kSelThreads) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const bool up = (i & k) == 0;
-          const uint64_t ka = keys[i], kb = keys[ixj];
-          const int32_t ia = ids[i], ib = ids[ixj];
-          const bool gt = (ka > kb) || (ka == kb && ia > ib);
-          if (gt == up) {
-            keys[i] = kb; keys[ixj] = ka;
-            ids[i] = ib; ids[ixj] = ia;
-          }
-        }
-      }
-      __syncthreads();
+  for (int i = threadIdx.x; i < kSelBins; i += blockDim.x)
+    if (h[i]) atomicAdd(&w.hist[i], h[i]);
+}
+
+__global__ void k_sel_scan(int64_t n, int B, SelWs w, const int32_t* __restrict__ flags) {
+  __shared__ uint32_t part[1024];
+  if (flags && (flags[0] & 3)) return;
+  const int t = threadIdx.x;  // 1024 threads x 4 bins
+  uint32_t v[4], s = 0;
+  for (int q = 0; q < 4; ++q) {
+    v[q] = w.hist[t * 4 + q];
+    s += v[q];
+  }
+  part[t] = s;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {  // inclusive Hillis-Steele scan
+    const uint32_t x = t >= off ? part[t - off] : 0u;
+    __syncthreads();
+    part[t] += x;
+    __syncthreads();
+  }
+  uint32_t run = part[t] - s;
+  for (int q = 0; q < 4; ++q) {
+    const int b = t * 4 + q;
+    w.boff[b] = run;
+    w.fill[b] = 0;
+    // the bucket containing rank B-1 (or the last bucket when n <= B)
+    if (run < (uint32_t)B && run + v[q] >= (uint32_t)B) {
+      w.bstar[0] = b;
+      w.bstar[1] = (int32_t)(run + v[q]);
+    }
+    run += v[q];
+  }
+  if (t == 1023) w.boff[kSelBins] = run;
+  if (n <= B && t == 0) {
+    w.bstar[0] = kSelBins - 1;
+    w.bstar[1] = (int32_t)n;
+  }
+}
+
+__global__ void k_sel_scatter(int64_t n, SelWs w, const int32_t* __restrict__ flags) {
+  if (flags && (flags[0] & 3)) return;
+  const int bs = w.bstar[0];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = w.keys[i];
+    const int b = (int)(k >> kSelShift);
+    if (b <= bs) {
+      const uint32_t pos = w.boff[b] + atomicAdd(&w.fill[b], 1u);
+      w.skey[pos] = k;
+      w.sidx[pos] = i;
     }
   }
-  for (int i = tid; i < B; i += kSelThreads) idx_out[i] = ids[i];
+}
+
+__global__ void k_sel_sort(SelWs w, const int32_t* __restrict__ flags) {
+  if (flags && (flags[0] & 3)) return;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b > w.bstar[0]) return;
+  const uint32_t lo = w.boff[b], hi = w.boff[b + 1];
+  for (uint32_t i = lo + 1; i < hi; ++i) {  // insertion sort by (key, index)
+    const uint64_t k = w.skey[i];
+    const int64_t x = w.sidx[i];
+    uint32_t j = i;
+    while (j > lo && (w.skey[j - 1] > k || (w.skey[j - 1] == k && w.sidx[j - 1] > x))) {
+      w.skey[j] = w.skey[j - 1];
+      w.sidx[j] = w.sidx[j - 1];
+      --j;
+    }
+    w.skey[j] = k;
+    w.sidx[j] = x;
+  }
 }
 
 // Gather + encode + forward for the training batch: row i of the batch is
@@ -785,6 +768,7 @@ extern "C" int nirc_adam_step(float* theta, float* m, float* v, const float* gra
 // ---------------------------------------------------------------- train --
 namespace {
 struct TrainWs {
+  SelWs sel;
   int64_t* idx;
   float *X, *zs, *Y, *dY, *dzs, *dX, *grad;
   double* partial;
@@ -792,7 +776,7 @@ struct TrainWs {
   size_t bytes;
 };
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
-TrainWs carve_train(const nirc_spec_t& sp, int64_t B, void* base) {
+TrainWs carve_train(const nirc_spec_t& sp, int64_t n, int64_t B, void* base) {
   TrainWs w{};
   char* p = reinterpret_cast<char*>(base);
   size_t off = 0;
@@ -802,7 +786,14 @@ TrainWs carve_train(const nirc_spec_t& sp, int64_t B, void* base) {
     return r;
   };
   const int zw = zs_width(sp);
-  w.idx = (int64_t*)take(B * 8);
+  w.sel.keys = (uint64_t*)take(n * 8);
+  w.sel.hist = (uint32_t*)take(kSelBins * 4);
+  w.sel.fill = (uint32_t*)take(kSelBins * 4);
+  w.sel.boff = (uint32_t*)take((kSelBins + 1) * 4);
+  w.sel.bstar = (int32_t*)take(16);
+  w.sel.skey = (uint64_t*)take(n * 8);
+  w.sel.sidx = (int64_t*)take(n * 8);
+  w.idx = w.sel.sidx;
   w.X = (float*)take(B * sp.in_dim * 4);
   w.zs = (float*)take(B * zw * 4);
   w.Y = (float*)take(B * 3 * 4 + 16);
@@ -820,7 +811,7 @@ TrainWs carve_train(const nirc_spec_t& sp, int64_t B, void* base) {
 extern "C" int64_t nirc_train_workspace_bytes(const nirc_spec_t* spec, int64_t n_records,
                                               int32_t batch_cap) {
   const int64_t B = n_records < batch_cap ? n_records : batch_cap;
-  return (int64_t)carve_train(*spec, B, nullptr).bytes;
+  return (int64_t)carve_train(*spec, n_records, B, nullptr).bytes;
 }
 
 extern "C" int nirc_train_step(const nirc_spec_t* spec, float* theta, float* m, float* v,
@@ -835,13 +826,9 @@ extern "C" int nirc_train_step(const nirc_spec_t* spec, float* theta, float* m, 
   const int64_t n = rec->n;
   if (n <= 0) { set_last_error("cannot train on an empty record set"); return NIRC_E_CONFIG; }
   if (batch_cap < 1) { set_last_error("batch must be positive"); return NIRC_E_CONFIG; }
-  if (batch_cap > kSelMax && n > kSelMax) {
-    set_last_error("batch cap %d > %d unsupported", batch_cap, kSelMax);
-    return NIRC_E_UNSUPPORTED;
-  }
   if (n > INT_MAX) { set_last_error("too many records"); return NIRC_E_UNSUPPORTED; }
   const int64_t B = n < batch_cap ? n : batch_cap;
-  TrainWs w = carve_train(*spec, B, workspace);
+  TrainWs w = carve_train(*spec, n, B, workspace);
   if ((int64_t)w.bytes > workspace_bytes) {
     set_last_error("train workspace too small (%lld < %lld)", (long long)workspace_bytes,
                    (long long)w.bytes);
@@ -849,11 +836,14 @@ extern "C" int nirc_train_step(const nirc_spec_t* spec, float* theta, float* m, 
   }
   cudaStream_t s = S(stream);
   const uint64_t K = stream_key(seed, P_SHUFFLE, 0, (uint64_t)frame, 0);
-  const size_t sel_smem = kSelMax * (8 + 4);
-  if ((st = set_smem((const void*)k_select, sel_smem))) return st;
-  k_select<<<1, kSelThreads, sel_smem, s>>>(K, (uint64_t)step * (uint64_t)n, n, (int)B,
-                                            w.idx, status_flags);
-  NIRC_LAUNCH_CHECK("k_select");
+  const uint64_t off = (uint64_t)step * (uint64_t)n;
+  NIRC_CUDA_TRY(cudaMemsetAsync(w.sel.hist, 0, kSelBins * 4, s));
+  const int sel_grid = (int)((n + 255) / 256 < 4 * 148 ? (n + 255) / 256 : 4 * 148);
+  k_sel_hist<<<sel_grid, 256, 0, s>>>(K, off, n, w.sel, status_flags);
+  k_sel_scan<<<1, 1024, 0, s>>>(n, (int)B, w.sel, status_flags);
+  k_sel_scatter<<<sel_grid, 256, 0, s>>>(n, w.sel, status_flags);
+  k_sel_sort<<<kSelBins / 128, 128, 0, s>>>(w.sel, status_flags);
+  NIRC_LAUNCH_CHECK("k_sel_*");
   if (batch_idx_out)
     NIRC_CUDA_TRY(cudaMemcpyAsync(batch_idx_out, w.idx, B * 8, cudaMemcpyDeviceToDevice, s));
   const size_t sm = simt_smem_bytes(*spec);
