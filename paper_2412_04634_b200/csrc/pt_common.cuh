@@ -64,7 +64,11 @@ __device__ inline double ray_sph(V3 o, V3 d, V3 c, double r) {
   return -1.0;
 }
 
-__device__ inline bool box_hit(V3 o, V3 d, const double* lo, const double* hi, double t_best) {
+// _box_hit (geometry.py:66-99).  inv_d[a] = 1.0 / d[a] is computed once per
+// ray: it is the same IEEE quotient the reference recomputes per box, so the
+// slab test is bit-identical.
+__device__ inline bool box_hit(V3 o, V3 d, const double* inv_d, const double* lo,
+                               const double* hi, double t_best) {
   double t0 = 0.0, t1 = t_best;
   const double oo[3] = {o.x, o.y, o.z}, dd[3] = {d.x, d.y, d.z};
 #pragma unroll
@@ -72,9 +76,8 @@ __device__ inline bool box_hit(V3 o, V3 d, const double* lo, const double* hi, d
     if (dd[a] > -1e-30 && dd[a] < 1e-30) {
       if (oo[a] < lo[a] || oo[a] > hi[a]) return false;
     } else {
-      const double inv = 1.0 / dd[a];
-      double ta = (lo[a] - oo[a]) * inv;
-      double tb = (hi[a] - oo[a]) * inv;
+      double ta = (lo[a] - oo[a]) * inv_d[a];
+      double tb = (hi[a] - oo[a]) * inv_d[a];
       if (ta > tb) {
         const double s = ta;
         ta = tb;
@@ -105,9 +108,10 @@ __device__ inline Hit intersect(const nirc_scene_t& s, V3 o, V3 d, double t_max)
   int stack[64];
   int top = 0;
   stack[top++] = 0;
+  const double inv_d[3] = {1.0 / d.x, 1.0 / d.y, 1.0 / d.z};
   while (top > 0) {
     const int node = stack[--top];
-    if (!box_hit(o, d, s.bvh_lo + 3 * node, s.bvh_hi + 3 * node, best)) continue;
+    if (!box_hit(o, d, inv_d, s.bvh_lo + 3 * node, s.bvh_hi + 3 * node, best)) continue;
     const int count = s.bvh_b[node];
     if (count > 0) {
       const int first = s.bvh_a[node];
@@ -478,6 +482,48 @@ __device__ inline V3 nee_contrib(const nirc_scene_t& s, V3 p, V3 ns, V3 gn, int 
   }
   const double sc = w * cs / L.pdf;
   return {f.x * L.e.x * sc, f.y * L.e.y * sc, f.z * L.e.z * sc};
+}
+
+// Copies the geometry the traversal touches (triangles, spheres, BVH) into
+// shared memory when it fits and redirects the scene pointers there; the
+// kernel then reads it through generic loads that resolve to shared memory.
+constexpr int kSceneSmemBytes = 40 * 1024;
+
+__host__ __device__ inline size_t scene_smem_bytes(const nirc_scene_t& s) {
+  return (size_t)s.n_tri * (4 * 3 * 8 + 4) + (size_t)s.n_sph * (4 * 8 + 4) +
+         (size_t)s.n_bvh * (6 * 8 + 8) + (size_t)(s.n_tri + s.n_sph) * 4 + 64;
+}
+
+__device__ inline void stage_scene(nirc_scene_t& s, unsigned char* sm) {
+  if (scene_smem_bytes(s) > (size_t)kSceneSmemBytes) return;
+  double* dp = reinterpret_cast<double*>(sm);
+  auto cp = [&](const double* src, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dp[i] = src[i];
+    const double* r = dp;
+    dp += n;
+    return r;
+  };
+  s.tri_v0 = cp(s.tri_v0, 3 * s.n_tri);
+  s.tri_e1 = cp(s.tri_e1, 3 * s.n_tri);
+  s.tri_e2 = cp(s.tri_e2, 3 * s.n_tri);
+  s.tri_ng = cp(s.tri_ng, 3 * s.n_tri);
+  s.sph_c = cp(s.sph_c, 3 * s.n_sph);
+  s.sph_r = cp(s.sph_r, s.n_sph);
+  s.bvh_lo = cp(s.bvh_lo, 3 * s.n_bvh);
+  s.bvh_hi = cp(s.bvh_hi, 3 * s.n_bvh);
+  int* ip = reinterpret_cast<int*>(dp);
+  auto cpi = [&](const int* src, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) ip[i] = src[i];
+    const int* r = ip;
+    ip += n;
+    return r;
+  };
+  s.tri_mat = cpi(s.tri_mat, s.n_tri);
+  s.sph_mat = cpi(s.sph_mat, s.n_sph);
+  s.bvh_a = cpi(s.bvh_a, s.n_bvh);
+  s.bvh_b = cpi(s.bvh_b, s.n_bvh);
+  s.bvh_prim = cpi(s.bvh_prim, s.n_tri + s.n_sph);
+  __syncthreads();
 }
 
 }  // namespace pt

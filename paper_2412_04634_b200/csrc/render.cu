@@ -203,8 +203,10 @@ __device__ inline bool trace_vertex(const nirc_scene_t& scn, const nirc_render_c
 // the next (pixel, sample) from a global counter as soon as its path ends,
 // so lanes stay busy despite Russian-roulette path-length variance (a plain
 // one-thread-per-sample megakernel idles ~80% of each warp).
-__global__ void __launch_bounds__(128) k_trace(nirc_scene_t scn, const double* __restrict__ cam,
-                                               nirc_render_cfg_t cfg, TraceOut out) {
+__global__ void __launch_bounds__(128, 3) k_trace(nirc_scene_t scn, const double* __restrict__ cam,
+                                                  nirc_render_cfg_t cfg, TraceOut out) {
+  __shared__ __align__(16) unsigned char scene_sm[pt::kSceneSmemBytes];
+  pt::stage_scene(scn, scene_sm);
   const int64_t nsamp = (int64_t)(cfg.row1 - cfg.row0) * cfg.width * cfg.spp;
   PathState p;
   bool active = false;
@@ -332,11 +334,10 @@ __global__ void __launch_bounds__(NG * 128, 1)
   const float* s_bias = reinterpret_cast<const float*>(smem + L.bias_off);
   // per-group extra shared memory: surface features + row contributions
   uint8_t* extra = smem + L.a_off + NG * L.abuf_bytes;
-  float* s_feat = reinterpret_cast<float*>(extra) + group * kMaxVertsPerTile * 24;
-  double* s_con = reinterpret_cast<double*>(extra + NG * kMaxVertsPerTile * 24 * 4) +
-                  group * 128 * 3;
-  const uint32_t T = 1u << sp.table_log2;
   const int R = a.rows_per_vertex, S = a.verts_per_tile;
+  double* s_con = reinterpret_cast<double*>(extra) + group * 128 * 3;
+  float* s_feat = reinterpret_cast<float*>(extra + NG * 128 * 3 * 8) + group * S * 24;
+  const uint32_t T = 1u << sp.table_log2;
   const int64_t nverts = (int64_t)a.counters[0];
   const int64_t ntiles = (nverts + S - 1) / S;
   uint32_t phase = 0;
@@ -568,6 +569,8 @@ struct Stage {
 
 __global__ void k_walk_record(nirc_scene_t scn, const double* __restrict__ cam, uint64_t seed,
                               uint64_t frame, Stage st) {
+  __shared__ __align__(16) unsigned char scene_sm[pt::kSceneSmemBytes];
+  pt::stage_scene(scn, scene_sm);
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= st.count) return;
   const int64_t C = st.count;
@@ -848,7 +851,7 @@ extern "C" int nirc_render(const nirc_scene_t* scene, const double* cam,
     tc::TcNet net;
     const bool tc_ok =
         c.precision != 1 && default_layout(*spec) && tc::tc_net_for(*spec, &net, prec);
-    const uint32_t extra = kMaxVertsPerTile * 24 * 4 + 128 * 3 * 8;
+    const uint32_t extra = (uint32_t)(128 * 3 * 8 + a.verts_per_tile * 24 * 4);
     const int ng = tc_ok ? tc_groups_for(net, extra) : 0;
     if (ng > 0) {
       uint8_t* img_w;

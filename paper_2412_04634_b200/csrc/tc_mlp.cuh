@@ -52,14 +52,15 @@ struct PrecF16x2 {
   static constexpr uint32_t kIdescFmt = (1u << 4);  // f32 <- f16 x f16
   static constexpr int kId = 2;
   __device__ static inline void split8(const float* x, uint32_t* hi, uint32_t* lo) {
-    // 8 elements -> one 16-byte chunk each of hi and lo
+    // 8 elements -> one 16-byte chunk each of hi and lo; packed f16x2
+    // conversions (one cvt per pair) keep the epilogue off the slow pipe
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const __half h0 = __float2half_rn(x[2 * q]), h1 = __float2half_rn(x[2 * q + 1]);
-      const __half l0 = __float2half_rn(x[2 * q] - __half2float(h0));
-      const __half l1 = __float2half_rn(x[2 * q + 1] - __half2float(h1));
-      hi[q] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-      lo[q] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+      const __half2 h = __floats2half2_rn(x[2 * q], x[2 * q + 1]);
+      const float2 hf = __half22float2(h);
+      const __half2 l = __floats2half2_rn(x[2 * q] - hf.x, x[2 * q + 1] - hf.y);
+      hi[q] = *reinterpret_cast<const uint32_t*>(&h);
+      lo[q] = *reinterpret_cast<const uint32_t*>(&l);
     }
   }
 };
