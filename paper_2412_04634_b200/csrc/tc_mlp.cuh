@@ -197,10 +197,15 @@ __device__ __forceinline__ void run_chain(const TcNet& net, uint32_t w_base,
       for (int q = 0; q < 4; ++q) {
         float h[16];
         tmem_ld16(tmem_d + lane_off + q * 16, h);
+        float bq[16];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)  // broadcast 16-byte bias loads
+          *reinterpret_cast<float4*>(bq + 4 * j) =
+              *reinterpret_cast<const float4*>(b + q * 16 + 4 * j);
         tmem_wait_ld();
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const float z = h[j] + b[q * 16 + j];
+          const float z = h[j] + bq[j];
           h[j] = z > 0.0f ? z : 0.0f;
         }
         // 16 columns = 4 (tf32) or 2 (f16) operand chunks
