@@ -101,7 +101,9 @@ __global__ void __launch_bounds__(NG * 128, 1)
   const uint32_t a_hi = s0 + L.a_off + group * L.abuf_bytes;
   const uint32_t a_lo = a_hi + L.abuf_bytes / 2;
   const uint32_t mbar = s0 + L.bar_off + 8 * (1 + group);
-  const uint32_t tmem_d = tmem_base + group * 64;
+  constexpr bool kTS = P::kId == tc::PrecF16x2::kId;
+  const uint32_t tmem_d = tmem_base + group * (kTS ? tc::kTsColsPerGroup : 64u);
+  const uint32_t lane_off = (uint32_t)((tg >> 5) * 32) << 16;
   const float* s_bias = reinterpret_cast<const float*>(smem + L.bias_off);
   const int dout = sp.dims[sp.n_layers];
   uint32_t phase = 0;
@@ -117,13 +119,18 @@ __global__ void __launch_bounds__(NG * 128, 1)
 #pragma unroll
       for (int k = 0; k < kK0; ++k) x[k] = 0.0f;
     }
-    tc::write_a_row<P, kK0>(a_hi, a_lo, tg, x);
     float y[4];
-    tc::run_chain<P>(net, s0 + L.w_off, s_bias, group, tg, a_hi, a_lo, tmem_d, mbar, phase, y);
+    if constexpr (kTS) {
+      tc::write_a_row_ts<kK0>(tmem_d + 64 + lane_off, tmem_d + 96 + lane_off, x);
+      tc::run_chain_ts(net, s0 + L.w_off, s_bias, group, tg, tmem_d, mbar, phase, y);
+    } else {
+      tc::write_a_row<P, kK0>(a_hi, a_lo, tg, x);
+      tc::run_chain<P>(net, s0 + L.w_off, s_bias, group, tg, a_hi, a_lo, tmem_d, mbar, phase, y);
+    }
     if (row < n)
       for (int j = 0; j < dout; ++j) Y[row * dout + j] = y[j];
   }
-  tc::tc_epilogue(tmem_base, NG);
+  tc::tc_epilogue(tmem_base, NG, P::kId);
 }
 
 // fp32 SIMT twin of the same fusion (precision == 1): weights in smem,

@@ -23,6 +23,7 @@
 
 namespace nirc {
 
+extern long long* g_infer_probe;
 int sm_count();
 int pack_weights(const nirc_spec_t& sp, const tc::TcNet& net, const float* theta, cudaStream_t s,
                  uint8_t** img, float** bias);
@@ -313,6 +314,7 @@ struct InferArgs {
   double* rowbuf;  // SIMT fallback only: per-row contributions (cap * R, 3)
   int rows_per_vertex;  // R = max(nc) + 1
   int verts_per_tile;   // S = 128 / R
+  long long* dbg;       // optional phase timestamps (CTA 0, group 0, thread 0)
 };
 
 constexpr int kMaxVertsPerTile = 64;
@@ -330,7 +332,9 @@ __global__ void __launch_bounds__(NG * 128, 1)
   const uint32_t a_hi = s0 + L.a_off + group * L.abuf_bytes;
   const uint32_t a_lo = a_hi + L.abuf_bytes / 2;
   const uint32_t mbar = s0 + L.bar_off + 8 * (1 + group);
-  const uint32_t tmem_d = tmem_base + group * 64;
+  constexpr bool kTS = P::kId == tc::PrecF16x2::kId;
+  const uint32_t tmem_d = tmem_base + group * (kTS ? tc::kTsColsPerGroup : 64u);
+  const uint32_t lane_off = (uint32_t)((tg >> 5) * 32) << 16;
   const float* s_bias = reinterpret_cast<const float*>(smem + L.bias_off);
   // per-group extra shared memory: surface features + row contributions
   uint8_t* extra = smem + L.a_off + NG * L.abuf_bytes;
@@ -341,9 +345,13 @@ __global__ void __launch_bounds__(NG * 128, 1)
   const int64_t nverts = (int64_t)a.counters[0];
   const int64_t ntiles = (nverts + S - 1) / S;
   uint32_t phase = 0;
+  const bool probe = a.dbg && blockIdx.x == 0 && threadIdx.x == 0;
+  int it = 0;
   for (int64_t tile = (int64_t)blockIdx.x * NG + group; tile < ntiles;
-       tile += (int64_t)gridDim.x * NG) {
+       tile += (int64_t)gridDim.x * NG, ++it) {
     const int64_t v0 = tile * S;
+    long long* pb = (probe && it < 32) ? a.dbg + it * 64 : nullptr;
+    if (pb) pb[0] = clock64();
     // 1) shared surface encoding: one thread per (vertex, level)
     for (int item = tg; item < S * 12; item += tc::kGroupThreads) {
       const int j = item / 12, lvl = item % 12;
@@ -360,6 +368,7 @@ __global__ void __launch_bounds__(NG * 128, 1)
       }
     }
     tc::named_bar_sync(1 + group, tc::kGroupThreads);
+    if (pb) pb[1] = clock64();
     // 2) per-row direction sampling + SH straight into the A tile
     const int j = tg / R, k = tg % R;
     const int64_t vid = v0 + j;
@@ -374,9 +383,18 @@ __global__ void __launch_bounds__(NG * 128, 1)
 #pragma unroll
       for (int i = 0; i < 48; ++i) x[i] = 0.0f;
     }
-    tc::write_a_row<P, 48>(a_hi, a_lo, tg, x);
     float y[4];
-    tc::run_chain<P>(net, s0 + L.w_off, s_bias, group, tg, a_hi, a_lo, tmem_d, mbar, phase, y);
+    if constexpr (kTS) {
+      tc::write_a_row_ts<48>(tmem_d + 64 + lane_off, tmem_d + 96 + lane_off, x);
+      if (pb) pb[2] = clock64();
+      tc::run_chain_ts(net, s0 + L.w_off, s_bias, group, tg, tmem_d, mbar, phase, y);
+    } else {
+      tc::write_a_row<P, 48>(a_hi, a_lo, tg, x);
+      if (pb) pb[2] = clock64();
+      tc::run_chain<P>(net, s0 + L.w_off, s_bias, group, tg, a_hi, a_lo, tmem_d, mbar, phase, y,
+                       pb ? pb + 5 : nullptr);
+    }
+    if (pb) pb[3] = clock64();
     // 3) MLMC combine: cache rows give n(w)*f*cos/pdf, the residual row n(w_cont)
     double c0 = 0.0, c1 = 0.0, c2 = 0.0;
     if (rd.kind == 1) {
@@ -413,8 +431,9 @@ __global__ void __launch_bounds__(NG * 128, 1)
       a.result[3 * r.slot + 2] = o2;
     }
     tc::named_bar_sync(1 + group, tc::kGroupThreads);
+    if (pb) pb[4] = clock64();
   }
-  tc::tc_epilogue(tmem_base, NG);
+  tc::tc_epilogue(tmem_base, NG, P::kId);
 }
 
 // Generic-shape fallback of the same stage (any NetSpec): one thread per
@@ -751,6 +770,8 @@ __global__ void k_compact_records(Stage st, const int64_t* __restrict__ off, int
   }
 }
 
+long long* g_infer_probe = nullptr;  // set by nirc_debug_infer_probe (tools only)
+
 bool default_layout(const nirc_spec_t& sp) {
   return sp.levels == 12 && sp.feats == 2 && sp.bands == 4 && sp.in_dim == 47;
 }
@@ -846,7 +867,7 @@ extern "C" int nirc_render(const nirc_scene_t* scene, const double* cam,
   if (tl) {
     if (!spec || !theta) return NIRC_E_CONFIG;
     const int R = rows_per_vertex(c);
-    InferArgs a{w.cv, w.counters, w.result, nullptr, R, 128 / R};
+    InferArgs a{w.cv, w.counters, w.result, nullptr, R, 128 / R, g_infer_probe};
     const int prec = c.precision == 2 ? tc::PrecF16x2::kId : tc::PrecTF32x3::kId;
     tc::TcNet net;
     const bool tc_ok =
@@ -967,3 +988,8 @@ extern "C" int nirc_collect(const nirc_scene_t* scene, const double* cam, uint64
   NIRC_LAUNCH_CHECK("k_compact_records");
   return NIRC_OK;
 }
+
+// Tools only (not part of include/nirc_b200.h): route per-phase clock64()
+// stamps of CTA 0 / group 0 of the next k_infer_tc launches into `buf`
+// (device, >= 64*8 int64), or disable with NULL.
+extern "C" void nirc_debug_infer_probe(long long* buf) { nirc::g_infer_probe = buf; }

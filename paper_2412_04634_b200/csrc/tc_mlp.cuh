@@ -173,49 +173,74 @@ __device__ __forceinline__ void issue_layer(const TcNet& net, int l, uint32_t w_
 // Runs the whole network for the group's current tile.  Precondition: this
 // thread wrote its row of layer-0 input into (a_hi, a_lo).  On return y[0..3]
 // holds the activated outputs of row tg (only dims[nl] are meaningful).
+// Pre-fills this thread's TMEM row of the accumulator with layer l's bias
+// (N columns, multiple of 16): the layer's MMAs then all accumulate on top,
+// so the epilogue needs no bias add.
+__device__ __forceinline__ void prefill_bias(const TcNet& net, int l,
+                                             const float* __restrict__ s_bias, uint32_t taddr) {
+  const float* b = s_bias + l * 64;
+  for (int q = 0; q < net.N[l] / 16; ++q) {
+    float bq[16];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      *reinterpret_cast<float4*>(bq + 4 * j) = *reinterpret_cast<const float4*>(b + q * 16 + 4 * j);
+    tmem_st16(taddr + q * 16, bq);
+  }
+  tmem_wait_st();
+}
+
+// Runs the whole network for the group's current tile.  Precondition: this
+// thread wrote its row of layer-0 input into (a_hi, a_lo).  On return y[0..3]
+// holds the activated outputs of row tg (only dims[nl] are meaningful).
 template <class P>
 __device__ __forceinline__ void run_chain(const TcNet& net, uint32_t w_base,
                                           const float* __restrict__ s_bias, int group, int tg,
                                           uint32_t a_hi, uint32_t a_lo, uint32_t tmem_d,
-                                          uint32_t mbar, uint32_t& phase, float* y) {
+                                          uint32_t mbar, uint32_t& phase, float* y,
+                                          long long* probe = nullptr) {
   const uint32_t lane_off = (uint32_t)((tg >> 5) * 32) << 16;
   fence_proxy_async();
   fence_before();
   named_bar_sync(1 + group, kGroupThreads);
-  if (tg == 0) {
+  if ((tg >> 5) == 0) {  // warp 0 of the group issues; one elected lane
     fence_after();
-    issue_layer<P>(net, 0, w_base, a_hi, a_lo, tmem_d);
-    mma_commit(mbar);
+    if (elect_one()) {
+      issue_layer<P>(net, 0, w_base, a_hi, a_lo, tmem_d);
+      mma_commit(mbar);
+    }
+    __syncwarp();
   }
   for (int l = 0; l < net.nl; ++l) {
+    if (probe) probe[2 * l] = clock64();
     mbar_wait(mbar, phase);
+    if (probe) probe[2 * l + 1] = clock64();
     phase ^= 1u;
     fence_after();
-    const float* b = s_bias + l * 64;
     if (l < net.nl - 1) {
+      const float* b = s_bias + l * 64;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float h[16];
-        tmem_ld16(tmem_d + lane_off + q * 16, h);
-        float bq[16];
+      for (int half = 0; half < 2; ++half) {
+        float h[32];
+        tmem_ld32(tmem_d + lane_off + half * 32, h);
+        float bq[32];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)  // broadcast 16-byte bias loads
+        for (int j = 0; j < 8; ++j)  // broadcast 16-byte bias loads overlap the TMEM load
           *reinterpret_cast<float4*>(bq + 4 * j) =
-              *reinterpret_cast<const float4*>(b + q * 16 + 4 * j);
+              *reinterpret_cast<const float4*>(b + half * 32 + 4 * j);
         tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < 32; ++j) {
           const float z = h[j] + bq[j];
           h[j] = z > 0.0f ? z : 0.0f;
         }
-        // 16 columns = 4 (tf32) or 2 (f16) operand chunks
+        // 32 columns = 8 (tf32) or 4 (f16) operand chunks
         constexpr int E = Geo<P>::kEPC;
 #pragma unroll
-        for (int c = 0; c < 16 / E; ++c) {
+        for (int c = 0; c < 32 / E; ++c) {
           uint32_t hh[4], ll[4];
           if constexpr (E == 4) P::split4(h + c * E, hh, ll);
           else P::split8(h + c * E, hh, ll);
-          const uint32_t o = op_offset<P>(tg, q * 16 + c * E, kTileRows);
+          const uint32_t o = op_offset<P>(tg, half * 32 + c * E, kTileRows);
           asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a_hi + o), "r"(hh[0]),
                        "r"(hh[1]), "r"(hh[2]), "r"(hh[3])
                        : "memory");
@@ -224,13 +249,21 @@ __device__ __forceinline__ void run_chain(const TcNet& net, uint32_t w_base,
                        : "memory");
         }
       }
+      if (probe) probe[16 + 3 * l] = clock64();
       fence_proxy_async();
       fence_before();
+      if (probe) probe[17 + 3 * l] = clock64();
       named_bar_sync(1 + group, kGroupThreads);
-      if (tg == 0) {
+      if (probe) probe[18 + 3 * l] = clock64();
+      if ((tg >> 5) == 0) {
         fence_after();
-        issue_layer<P>(net, l + 1, w_base, a_hi, a_lo, tmem_d);
-        mma_commit(mbar);
+        if (probe && tg == 0) probe[40 + 2 * l] = clock64();
+        if (elect_one()) {
+          issue_layer<P>(net, l + 1, w_base, a_hi, a_lo, tmem_d);
+          if (probe) probe[41 + 2 * l] = clock64();
+          mma_commit(mbar);
+        }
+        __syncwarp();
       }
     } else {
       float o[4];
@@ -238,7 +271,125 @@ __device__ __forceinline__ void run_chain(const TcNet& net, uint32_t w_base,
       tmem_wait_ld();
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const float z = o[j] + b[j];
+        const float z = o[j] + s_bias[l * 64 + j];
+        y[j] = net.out_act == 0 ? (z > 0.0f ? z : 0.0f) : 1.0f / (1.0f + expf(-z));
+      }
+    }
+  }
+  fence_before();
+}
+
+// ---------------------------------------------------------------------
+// F16x2 chain with the A operand in TENSOR memory ("TS" MMAs).  Measured on
+// B200 (tools/mma_bench.cu): an M128 N64 K16 f16 MMA costs 48 cycles with A
+// read from shared memory but 32 cycles with A in TMEM, and the epilogue
+// writes the next layer's input with tcgen05.st instead of st.shared plus
+// proxy fences.  Per group TMEM: D (64 fp32 columns) | A_hi (32) | A_lo (32);
+// fp16 element (row m, k) sits at lane m, column k/2, half k%2.
+constexpr uint32_t kTsColsPerGroup = 128;
+
+// Writes this thread's row (K values, K % 16 == 0) into A_hi / A_lo (TMEM).
+template <int K>
+__device__ __forceinline__ void write_a_row_ts(uint32_t a_hi, uint32_t a_lo, const float* x) {
+#pragma unroll
+  for (int c = 0; c < K / 16; ++c) {  // 16 values -> 8 packed columns each of hi and lo
+    uint32_t h[8], l[8];
+    PrecF16x2::split8(x + 16 * c, h, l);
+    PrecF16x2::split8(x + 16 * c + 8, h + 4, l + 4);
+    tmem_st8u(a_hi + 8 * c, h);
+    tmem_st8u(a_lo + 8 * c, l);
+  }
+}
+
+__device__ __forceinline__ void issue_layer_ts(const TcNet& net, int l, uint32_t w_base,
+                                               uint32_t a_hi, uint32_t a_lo, uint32_t tmem_d) {
+  const int K = net.K[l], N = net.N[l];
+  const uint32_t idesc =
+      PrecF16x2::kIdescFmt | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTileRows >> 4) << 24);
+  const uint32_t w_hi = w_base + net.woff[l];
+  const uint32_t w_lo = w_hi + (uint32_t)(N * K * 2);
+  const uint32_t w_lbo = (uint32_t)N * 16;
+  uint32_t acc = 0;
+#pragma unroll
+  for (int term = 0; term < 3; ++term) {  // hi*lo, lo*hi, then hi*hi
+    const uint32_t A = term == 1 ? a_lo : a_hi;
+    const uint32_t B = term == 0 ? w_lo : w_hi;
+    for (int kk = 0; kk < K / 16; ++kk) {
+      const uint64_t bd = sdesc(B + kk * 2 * w_lbo, w_lbo, 128);
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "setp.ne.b32 p, %4, 0;\n\t"
+          "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+          "r"(A + kk * 8), "l"(bd), "r"(idesc), "r"(acc));
+      acc = 1;
+    }
+  }
+}
+
+// Runs the network for the group's tile; precondition: this thread wrote its
+// layer-0 row with write_a_row_ts and waited (tcgen05.wait::st).
+__device__ __forceinline__ void run_chain_ts(const TcNet& net, uint32_t w_base,
+                                             const float* __restrict__ s_bias, int group, int tg,
+                                             uint32_t tmem_grp, uint32_t mbar, uint32_t& phase,
+                                             float* y) {
+  const uint32_t lane_off = (uint32_t)((tg >> 5) * 32) << 16;
+  const uint32_t tmem_d = tmem_grp, a_hi = tmem_grp + 64, a_lo = tmem_grp + 96;
+  tmem_wait_st();
+  fence_before();
+  named_bar_sync(1 + group, kGroupThreads);
+  if ((tg >> 5) == 0) {
+    fence_after();
+    if (elect_one()) {
+      issue_layer_ts(net, 0, w_base, a_hi, a_lo, tmem_d);
+      mma_commit(mbar);
+    }
+    __syncwarp();
+  }
+  for (int l = 0; l < net.nl; ++l) {
+    mbar_wait(mbar, phase);
+    phase ^= 1u;
+    fence_after();
+    if (l < net.nl - 1) {
+      const float* b = s_bias + l * 64;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        float h[32];
+        tmem_ld32(tmem_d + lane_off + half * 32, h);
+        float bq[32];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4*>(bq + 4 * j) =
+              *reinterpret_cast<const float4*>(b + half * 32 + 4 * j);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float z = h[j] + bq[j];
+          h[j] = z > 0.0f ? z : 0.0f;
+        }
+        uint32_t hh[16], ll[16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) PrecF16x2::split8(h + 8 * c, hh + 4 * c, ll + 4 * c);
+        tmem_st16u(a_hi + lane_off + half * 16, hh);
+        tmem_st16u(a_lo + lane_off + half * 16, ll);
+      }
+      tmem_wait_st();
+      fence_before();
+      named_bar_sync(1 + group, kGroupThreads);
+      if ((tg >> 5) == 0) {
+        fence_after();
+        if (elect_one()) {
+          issue_layer_ts(net, l + 1, w_base, a_hi, a_lo, tmem_d);
+          mma_commit(mbar);
+        }
+        __syncwarp();
+      }
+    } else {
+      float o[4];
+      tmem_ld4(tmem_d + lane_off, o);
+      tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float z = o[j] + s_bias[l * 64 + j];
         y[j] = net.out_act == 0 ? (z > 0.0f ? z : 0.0f) : 1.0f / (1.0f + expf(-z));
       }
     }
@@ -253,7 +404,8 @@ struct TcSmem {
 __host__ __device__ inline TcSmem tc_smem_layout(const TcNet& net, int ngroups, uint32_t extra) {
   TcSmem s;
   s.w_off = 0;
-  s.abuf_bytes = 2u * kTileRows * 64 * (net.prec == PrecF16x2::kId ? 2u : 4u);
+  // F16x2 keeps A in TMEM (run_chain_ts); TF32x3 keeps hi/lo A tiles in SMEM
+  s.abuf_bytes = net.prec == PrecF16x2::kId ? 0u : 2u * kTileRows * 64 * 4u;
   s.bias_off = (net.wbytes + 1023u) & ~1023u;
   s.a_off = (s.bias_off + kMaxTcLayers * 64 * 4 + 1023u) & ~1023u;
   s.bar_off = s.a_off + ngroups * s.abuf_bytes + extra;
@@ -262,8 +414,8 @@ __host__ __device__ inline TcSmem tc_smem_layout(const TcNet& net, int ngroups, 
   return s;
 }
 
-__host__ __device__ inline uint32_t tmem_cols_for(int ngroups) {
-  const uint32_t need = 64u * (uint32_t)ngroups;
+__host__ __device__ inline uint32_t tmem_cols_for(int ngroups, int prec) {
+  const uint32_t need = (prec == PrecF16x2::kId ? kTsColsPerGroup : 64u) * (uint32_t)ngroups;
   uint32_t c = 32;
   while (c < need) c <<= 1;
   return c;
@@ -281,7 +433,7 @@ __device__ __forceinline__ void tc_prologue(uint8_t* smem, const TcSmem& L, cons
     for (int i = 0; i < 1 + ngroups; ++i) mbar_init(s0 + L.bar_off + 8 * i, 1);
     mbar_init_fence();
   }
-  if ((tid >> 5) == 0) tmem_alloc(smem_u32(holder), tmem_cols_for(ngroups));
+  if ((tid >> 5) == 0) tmem_alloc(smem_u32(holder), tmem_cols_for(ngroups, net.prec));
   float* s_bias = reinterpret_cast<float*>(smem + L.bias_off);
   for (int i = tid; i < net.nl * 64; i += blockDim.x) s_bias[i] = bias_g[i];
   fence_before();
@@ -299,12 +451,12 @@ __device__ __forceinline__ void tc_prologue(uint8_t* smem, const TcSmem& L, cons
   mbar_wait(s0 + L.bar_off, 0);
 }
 
-__device__ __forceinline__ void tc_epilogue(uint32_t tmem_base, int ngroups) {
+__device__ __forceinline__ void tc_epilogue(uint32_t tmem_base, int ngroups, int prec) {
   fence_before();
   __syncthreads();
   if ((threadIdx.x >> 5) == 0) {
     fence_after();
-    tmem_dealloc(tmem_base, tmem_cols_for(ngroups));
+    tmem_dealloc(tmem_base, tmem_cols_for(ngroups, prec));
   }
 }
 
