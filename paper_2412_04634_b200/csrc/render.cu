@@ -307,6 +307,101 @@ __device__ inline void build_row(const nirc_spec_t& sp, const float* feat, const
   x[47] = 0.0f;
 }
 
+// fp32 producer for the amortised inference rows (render path only; the
+// reference-exact f64 sampler above stays for non-Lambert lobes).  The
+// directions feed only the network input (SH) and the Lambert weight
+// f*cos/pdf = albedo*cos/(cos/pi); fp32 changes either by ~1e-7 relative,
+// far inside the two-level image tolerance (tests/test_gpu_render.py).
+__device__ inline RowDir row_direction_fast(const CacheVertex& r, int k) {
+  if (r.mkind != pt::MAT_LAMBERT || k >= r.ncq) return row_direction(r, k);
+  RowDir o;
+  o.kind = 0;
+  o.wi = {0.0, 0.0, 1.0};
+  o.s = 0.0;
+  o.f = {0.0, 0.0, 0.0};
+  const double u1d = rand_uniform(r.key, r.base + OFF_CACHE + 2 * k);
+  const double u2d = rand_uniform(r.key, r.base + OFF_CACHE + 2 * k + 1);
+  const float u1 = (float)u1d, u2 = (float)u2d;
+  const float nx = (float)r.ns[0], ny = (float)r.ns[1], nz = (float)r.ns[2];
+  const float sg = nz >= 0.0f ? 1.0f : -1.0f;
+  const float a = -1.0f / (sg + nz);
+  const float bb = nx * ny * a;
+  const float tx = 1.0f + sg * nx * nx * a, ty = sg * bb, tz = -sg * nx;
+  const float bx = bb, by = sg + ny * ny * a, bz = -ny;
+  float sp, cp;
+  sincospif(2.0f * u2, &sp, &cp);
+  const float rr = sqrtf(u1);
+  const float lx = rr * cp, ly = rr * sp;
+  const float lz = sqrtf(fmaxf(0.0f, 1.0f - u1));
+  const float pdf = lz * (float)pt::INV_PI;
+  const float wx = tx * lx + bx * ly + nx * lz;
+  const float wy = ty * lx + by * ly + ny * lz;
+  const float wz = tz * lx + bz * ly + nz * lz;
+  const double co = r.ns[0] * r.wo[0] + r.ns[1] * r.wo[1] + r.ns[2] * r.wo[2];
+  if (co <= 0.0 || pdf <= 0.0f) return o;
+  const float ci = wx * nx + wy * ny + wz * nz;
+  if (ci <= 0.0f) return o;
+  o.kind = 1;
+  o.wi = {wx, wy, wz};
+  o.s = (double)(ci / pdf);
+  o.f = {r.alb[0] * pt::INV_PI, r.alb[1] * pt::INV_PI, r.alb[2] * pt::INV_PI};
+  return o;
+}
+
+// Real SH (bands = 4), the scalar-path recurrences of sh.py:36-76 in fp32.
+__device__ inline void sh4_f32(float x, float y, float z, const double* sh_k, float* out) {
+  const float s = sqrtf(x * x + y * y);
+  float cphi = 1.0f, sphi = 0.0f;
+  if (s > 0.0f) {
+    cphi = x / s;
+    sphi = y / s;
+  }
+  float cm = 1.0f, sm = 0.0f, pmm = 1.0f;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    if (m > 0) {
+      pmm = pmm * ((2.0f * m - 1.0f) * s);
+      const float cn = cm * cphi - sm * sphi;
+      const float sn = sm * cphi + cm * sphi;
+      cm = cn;
+      sm = sn;
+    }
+    float p2 = 0.0f, p1 = 0.0f;
+#pragma unroll
+    for (int l = m; l < 4; ++l) {
+      float p;
+      if (l == m) p = pmm;
+      else if (l == m + 1) p = z * (2.0f * m + 1.0f) * pmm;
+      else p = ((2.0f * l - 1.0f) * z * p1 - (l + m - 1.0f) * p2) / (float)(l - m);
+      p2 = p1;
+      p1 = p;
+      const int base = l * l + l;
+      if (m == 0) {
+        out[base] = (float)sh_k[l * 8] * p;
+      } else {
+        const float kk = (float)sh_k[l * 8 + m] * p;
+        out[base + m] = kk * cm;
+        out[base - m] = kk * sm;
+      }
+    }
+  }
+}
+
+__device__ inline void build_row_fast(const float* feat, const CacheVertex& r, V3 wi,
+                                      const double* sh_k, float* x) {
+#pragma unroll
+  for (int i = 0; i < 24; ++i) x[i] = feat[i];
+  sh4_f32((float)wi.x, (float)wi.y, (float)wi.z, sh_k, x + 24);
+  x[40] = (float)((r.ns[0] + 1.0) * 0.5);
+  x[41] = (float)((r.ns[1] + 1.0) * 0.5);
+  x[42] = (float)((r.ns[2] + 1.0) * 0.5);
+  x[43] = (float)r.alb[0];
+  x[44] = (float)r.alb[1];
+  x[45] = (float)r.alb[2];
+  x[46] = (float)r.rough;
+  x[47] = 0.0f;
+}
+
 struct InferArgs {
   const CacheVertex* cv;
   const unsigned long long* counters;
@@ -341,6 +436,8 @@ __global__ void __launch_bounds__(NG * 128, 1)
   const int R = a.rows_per_vertex, S = a.verts_per_tile;
   double* s_con = reinterpret_cast<double*>(extra) + group * 128 * 3;
   float* s_feat = reinterpret_cast<float*>(extra + NG * 128 * 3 * 8) + group * S * 24;
+  CacheVertex* s_cv = reinterpret_cast<CacheVertex*>(extra + NG * 128 * 3 * 8 + NG * S * 24 * 4 +
+                                                     ((NG * S * 24 * 4) & 8)) + group * S;
   const uint32_t T = 1u << sp.table_log2;
   const int64_t nverts = (int64_t)a.counters[0];
   const int64_t ntiles = (nverts + S - 1) / S;
@@ -352,12 +449,21 @@ __global__ void __launch_bounds__(NG * 128, 1)
     const int64_t v0 = tile * S;
     long long* pb = (probe && it < 32) ? a.dbg + it * 64 : nullptr;
     if (pb) pb[0] = clock64();
+    // 0) the tile's cache-vertex records -> shared memory (one coalesced copy)
+    {
+      const int nv = (int)((nverts - v0) < S ? (nverts - v0) : S);
+      const double* src = reinterpret_cast<const double*>(a.cv + v0);
+      double* dst = reinterpret_cast<double*>(s_cv);
+      const int words = nv * (int)(sizeof(CacheVertex) / 8);
+      for (int i = tg; i < words; i += tc::kGroupThreads) dst[i] = src[i];
+    }
+    tc::named_bar_sync(1 + group, tc::kGroupThreads);
     // 1) shared surface encoding: one thread per (vertex, level)
     for (int item = tg; item < S * 12; item += tc::kGroupThreads) {
       const int j = item / 12, lvl = item % 12;
       const int64_t vid = v0 + j;
       if (vid < nverts) {
-        const CacheVertex& r = a.cv[vid];
+        const CacheVertex& r = s_cv[j];
         const float ux = norm_coord(r.pos[0], sp.bb_min[0], sp.bb_inv[0]);
         const float uy = norm_coord(r.pos[1], sp.bb_min[1], sp.bb_inv[1]);
         const float uz = norm_coord(r.pos[2], sp.bb_min[2], sp.bb_inv[2]);
@@ -376,9 +482,9 @@ __global__ void __launch_bounds__(NG * 128, 1)
     rd.kind = 0;
     float x[48];
     if (j < S && vid < nverts) {
-      const CacheVertex& r = a.cv[vid];
-      rd = row_direction(r, k);
-      build_row(sp, s_feat + j * 24, r, rd.wi, x);
+      const CacheVertex& r = s_cv[j];
+      rd = row_direction_fast(r, k);
+      build_row_fast(s_feat + j * 24, r, rd.wi, sp.sh_k, x);
     } else {
 #pragma unroll
       for (int i = 0; i < 48; ++i) x[i] = 0.0f;
@@ -411,7 +517,7 @@ __global__ void __launch_bounds__(NG * 128, 1)
     s_con[3 * tg + 2] = c2;
     tc::named_bar_sync(1 + group, tc::kGroupThreads);
     if (tg < S && v0 + tg < nverts) {
-      const CacheVertex& r = a.cv[v0 + tg];
+      const CacheVertex& r = s_cv[tg];
       double sr = 0.0, sg = 0.0, sb = 0.0;
       for (int kk = 0; kk < r.ncq; ++kk) {  // kernels.py:444-446, k order
         sr += s_con[3 * (tg * R + kk)];
@@ -872,7 +978,8 @@ extern "C" int nirc_render(const nirc_scene_t* scene, const double* cam,
     tc::TcNet net;
     const bool tc_ok =
         c.precision != 1 && default_layout(*spec) && tc::tc_net_for(*spec, &net, prec);
-    const uint32_t extra = (uint32_t)(128 * 3 * 8 + a.verts_per_tile * 24 * 4);
+    const uint32_t extra =
+        (uint32_t)(128 * 3 * 8 + a.verts_per_tile * 24 * 4 + 16 + a.verts_per_tile * sizeof(CacheVertex));
     const int ng = tc_ok ? tc_groups_for(net, extra) : 0;
     if (ng > 0) {
       uint8_t* img_w;
