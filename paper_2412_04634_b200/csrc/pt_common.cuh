@@ -100,11 +100,31 @@ struct Hit {
 // intersect_bvh (geometry.py:153-202): nearest hit with t in (eps, t_max).
 // any_hit stops at the first accepted primitive (occlusion queries only
 // need the boolean, which is identical).
+// Scenes up to this many primitives are intersected by a warp-uniform scan
+// over the BVH's primitive order instead of a per-lane stack traversal: every
+// lane runs the same loop (no divergence; broadcast shared-memory reads), and
+// the test order is the BVH's depth-first leaf order, so exact ties resolve
+// to the same primitive.
+constexpr int kLinearMaxPrims = 64;
+
 template <bool AnyHit>
 __device__ inline Hit intersect(const nirc_scene_t& s, V3 o, V3 d, double t_max) {
   const double eps = s.eps;
   double best = t_max;
   int kind = -1, prim = -1;
+  if (s.n_tri + s.n_sph <= kLinearMaxPrims && s.n_sph == 0) {
+    const int np = s.n_tri;
+    for (int k = 0; k < np; ++k) {
+      const int pid = s.bvh_prim[k];
+      const double t = ray_tri(o, d, ld3(s.tri_v0, pid), ld3(s.tri_e1, pid), ld3(s.tri_e2, pid));
+      if (t > eps && t < best) {
+        best = t;
+        kind = 0;
+        prim = pid;
+        if (AnyHit) break;
+      }
+    }
+  } else {
   int stack[64];
   int top = 0;
   stack[top++] = 0;
@@ -144,6 +164,7 @@ __device__ inline Hit intersect(const nirc_scene_t& s, V3 o, V3 d, double t_max)
       stack[top++] = s.bvh_a[node];
       stack[top++] = node + 1;
     }
+  }
   }
   Hit h;
   h.kind = kind;
