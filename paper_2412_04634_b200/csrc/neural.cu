@@ -467,12 +467,12 @@ __device__ inline uint64_t shuffle_key(uint64_t K, uint64_t dim) {
 }
 
 // Multi-CTA exact selection (the production path): bucket the 53-bit keys
-// by their top 12 bits, find the bucket holding rank B-1, scatter every key
+// by their top 14 bits, find the bucket holding rank B-1, scatter every key
 // of the buckets up to it into bucket order, then sort each bucket by
 // (key, index) with one thread per bucket (~n/4096 keys each).  The result
 // is exactly argsort(key, stable)[:B] in O(n) work with no single-CTA pass.
-constexpr int kSelBins = 4096;
-constexpr int kSelShift = 53 - 12;
+constexpr int kSelBins = 16384;
+constexpr int kSelShift = 53 - 14;
 
 struct SelWs {
   uint64_t* keys;      // (n,)
@@ -486,7 +486,7 @@ struct SelWs {
 
 __global__ void k_sel_hist(uint64_t K, uint64_t offset, int64_t n, SelWs w,
                            const int32_t* __restrict__ flags) {
-  __shared__ uint32_t h[kSelBins];
+  extern __shared__ uint32_t h[];  // kSelBins
   if (flags && (flags[0] & 3)) return;
   for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) h[i] = 0;
   __syncthreads();
@@ -504,10 +504,11 @@ __global__ void k_sel_hist(uint64_t K, uint64_t offset, int64_t n, SelWs w,
 __global__ void k_sel_scan(int64_t n, int B, SelWs w, const int32_t* __restrict__ flags) {
   __shared__ uint32_t part[1024];
   if (flags && (flags[0] & 3)) return;
-  const int t = threadIdx.x;  // 1024 threads x 4 bins
-  uint32_t v[4], s = 0;
-  for (int q = 0; q < 4; ++q) {
-    v[q] = w.hist[t * 4 + q];
+  const int t = threadIdx.x;  // 1024 threads x 16 bins
+  constexpr int kPer = kSelBins / 1024;
+  uint32_t v[kPer], s = 0;
+  for (int q = 0; q < kPer; ++q) {
+    v[q] = w.hist[t * kPer + q];
     s += v[q];
   }
   part[t] = s;
@@ -519,8 +520,8 @@ __global__ void k_sel_scan(int64_t n, int B, SelWs w, const int32_t* __restrict_
     __syncthreads();
   }
   uint32_t run = part[t] - s;
-  for (int q = 0; q < 4; ++q) {
-    const int b = t * 4 + q;
+  for (int q = 0; q < kPer; ++q) {
+    const int b = t * kPer + q;
     w.boff[b] = run;
     w.fill[b] = 0;
     // the bucket containing rank B-1 (or the last bucket when n <= B)
@@ -631,6 +632,15 @@ __global__ void k_train_scatter(nirc_spec_t sp, nirc_records_t rec,
   }
 }
 
+}  // namespace nirc
+
+namespace nirc {
+bool fused_supported(const nirc_spec_t& sp);
+size_t fused_smem_bytes(const nirc_spec_t& sp);
+int launch_fused_train(const nirc_spec_t& sp, const float* theta, const nirc_records_t& rec,
+                       const int64_t* idx, int64_t B, int loss_kind, double loss_eps,
+                       float* grad, float* partials, double* loss_part, double* loss_out,
+                       int32_t* flags, int32_t* adam_bad, cudaStream_t s);
 }  // namespace nirc
 
 using namespace nirc;
@@ -773,6 +783,8 @@ struct TrainWs {
   float *X, *zs, *Y, *dY, *dzs, *dX, *grad;
   double* partial;
   int32_t* adam_bad;
+  float* fpart;      // fused path: per-tile MLP gradient partials
+  double* floss;     // fused path: per-tile loss partials
   size_t bytes;
 };
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -803,6 +815,9 @@ TrainWs carve_train(const nirc_spec_t& sp, int64_t n, int64_t B, void* base) {
   w.grad = (float*)take(sp.theta_len * 4);
   w.partial = (double*)take((B / kLossThreads + 2) * 3 * 8);
   w.adam_bad = (int32_t*)take(16);
+  const int64_t ntiles = (B + 63) / 64;
+  w.fpart = (float*)take(ntiles * (sp.theta_len - sp.grid_len) * 4);
+  w.floss = (double*)take(ntiles * 8);
   w.bytes = off;
   return w;
 }
@@ -839,13 +854,29 @@ extern "C" int nirc_train_step(const nirc_spec_t* spec, float* theta, float* m, 
   const uint64_t off = (uint64_t)step * (uint64_t)n;
   NIRC_CUDA_TRY(cudaMemsetAsync(w.sel.hist, 0, kSelBins * 4, s));
   const int sel_grid = (int)((n + 255) / 256 < 4 * 148 ? (n + 255) / 256 : 4 * 148);
-  k_sel_hist<<<sel_grid, 256, 0, s>>>(K, off, n, w.sel, status_flags);
+  NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)k_sel_hist,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSelBins * 4));
+  k_sel_hist<<<sel_grid, 256, kSelBins * 4, s>>>(K, off, n, w.sel, status_flags);
   k_sel_scan<<<1, 1024, 0, s>>>(n, (int)B, w.sel, status_flags);
   k_sel_scatter<<<sel_grid, 256, 0, s>>>(n, w.sel, status_flags);
   k_sel_sort<<<kSelBins / 128, 128, 0, s>>>(w.sel, status_flags);
   NIRC_LAUNCH_CHECK("k_sel_*");
   if (batch_idx_out)
     NIRC_CUDA_TRY(cudaMemcpyAsync(batch_idx_out, w.idx, B * 8, cudaMemcpyDeviceToDevice, s));
+  if ((loss_kind == 0 || loss_kind == 1) && fused_supported(*spec) &&
+      fused_smem_bytes(*spec) <= 227 * 1024) {
+    // one fused kernel per step: encode, forward, loss, backward, scatter
+    if ((st = launch_fused_train(*spec, theta, *rec, w.idx, B, loss_kind, loss_eps, w.grad,
+                                 w.fpart, w.floss, loss_out, status_flags, w.adam_bad, s)))
+      return st;
+    const int nb = 148 * 4;
+    k_adam_apply<<<nb, 256, 0, s>>>(theta, m, v, w.grad, spec->theta_len, t, skipped, (float)lr,
+                                    0.9, 0.99, (float)1e-8, w.adam_bad, status_flags);
+    NIRC_LAUNCH_CHECK("k_adam_apply");
+    k_adam_tick<<<1, 1, 0, s>>>(t, w.adam_bad, status_flags);
+    NIRC_LAUNCH_CHECK("k_adam_tick");
+    return NIRC_OK;
+  }
   const size_t sm = simt_smem_bytes(*spec);
   if ((st = set_smem((const void*)k_train_forward, sm))) return st;
   k_train_forward<<<blocks_for(B, kRowsPerBlock), kRowsPerBlock, sm, s>>>(
