@@ -178,13 +178,17 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------- frame leg -------
-def frame_bench(frames, warmup, width=1920, height=1080, nc=(16,)):
+def frame_bench(frames, warmup, width=1920, height=1080, nc=(16,), comm=None):
     """BASELINE config 3: Cornell at 1920x1080, two-level with nc=(16,) at
     the first cache vertex, spp 1, D = 4 cache; then collect ceil(0.025 W H)
     training paths and 4 Adam steps of 16384 records.  Device time per
-    phase with CUDA events; frames after `warmup` are timed."""
+    phase with CUDA events; frames after `warmup` are timed.  With a
+    multi-rank `comm` the frame is sharded (distributed.py: pixel-row bands,
+    path shards + record all-gather, tile shards + gradient all-reduce) and
+    each phase time is the max over ranks."""
     import torch
 
+    from paper_2412_04634_b200 import distributed as D
     from paper_2412_04634_b200.caches import Cache, default_train_count, train_frame
     from paper_2412_04634_b200.estimators import render_device
     from paper_2412_04634_b200.frame import config3
@@ -197,34 +201,61 @@ def frame_bench(frames, warmup, width=1920, height=1080, nc=(16,)):
     phases = {"render": [], "collect": [], "train": [], "frame": []}
     queries, records = [], []
     count = default_train_count(scene)
+    world = comm.world if comm is not None else 1
+    ops = D.DeviceOps() if world > 1 else None
     for f in range(warmup + frames):
+        if comm is not None:
+            comm.barrier()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         ev[0].record(stream)
-        _, _, _, q = render_device(scene, cfg, cache, seed=0, spp=1, frame=f)
+        if world > 1:
+            _, _, _, q, _ = D.render_band(scene, cfg, cache, comm, seed=0, spp=1, frame=f)
+        else:
+            _, _, _, q = render_device(scene, cfg, cache, seed=0, spp=1, frame=f)
         ev[1].record(stream)
-        rec = cache.collect(count=count, frame=f)
+        if world > 1:
+            rec = D.collect_sharded(cache, comm, count=count, frame=f, ops=ops)
+        else:
+            rec = cache.collect(count=count, frame=f)
         ev[2].record(stream)
-        train_frame(cache, rec, steps=4)
+        if world > 1:
+            D.train_frame_sharded(cache, rec, comm, steps=4, ops=ops)
+        else:
+            train_frame(cache, rec, steps=4)
         ev[3].record(stream)
         torch.cuda.synchronize()
         if f >= warmup:
-            phases["render"].append(ev[0].elapsed_time(ev[1]))
-            phases["collect"].append(ev[1].elapsed_time(ev[2]))
-            phases["train"].append(ev[2].elapsed_time(ev[3]))
-            phases["frame"].append(ev[0].elapsed_time(ev[3]))
-            queries.append(int(q.item()))
+            t = torch.tensor([ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]),
+                              ev[2].elapsed_time(ev[3]), ev[0].elapsed_time(ev[3])],
+                             device="cuda")
+            if comm is not None:
+                comm.all_reduce_max_(t)
+            t = t.tolist()
+            for k, v in zip(("render", "collect", "train", "frame"), t):
+                phases[k].append(v)
+            qt = q.clone()
+            if comm is not None:
+                comm.all_reduce_sum_(qt)
+            queries.append(int(qt.item()))
             records.append(len(rec))
+    if world > 1:
+        same = D.replicas_identical(cache, comm)
+    else:
+        same = True
     med = {k: sorted(v)[len(v) // 2] for k, v in phases.items()}
     return {
         "metric": "ms_per_frame_1080p", "value": med["frame"], "unit": "ms/frame",
-        "higher_is_better": False, "frames": frames, "warmup": warmup,
+        "higher_is_better": False, "frames": frames, "warmup": warmup, "n_gpus": world,
         "render_ms": med["render"], "collect_ms": med["collect"], "train_ms": med["train"],
         "queries_per_frame": queries[-1], "records_per_frame": records[-1],
         "train_paths_per_frame": count,
         "train_samples_per_sec": 4 * min(16384, records[-1]) / (med["train"] * 1e-3),
         "render_queries_per_sec": queries[-1] / (med["render"] * 1e-3),
+        "replicas_identical": same,
         "config": "cfg3: cornell 1920x1080, two-level nc=(16,), spp 1, D=4 cache, "
-                  "collect 51,840 paths, 4 x 16384 train steps",
+                  "collect 51,840 paths, 4 x 16384 train steps"
+                  + (f"; sharded over {world} GPUs (row bands, path shards, "
+                     "NCCL gradient all-reduce)" if world > 1 else ""),
         "reference_cpu_context": "SURVEY.md 6: 122.6 s/frame on 1 core (not re-timed here)",
     }
 
@@ -234,7 +265,7 @@ def run_b200(args, rank, world, local_rank):
     import numpy as np
     import torch
 
-    torch.cuda.set_device(local_rank)
+    torch.cuda.set_device(local_rank % torch.cuda.device_count())
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -313,6 +344,11 @@ def run_b200(args, rank, world, local_rank):
     h2d = int(sum(h.numel() * h.element_size() for h in host))
     d2h = int(y_host.numel() * 4)
 
+    fb = None
+    if not args.no_frame:
+        from paper_2412_04634_b200 import distributed as D
+
+        fb = frame_bench(args.frame_steps, 3, comm=D.Comm() if world > 1 else None)
     if rank != 0:
         return
     import json as _json
@@ -359,8 +395,8 @@ def run_b200(args, rank, world, local_rank):
                 "path": "paper_2412_04634_b200.mlp.full_forward, pinned host buffers"},
         "gpu_launches": 2 * args.steps,
     }
-    if world == 1 and not args.no_frame:
-        line["frame_1080p"] = frame_bench(args.frame_steps, 3)
+    if fb is not None:
+        line["frame_1080p"] = fb
     if world == 1 and not args.no_cpu_baseline:
         rate, nq = cpu_baseline(cores=1, chunks=6, chunk=1 << 15)
         line["cpu_baseline"] = {"value": rate, "unit": "queries/s", "cores": 1, "kind": "port",
@@ -381,8 +417,10 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local_rank % torch.cuda.device_count())
+        # NCCL over NVLink; NIRC_DIST_BACKEND=gloo lets several ranks share
+        # one GPU (a smoke test of the multi-rank path on a 1-GPU box)
+        dist.init_process_group(os.environ.get("NIRC_DIST_BACKEND", "nccl"))
     run_b200(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist

@@ -188,6 +188,32 @@ int nirc_train_step(const nirc_spec_t* spec, float* theta, float* m, float* v,
 int64_t nirc_train_workspace_bytes(const nirc_spec_t* spec, int64_t n_records,
                                    int32_t batch_cap);
 
+/* Multi-GPU split of nirc_train_step (the reference step is
+ * caches.py:327-350).  Every rank holds the same records and selects the
+ * same batch; rank r runs the fused encode/forward/loss/backward over the
+ * 64-row batch tiles [tile_begin, tile_end) of nirc_train_tiles() and writes
+ *   grad (theta_len f32, overwritten): its shard's gradient, the loss still
+ *        normalised by the GLOBAL batch (losses.py:33-42 divides by B*3);
+ *   aux (2 f64): [0] its shard's raw loss sum, [1] 1.0 if a row had pdf <= 0.
+ * The caller sums grad and aux over the ranks (ncclAllReduce) and then runs
+ * nirc_train_apply, identical on every rank, so replicas stay bit-identical.
+ * l2 / relative_l2 losses only (NIRC_E_UNSUPPORTED otherwise). */
+int64_t nirc_train_tiles(int64_t n_records, int32_t batch_cap);
+int nirc_train_grad(const nirc_spec_t* spec, const float* theta,
+                    const nirc_records_t* rec, uint64_t seed, int64_t frame,
+                    int32_t step, int32_t batch_cap, int32_t loss_kind,
+                    double loss_eps, int64_t tile_begin, int64_t tile_end,
+                    float* grad, double* aux, int32_t* status_flags,
+                    int64_t* batch_idx_out, void* workspace,
+                    int64_t workspace_bytes, void* stream);
+/* loss_out = aux[0] / (batch*3) (status bit 2 if non-finite), status bit 1
+ * if aux[1] > 0, then the dense Adam step of nirc_adam_step gated by the
+ * status flags.  scratch: >= 4 bytes of device memory. */
+int nirc_train_apply(const nirc_spec_t* spec, float* theta, float* m, float* v,
+                     int64_t* t, int64_t* skipped, const float* grad,
+                     const double* aux, int64_t batch, double lr, double* loss_out,
+                     int32_t* status_flags, int32_t* scratch, void* stream);
+
 /* ---- rendering (pkg/src/nirclab/kernels.py:451-759) --------------------- */
 /* render_kernel for MODE_PT / MODE_TL: per-pixel sums img, img2 (h,w,3) f64
  * and term (h,w) f64 are ACCUMULATED (caller zeroes).  The two-level cache
@@ -217,6 +243,16 @@ int nirc_collect(const nirc_scene_t* scene, const double* cam, uint64_t seed,
                  const nirc_records_out_t* out, int64_t* n_out,
                  void* workspace, int64_t workspace_bytes, void* stream);
 int64_t nirc_collect_workspace_bytes(int64_t count);
+
+/* Paths [path0, path0 + count) of collect_training_records (one GPU's shard
+ * in the multi-GPU frame): path p keys stream_key(seed, P_TRAIN, frame, p, 0)
+ * (kernels.py:298), so the rank-ordered concatenation of the shards' records
+ * equals nirc_collect over all paths row for row. */
+int nirc_collect_range(const nirc_scene_t* scene, const double* cam,
+                       uint64_t seed, uint64_t frame, int64_t path0,
+                       int64_t count, int32_t kind,
+                       const nirc_records_out_t* out, int64_t* n_out,
+                       void* workspace, int64_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -640,7 +640,9 @@ size_t fused_smem_bytes(const nirc_spec_t& sp);
 int launch_fused_train(const nirc_spec_t& sp, const float* theta, const nirc_records_t& rec,
                        const int64_t* idx, int64_t B, int loss_kind, double loss_eps,
                        float* grad, float* partials, double* loss_part, double* loss_out,
-                       int32_t* flags, int32_t* adam_bad, cudaStream_t s);
+                       int32_t* flags, int32_t* adam_bad, cudaStream_t s, int64_t tile0,
+                       int64_t tile1, int mode);
+constexpr int kFusedTileRows = 64;  // rows per k_train_tile CTA (train_fused.cu kTR)
 }  // namespace nirc
 
 using namespace nirc;
@@ -829,27 +831,10 @@ extern "C" int64_t nirc_train_workspace_bytes(const nirc_spec_t* spec, int64_t n
   return (int64_t)carve_train(*spec, n_records, B, nullptr).bytes;
 }
 
-extern "C" int nirc_train_step(const nirc_spec_t* spec, float* theta, float* m, float* v,
-                               int64_t* t, int64_t* skipped, const nirc_records_t* rec,
-                               uint64_t seed, int64_t frame, int32_t step, int32_t batch_cap,
-                               int32_t loss_kind, double loss_eps, double lr,
-                               double* running_mean, double* loss_out, int32_t* status_flags,
-                               int64_t* batch_idx_out, void* workspace,
-                               int64_t workspace_bytes, void* stream) {
-  int st = check_spec(spec);
-  if (st) return st;
-  const int64_t n = rec->n;
-  if (n <= 0) { set_last_error("cannot train on an empty record set"); return NIRC_E_CONFIG; }
-  if (batch_cap < 1) { set_last_error("batch must be positive"); return NIRC_E_CONFIG; }
-  if (n > INT_MAX) { set_last_error("too many records"); return NIRC_E_UNSUPPORTED; }
-  const int64_t B = n < batch_cap ? n : batch_cap;
-  TrainWs w = carve_train(*spec, n, B, workspace);
-  if ((int64_t)w.bytes > workspace_bytes) {
-    set_last_error("train workspace too small (%lld < %lld)", (long long)workspace_bytes,
-                   (long long)w.bytes);
-    return NIRC_E_CONFIG;
-  }
-  cudaStream_t s = S(stream);
+// Batch selection of one optimizer step into w.idx (caches.py:327-329).
+static int select_batch(const TrainWs& w, uint64_t seed, int64_t frame, int32_t step, int64_t n,
+                        int64_t B, int32_t* status_flags, int64_t* batch_idx_out,
+                        cudaStream_t s) {
   const uint64_t K = stream_key(seed, P_SHUFFLE, 0, (uint64_t)frame, 0);
   const uint64_t off = (uint64_t)step * (uint64_t)n;
   NIRC_CUDA_TRY(cudaMemsetAsync(w.sel.hist, 0, kSelBins * 4, s));
@@ -863,11 +848,47 @@ extern "C" int nirc_train_step(const nirc_spec_t* spec, float* theta, float* m, 
   NIRC_LAUNCH_CHECK("k_sel_*");
   if (batch_idx_out)
     NIRC_CUDA_TRY(cudaMemcpyAsync(batch_idx_out, w.idx, B * 8, cudaMemcpyDeviceToDevice, s));
+  return NIRC_OK;
+}
+
+static int train_args_ok(const nirc_spec_t* spec, const nirc_records_t* rec, int32_t batch_cap) {
+  int st = check_spec(spec);
+  if (st) return st;
+  if (!rec || rec->n <= 0) {
+    set_last_error("cannot train on an empty record set");
+    return NIRC_E_CONFIG;
+  }
+  if (batch_cap < 1) { set_last_error("batch must be positive"); return NIRC_E_CONFIG; }
+  if (rec->n > INT_MAX) { set_last_error("too many records"); return NIRC_E_UNSUPPORTED; }
+  return NIRC_OK;
+}
+
+extern "C" int nirc_train_step(const nirc_spec_t* spec, float* theta, float* m, float* v,
+                               int64_t* t, int64_t* skipped, const nirc_records_t* rec,
+                               uint64_t seed, int64_t frame, int32_t step, int32_t batch_cap,
+                               int32_t loss_kind, double loss_eps, double lr,
+                               double* running_mean, double* loss_out, int32_t* status_flags,
+                               int64_t* batch_idx_out, void* workspace,
+                               int64_t workspace_bytes, void* stream) {
+  int st = train_args_ok(spec, rec, batch_cap);
+  if (st) return st;
+  const int64_t n = rec->n;
+  const int64_t B = n < batch_cap ? n : batch_cap;
+  TrainWs w = carve_train(*spec, n, B, workspace);
+  if ((int64_t)w.bytes > workspace_bytes) {
+    set_last_error("train workspace too small (%lld < %lld)", (long long)workspace_bytes,
+                   (long long)w.bytes);
+    return NIRC_E_CONFIG;
+  }
+  cudaStream_t s = S(stream);
+  if ((st = select_batch(w, seed, frame, step, n, B, status_flags, batch_idx_out, s))) return st;
   if ((loss_kind == 0 || loss_kind == 1) && fused_supported(*spec) &&
       fused_smem_bytes(*spec) <= 227 * 1024) {
     // one fused kernel per step: encode, forward, loss, backward, scatter
+    const int64_t ntiles = (B + kFusedTileRows - 1) / kFusedTileRows;
     if ((st = launch_fused_train(*spec, theta, *rec, w.idx, B, loss_kind, loss_eps, w.grad,
-                                 w.fpart, w.floss, loss_out, status_flags, w.adam_bad, s)))
+                                 w.fpart, w.floss, loss_out, status_flags, w.adam_bad, s, 0,
+                                 ntiles, 0)))
       return st;
     const int nb = 148 * 4;
     k_adam_apply<<<nb, 256, 0, s>>>(theta, m, v, w.grad, spec->theta_len, t, skipped, (float)lr,
@@ -906,4 +927,71 @@ extern "C" int nirc_train_step(const nirc_spec_t* spec, float* theta, float* m, 
   NIRC_LAUNCH_CHECK("k_train_scatter");
   return nirc_adam_step(theta, m, v, w.grad, spec->theta_len, t, skipped, lr, 0.9, 0.99, 1e-8,
                         status_flags, w.adam_bad, stream);
+}
+
+// ---- multi-GPU split of nirc_train_step ------------------
+extern "C" int64_t nirc_train_tiles(int64_t n_records, int32_t batch_cap) {
+  if (n_records <= 0 || batch_cap < 1) return 0;
+  const int64_t B = n_records < batch_cap ? n_records : batch_cap;
+  return (B + kFusedTileRows - 1) / kFusedTileRows;
+}
+
+extern "C" int nirc_train_grad(const nirc_spec_t* spec, const float* theta,
+                               const nirc_records_t* rec, uint64_t seed, int64_t frame,
+                               int32_t step, int32_t batch_cap, int32_t loss_kind,
+                               double loss_eps, int64_t tile_begin, int64_t tile_end,
+                               float* grad, double* aux, int32_t* status_flags,
+                               int64_t* batch_idx_out, void* workspace, int64_t workspace_bytes,
+                               void* stream) {
+  int st = train_args_ok(spec, rec, batch_cap);
+  if (st) return st;
+  if (!(loss_kind == 0 || loss_kind == 1) || !fused_supported(*spec) ||
+      fused_smem_bytes(*spec) > 227 * 1024) {
+    set_last_error("sharded training needs the fused l2 / relative_l2 path");
+    return NIRC_E_UNSUPPORTED;
+  }
+  const int64_t n = rec->n;
+  const int64_t B = n < batch_cap ? n : batch_cap;
+  const int64_t ntiles = (B + kFusedTileRows - 1) / kFusedTileRows;
+  if (tile_begin < 0 || tile_end > ntiles || tile_begin > tile_end) {
+    set_last_error("tile range [%lld, %lld) outside [0, %lld)", (long long)tile_begin,
+                   (long long)tile_end, (long long)ntiles);
+    return NIRC_E_CONFIG;
+  }
+  TrainWs w = carve_train(*spec, n, B, workspace);
+  if ((int64_t)w.bytes > workspace_bytes) {
+    set_last_error("train workspace too small (%lld < %lld)", (long long)workspace_bytes,
+                   (long long)w.bytes);
+    return NIRC_E_CONFIG;
+  }
+  cudaStream_t s = S(stream);
+  if ((st = select_batch(w, seed, frame, step, n, B, status_flags, batch_idx_out, s))) return st;
+  return launch_fused_train(*spec, theta, *rec, w.idx, B, loss_kind, loss_eps, grad, w.fpart,
+                            w.floss, aux, status_flags, nullptr, s, tile_begin, tile_end, 1);
+}
+
+namespace nirc {
+// Folds the cross-GPU sums: loss = sum / (B*3) (flag 2 if non-finite), flag
+// 1 if any shard saw pdf <= 0.
+__global__ void k_train_fold(const double* __restrict__ aux, int64_t B,
+                             double* __restrict__ loss_out, int32_t* __restrict__ flags) {
+  if (flags[0] & 3) return;
+  if (aux[1] > 0.0) atomicOr(flags, 1);
+  const double v = aux[0] / (double)(B * 3);
+  loss_out[0] = v;
+  if (!isfinite(v)) atomicOr(flags, 2);
+}
+}  // namespace nirc
+
+extern "C" int nirc_train_apply(const nirc_spec_t* spec, float* theta, float* m, float* v,
+                                int64_t* t, int64_t* skipped, const float* grad,
+                                const double* aux, int64_t batch, double lr, double* loss_out,
+                                int32_t* status_flags, int32_t* scratch, void* stream) {
+  int st = check_spec(spec);
+  if (st) return st;
+  if (batch < 1) { set_last_error("batch must be positive"); return NIRC_E_CONFIG; }
+  k_train_fold<<<1, 1, 0, S(stream)>>>(aux, batch, loss_out, status_flags);
+  NIRC_LAUNCH_CHECK("k_train_fold");
+  return nirc_adam_step(theta, m, v, grad, spec->theta_len, t, skipped, lr, 0.9, 0.99, 1e-8,
+                        status_flags, scratch, stream);
 }

@@ -690,6 +690,7 @@ struct Stage {
   int32_t* nrec;   // per path
   int32_t* nvert;  // per path
   int64_t count;
+  int64_t path0;   // global index of local path 0 (multi-GPU path shards)
 };
 
 __global__ void k_walk_record(nirc_scene_t scn, const double* __restrict__ cam, uint64_t seed,
@@ -699,7 +700,7 @@ __global__ void k_walk_record(nirc_scene_t scn, const double* __restrict__ cam, 
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= st.count) return;
   const int64_t C = st.count;
-  const uint64_t key = stream_key(seed, P_TRAIN, frame, (uint64_t)p, 0);
+  const uint64_t key = stream_key(seed, P_TRAIN, frame, (uint64_t)(st.path0 + p), 0);
   const double w = cam[14], h = cam[15];
   const double sx = rand_uniform(key, DIM_JITTER_X) * w;
   const double sy = rand_uniform(key, DIM_JITTER_Y) * h;
@@ -1067,13 +1068,13 @@ extern "C" int64_t nirc_collect_workspace_bytes(int64_t count) {
   return (int64_t)b;
 }
 
-extern "C" int nirc_collect(const nirc_scene_t* scene, const double* cam, uint64_t seed,
-                            uint64_t frame, int64_t count, int32_t kind,
-                            const nirc_records_out_t* out, int64_t* n_out, void* workspace,
-                            int64_t workspace_bytes, void* stream) {
+extern "C" int nirc_collect_range(const nirc_scene_t* scene, const double* cam, uint64_t seed,
+                                  uint64_t frame, int64_t path0, int64_t count, int32_t kind,
+                                  const nirc_records_out_t* out, int64_t* n_out, void* workspace,
+                                  int64_t workspace_bytes, void* stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (count <= 0) {
-    set_last_error("count must be positive");
+  if (count <= 0 || path0 < 0) {
+    set_last_error("count must be positive and path0 non-negative");
     return NIRC_E_CONFIG;
   }
   if (kind != 0 && kind != 1) {
@@ -1086,6 +1087,7 @@ extern "C" int nirc_collect(const nirc_scene_t* scene, const double* cam, uint64
     set_last_error("collect workspace too small");
     return NIRC_E_CONFIG;
   }
+  st.path0 = path0;
   int64_t* off = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(st.nvert) + aup(count * 4));
   k_walk_record<<<(int)((count + 63) / 64), 64, 0, s>>>(*scene, cam, seed, frame, st);
   NIRC_LAUNCH_CHECK("k_walk_record");
@@ -1094,6 +1096,14 @@ extern "C" int nirc_collect(const nirc_scene_t* scene, const double* cam, uint64
   k_compact_records<<<(int)((count + 127) / 128), 128, 0, s>>>(st, off, kind, *out);
   NIRC_LAUNCH_CHECK("k_compact_records");
   return NIRC_OK;
+}
+
+extern "C" int nirc_collect(const nirc_scene_t* scene, const double* cam, uint64_t seed,
+                            uint64_t frame, int64_t count, int32_t kind,
+                            const nirc_records_out_t* out, int64_t* n_out, void* workspace,
+                            int64_t workspace_bytes, void* stream) {
+  return nirc_collect_range(scene, cam, seed, frame, 0, count, kind, out, n_out, workspace,
+                            workspace_bytes, stream);
 }
 
 // Tools only (not part of include/nirc_b200.h): route per-phase clock64()

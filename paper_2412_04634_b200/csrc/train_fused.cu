@@ -219,11 +219,11 @@ __global__ void __launch_bounds__(kTT, 1)
     k_train_tile(nirc_spec_t sp, FusedLayout L, const float* __restrict__ theta,
                  nirc_records_t rec, const int64_t* __restrict__ idx, int64_t B, int loss_kind,
                  double loss_eps, float* __restrict__ grad, float* __restrict__ partials,
-                 double* __restrict__ loss_part, int32_t* __restrict__ flags) {
+                 double* __restrict__ loss_part, int32_t* __restrict__ flags, int64_t tile0) {
   extern __shared__ __align__(16) float fsm[];
   if (flags[0] & 3) return;
   const int tid = threadIdx.x;
-  const int64_t row0 = (int64_t)blockIdx.x * kTR;
+  const int64_t row0 = (tile0 + blockIdx.x) * kTR;
   const int nrows = (int)((B - row0) < kTR ? (B - row0) : kTR);
   // ---- stage the network (odd-stride rows) ---------------------------------
   for (int l = 0; l < L.nl; ++l) {
@@ -380,13 +380,18 @@ __global__ void __launch_bounds__(kTT, 1)
   }
 }
 
-// grad[mlp] = sum over tiles (tile order) of the partials; loss = mean;
-// flags: 2 = non-finite loss (stop), adam_bad = any non-finite gradient.
+// grad[mlp] = sum over tiles (tile order) of the partials.
+// mode 0 (whole batch on this GPU): loss = mean; flags: 2 = non-finite loss
+//   (stop), adam_bad = any non-finite gradient.
+// mode 1 (one shard of a multi-GPU batch): aux[0] = this shard's raw loss
+//   sum, aux[1] = 1 if a row of this shard had pdf <= 0; the finiteness
+//   checks run after the cross-GPU sum (nirc_train_apply).
 __global__ void k_reduce_grad(nirc_spec_t sp, const float* __restrict__ partials, int ntiles,
                               const double* __restrict__ loss_part, int64_t B,
                               float* __restrict__ grad, double* __restrict__ loss_out,
-                              int32_t* __restrict__ flags, int32_t* __restrict__ adam_bad) {
-  if (flags[0] & 3) return;
+                              int32_t* __restrict__ flags, int32_t* __restrict__ adam_bad,
+                              int mode) {
+  if (mode == 0 && (flags[0] & 3)) return;
   const int np = (int)(sp.theta_len - sp.grid_len);
   int bad = 0;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x) {
@@ -394,6 +399,15 @@ __global__ void k_reduce_grad(nirc_spec_t sp, const float* __restrict__ partials
     for (int t = 0; t < ntiles; ++t) s += partials[(int64_t)t * np + p];
     grad[sp.grid_len + p] = s;
     bad |= !isfinite(s);
+  }
+  if (mode == 1) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      double s = 0.0;
+      for (int t = 0; t < ntiles; ++t) s += loss_part[t];
+      loss_out[0] = s;
+      loss_out[1] = (flags[0] & 1) ? 1.0 : 0.0;
+    }
+    return;
   }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sp.grid_len;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -412,22 +426,27 @@ size_t fused_smem_bytes(const nirc_spec_t& sp) {
   return (size_t)fused_layout(sp).total_floats * 4;
 }
 
+// Tiles [tile0, tile1) of the batch (all of it on one GPU; one shard of it
+// per GPU in the multi-GPU frame, mode 1).
 int launch_fused_train(const nirc_spec_t& sp, const float* theta, const nirc_records_t& rec,
                        const int64_t* idx, int64_t B, int loss_kind, double loss_eps,
                        float* grad, float* partials, double* loss_part, double* loss_out,
-                       int32_t* flags, int32_t* adam_bad, cudaStream_t s) {
+                       int32_t* flags, int32_t* adam_bad, cudaStream_t s, int64_t tile0,
+                       int64_t tile1, int mode) {
   const FusedLayout L = fused_layout(sp);
   const size_t sm = (size_t)L.total_floats * 4;
   NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)k_train_tile,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  const int ntiles = (int)((B + kTR - 1) / kTR);
+  const int ntiles = (int)(tile1 > tile0 ? tile1 - tile0 : 0);
   NIRC_CUDA_TRY(cudaMemsetAsync(grad, 0, sp.grid_len * 4, s));
-  NIRC_CUDA_TRY(cudaMemsetAsync(adam_bad, 0, 4, s));
-  k_train_tile<<<ntiles, kTT, sm, s>>>(sp, L, theta, rec, idx, B, loss_kind, loss_eps, grad,
-                                       partials, loss_part, flags);
-  NIRC_LAUNCH_CHECK("k_train_tile");
+  if (adam_bad) NIRC_CUDA_TRY(cudaMemsetAsync(adam_bad, 0, 4, s));
+  if (ntiles > 0) {
+    k_train_tile<<<ntiles, kTT, sm, s>>>(sp, L, theta, rec, idx, B, loss_kind, loss_eps, grad,
+                                         partials, loss_part, flags, tile0);
+    NIRC_LAUNCH_CHECK("k_train_tile");
+  }
   k_reduce_grad<<<64, 256, 0, s>>>(sp, partials, ntiles, loss_part, B, grad, loss_out, flags,
-                                   adam_bad);
+                                   adam_bad, mode);
   NIRC_LAUNCH_CHECK("k_reduce_grad");
   return NIRC_OK;
 }
