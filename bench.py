@@ -190,7 +190,7 @@ def frame_bench(frames, warmup, width=1920, height=1080, nc=(16,), comm=None):
 
     from paper_2412_04634_b200 import distributed as D
     from paper_2412_04634_b200.caches import Cache, default_train_count, train_frame
-    from paper_2412_04634_b200.estimators import render_device
+    from paper_2412_04634_b200.estimators import render_and_collect
     from paper_2412_04634_b200.frame import config3
     from paper_2412_04634_b200.scene import load_builtin
 
@@ -208,15 +208,20 @@ def frame_bench(frames, warmup, width=1920, height=1080, nc=(16,), comm=None):
             comm.barrier()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         ev[0].record(stream)
+        # render + training walks of the frame in one trace launch (the
+        # record all-gather of the multi-GPU frame is inside "collect")
         if world > 1:
-            _, _, _, q, _ = D.render_band(scene, cfg, cache, comm, seed=0, spp=1, frame=f)
+            rows = D.split_range(height, world, comm.rank)
+            paths = D.split_range(count, world, comm.rank)
+            _, _, _, q, local = render_and_collect(scene, cfg, cache, seed=0, spp=1, frame=f,
+                                                   count=count, rows=rows, paths=paths)
         else:
-            _, _, _, q = render_device(scene, cfg, cache, seed=0, spp=1, frame=f)
+            _, _, _, q, rec = render_and_collect(scene, cfg, cache, seed=0, spp=1, frame=f,
+                                                 count=count)
         ev[1].record(stream)
         if world > 1:
-            rec = D.collect_sharded(cache, comm, count=count, frame=f, ops=ops)
-        else:
-            rec = cache.collect(count=count, frame=f)
+            packed = D.pack_records({k: getattr(local, k) for k, _ in D.REC_COLS})
+            rec = D.unpack_records(comm.all_gather_rows(packed), cache.record_kind, f)
         ev[2].record(stream)
         if world > 1:
             D.train_frame_sharded(cache, rec, comm, steps=4, ops=ops)
@@ -246,11 +251,15 @@ def frame_bench(frames, warmup, width=1920, height=1080, nc=(16,), comm=None):
     return {
         "metric": "ms_per_frame_1080p", "value": med["frame"], "unit": "ms/frame",
         "higher_is_better": False, "frames": frames, "warmup": warmup, "n_gpus": world,
-        "render_ms": med["render"], "collect_ms": med["collect"], "train_ms": med["train"],
+        "render_collect_ms": med["render"], "record_allgather_ms": med["collect"],
+        "train_ms": med["train"],
         "queries_per_frame": queries[-1], "records_per_frame": records[-1],
         "train_paths_per_frame": count,
         "train_samples_per_sec": 4 * min(16384, records[-1]) / (med["train"] * 1e-3),
         "render_queries_per_sec": queries[-1] / (med["render"] * 1e-3),
+        "phases": "render_collect = one nirc_render_collect launch set (path tracer with the "
+                  "training walks as its first work items, fused inference, accumulation, "
+                  "record compaction); record_allgather = multi-GPU record exchange",
         "replicas_identical": same,
         "config": "cfg3: cornell 1920x1080, two-level nc=(16,), spp 1, D=4 cache, "
                   "collect 51,840 paths, 4 x 16384 train steps"

@@ -188,6 +188,23 @@ int nirc_train_step(const nirc_spec_t* spec, float* theta, float* m, float* v,
 int64_t nirc_train_workspace_bytes(const nirc_spec_t* spec, int64_t n_records,
                                    int32_t batch_cap);
 
+/* The whole train_frame body (caches.py:310-354 without the frame counter):
+ * `steps` optimizer steps on the same records, the batches of all steps
+ * selected up front (they do not depend on theta), then per step the fused
+ * encode/forward/loss/backward/scatter and dense Adam.  loss_out receives
+ * `steps` f64 losses; status_flags as in nirc_train_step (a divergence stops
+ * the remaining steps). */
+int nirc_train_frame(const nirc_spec_t* spec, float* theta, float* m, float* v,
+                     int64_t* t, int64_t* skipped, const nirc_records_t* rec,
+                     uint64_t seed, int64_t frame, int32_t steps,
+                     int32_t batch_cap, int32_t loss_kind, double loss_eps,
+                     double lr, double* running_mean, double* loss_out,
+                     int32_t* status_flags, void* workspace,
+                     int64_t workspace_bytes, void* stream);
+int64_t nirc_train_frame_workspace_bytes(const nirc_spec_t* spec,
+                                         int64_t n_records, int32_t batch_cap,
+                                         int32_t steps);
+
 /* Multi-GPU split of nirc_train_step (the reference step is
  * caches.py:327-350).  Every rank holds the same records and selects the
  * same batch; rank r runs the fused encode/forward/loss/backward over the
@@ -227,6 +244,7 @@ int nirc_render(const nirc_scene_t* scene, const double* cam,
                 void* stream);
 int64_t nirc_render_workspace_bytes(const nirc_render_cfg_t* cfg);
 
+
 /* ---- training records (pkg/src/nirclab/kernels.py:85-311,
  *      caches.py:87-131) ------------------------------------------------- */
 /* collect_training_records, kind "nirc" (0) or "nirc_full" (1): traces
@@ -253,6 +271,25 @@ int nirc_collect_range(const nirc_scene_t* scene, const double* cam,
                        int64_t count, int32_t kind,
                        const nirc_records_out_t* out, int64_t* n_out,
                        void* workspace, int64_t workspace_bytes, void* stream);
+
+/* ---- one frame: render + collect ---------------------------------------- */
+/* One frame's render (nirc_render) AND training-record collection
+ * (nirc_collect_range over paths [path0, path0+count) with seed train_seed,
+ * frame train_frame) in one persistent trace launch: the training walks are
+ * the first work items of the path tracer, so their long roulette tails
+ * overlap the camera paths (render_kernel + collect_paths_kernel,
+ * kernels.py:289-311,723-759, in the order experiment.py:153-172 calls
+ * them; both read only the scene, neither reads theta's updates). */
+int nirc_render_collect(const nirc_scene_t* scene, const double* cam,
+                        const nirc_render_cfg_t* cfg, const nirc_spec_t* spec,
+                        const float* theta, double* img, double* img2,
+                        double* term, int64_t* queries_out, uint64_t train_seed,
+                        uint64_t train_frame, int64_t path0, int64_t count,
+                        int32_t kind, const nirc_records_out_t* out,
+                        int64_t* n_out, void* workspace, int64_t workspace_bytes,
+                        void* stream);
+int64_t nirc_render_collect_workspace_bytes(const nirc_render_cfg_t* cfg,
+                                            int64_t count);
 
 #ifdef __cplusplus
 }

@@ -116,6 +116,9 @@ SIGNATURES = {
     "nirc_train_step": (I32, [SPEC, P, P, P, P, P, C.POINTER(NircRecords), U64, I64, I32,
                               I32, I32, F64, F64, P, P, P, P, P, I64, P]),
     "nirc_train_workspace_bytes": (I64, [SPEC, I64, I32]),
+    "nirc_train_frame": (I32, [SPEC, P, P, P, P, P, C.POINTER(NircRecords), U64, I64, I32,
+                               I32, I32, F64, F64, P, P, P, P, I64, P]),
+    "nirc_train_frame_workspace_bytes": (I64, [SPEC, I64, I32, I32]),
     "nirc_train_tiles": (I64, [I64, I32]),
     "nirc_train_grad": (I32, [SPEC, P, C.POINTER(NircRecords), U64, I64, I32, I32, I32, F64,
                               I64, I64, P, P, P, P, P, I64, P]),
@@ -123,6 +126,10 @@ SIGNATURES = {
     "nirc_render": (I32, [C.POINTER(NircScene), P, C.POINTER(NircRenderCfg), SPEC, P, P, P,
                           P, P, P, I64, P]),
     "nirc_render_workspace_bytes": (I64, [C.POINTER(NircRenderCfg)]),
+    "nirc_render_collect": (I32, [C.POINTER(NircScene), P, C.POINTER(NircRenderCfg), SPEC, P,
+                                  P, P, P, P, U64, U64, I64, I64, I32,
+                                  C.POINTER(NircRecordsOut), P, P, I64, P]),
+    "nirc_render_collect_workspace_bytes": (I64, [C.POINTER(NircRenderCfg), I64]),
     "nirc_collect": (I32, [C.POINTER(NircScene), P, U64, U64, I64, I32,
                            C.POINTER(NircRecordsOut), P, P, I64, P]),
     "nirc_collect_workspace_bytes": (I64, [I64]),

@@ -2,10 +2,11 @@
 pkg/src/nirclab/caches.py).
 
 θ, the Adam moments and the training records live in device memory.
-``train_frame`` issues one fused C-ABI ``nirc_train_step`` per optimizer
-step (batch selection from the splitmix64 shuffle stream, encode, forward,
-loss, backward + hash-grid scatter, dense Adam) and synchronises with the
-host once per frame to read the loss trace and the status flags.
+``train_frame`` is one C-ABI ``nirc_train_frame`` call: the batches of all
+steps from the splitmix64 shuffle stream, then per optimizer step the fused
+encode / forward / loss / backward + hash-grid scatter kernel and dense Adam;
+it synchronises with the host once per frame to read the loss trace and the
+status flags.
 """
 
 from __future__ import annotations
@@ -108,19 +109,31 @@ def _launch_steps(spec, theta, adam, records, seed, frame, steps, batch, loss_ki
     cs = _lib.make_c_spec(spec)
     rec, _keep = records.c_struct()
     B = min(cap, n)
-    need = lib.nirc_train_workspace_bytes(cs, n, cap)
-    buf = ws.get(need)
     losses = _dev.zeros((steps,), torch.float64)
     flags = _dev.zeros((1,), torch.int32)
-    idx = [_dev.empty((B,), torch.int64) for _ in range(steps)] if return_idx else None
-    for s in range(steps):
-        _lib.check(lib.nirc_train_step(
+    idx = None
+    if not return_idx:
+        # one C call: batches of all steps selected at once, then the steps
+        need = lib.nirc_train_frame_workspace_bytes(cs, n, cap, steps)
+        buf = ws.get(need)
+        _lib.check(lib.nirc_train_frame(
             cs, _dev.ptr(theta), _dev.ptr(adam.m), _dev.ptr(adam.v), _dev.ptr(adam._t),
-            _dev.ptr(adam._skipped), rec, int(seed), int(frame), s, cap,
+            _dev.ptr(adam._skipped), rec, int(seed), int(frame), int(steps), cap,
             LOSS_KINDS.index(loss_kind), float(loss_eps), float(adam.lr),
-            _dev.ptr(running_mean), _dev.ptr(losses[s:s + 1]), _dev.ptr(flags),
-            _dev.ptr(idx[s]) if return_idx else None, _dev.ptr(buf), int(buf.numel()),
-            _dev.stream()), "nirc_train_step")
+            _dev.ptr(running_mean), _dev.ptr(losses), _dev.ptr(flags), _dev.ptr(buf),
+            int(buf.numel()), _dev.stream()), "nirc_train_frame")
+    else:
+        need = lib.nirc_train_workspace_bytes(cs, n, cap)
+        buf = ws.get(need)
+        idx = [_dev.empty((B,), torch.int64) for _ in range(steps)]
+        for s in range(steps):
+            _lib.check(lib.nirc_train_step(
+                cs, _dev.ptr(theta), _dev.ptr(adam.m), _dev.ptr(adam.v), _dev.ptr(adam._t),
+                _dev.ptr(adam._skipped), rec, int(seed), int(frame), s, cap,
+                LOSS_KINDS.index(loss_kind), float(loss_eps), float(adam.lr),
+                _dev.ptr(running_mean), _dev.ptr(losses[s:s + 1]), _dev.ptr(flags),
+                _dev.ptr(idx[s]), _dev.ptr(buf), int(buf.numel()), _dev.stream()),
+                "nirc_train_step")
     trace = losses.cpu().numpy().tolist()
     f = int(flags.item())
     res = TrainResult(trace=trace, adam=adam, flags=f)

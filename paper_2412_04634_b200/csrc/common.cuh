@@ -179,6 +179,64 @@ NIRC_D float2 level_features2(const float* __restrict__ table, const LevelCell& 
   return make_float2(x0, x1);
 }
 
+// Dense shared-memory copies of the coarse levels (feats == 2).  Level l's
+// cell coordinates lie in [0, res_l] and its corners in [0, res_l + 1], so a
+// dense (res_l + 2)^3 array indexed by (z, y, x) holds every slot the level
+// can touch: dense[(z*R + y)*R + x] = table_l[hash3(x, y, z)] -- the same
+// values, gathered from shared memory instead of scattered L2 lines.
+struct DenseLevels {
+  int n;                          // levels 0..n-1 are dense
+  int R[NIRC_MAX_LEVELS];         // res + 2
+  int off[NIRC_MAX_LEVELS + 1];   // float2 offsets; off[n] = total entries
+};
+
+inline DenseLevels dense_levels_for(const nirc_spec_t& sp, size_t budget_bytes,
+                                    int max_levels = NIRC_MAX_LEVELS) {
+  DenseLevels d{};
+  int total = 0;
+  d.off[0] = 0;
+  for (int l = 0; l < sp.levels && l < max_levels; ++l) {
+    const int R = sp.res[l] + 2;
+    const long long cnt = (long long)R * R * R;
+    if (sp.feats != 2 || (total + cnt) * 8 > (long long)budget_bytes) break;
+    d.R[l] = R;
+    total += (int)cnt;
+    d.n = l + 1;
+    d.off[l + 1] = total;
+  }
+  return d;
+}
+
+// Cooperative fill of the dense levels by the whole CTA.
+NIRC_D void fill_dense_levels(const nirc_spec_t& sp, const DenseLevels& d,
+                              const float* __restrict__ theta, float2* dense) {
+  const uint32_t T = 1u << sp.table_log2;
+  for (int l = 0; l < d.n; ++l) {
+    const int R = d.R[l];
+    const float2* tab = reinterpret_cast<const float2*>(theta + (size_t)l * T * 2);
+    for (int i = threadIdx.x; i < R * R * R; i += blockDim.x) {
+      const int x = i % R, y = (i / R) % R, z = i / (R * R);
+      dense[d.off[l] + i] = __ldg(tab + hash3((uint32_t)x, (uint32_t)y, (uint32_t)z, T - 1u));
+    }
+  }
+}
+
+NIRC_D float2 level_features2_dense(const float2* dense, int R, const LevelCell& c) {
+  const int b = (c.iz * R + c.iy) * R + c.ix;
+  float2 g[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    g[k] = dense[b + (k & 1) + ((k >> 1) & 1) * R + ((k >> 2) & 1) * R * R];
+  float x0 = 0.0f, x1 = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float w = corner_weight(c, k);
+    x0 = __fadd_rn(x0, __fmul_rn(w, g[k].x));
+    x1 = __fadd_rn(x1, __fmul_rn(w, g[k].y));
+  }
+  return make_float2(x0, x1);
+}
+
 // ------------------------------------------------------ sampling frames --
 // core.py:39-54 onb_s (Duff et al.), :57-65 cosine_dir_s.  Used by the render
 // and collection kernels (compiled with -fmad=false).

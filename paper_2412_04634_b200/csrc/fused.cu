@@ -3,6 +3,7 @@
 // (12-level hash grid, 8-corner gathers from the L2-resident tables, f64
 // SH, aux) straight into the SMEM A tile, then the group runs the network
 // on tcgen05 (tc_mlp.cuh).  No X, entries or weights ever touch HBM.
+#include <cstdlib>
 #include <mutex>
 #include "common.cuh"
 #include "tc_mlp.cuh"
@@ -49,6 +50,7 @@ __global__ void k_pack_weights(nirc_spec_t sp, TcNet net, const float* __restric
 // The default NIRC input layout (test_default_layout_dimensions,
 // tests/test_neural.py:81-88): 12 levels x 2 feats, 4 SH bands, 7 aux.
 constexpr int kL = 12, kF = 2, kBands = 4, kIn = 47, kK0 = 48;
+constexpr int kDenseLevels = 4;  // dense coarse levels of the cfg2 kernel (measured best)
 
 __host__ __device__ inline bool is_default_layout(const nirc_spec_t& sp) {
   return sp.levels == kL && sp.feats == kF && sp.bands == kBands && sp.in_dim == kIn &&
@@ -56,11 +58,14 @@ __host__ __device__ inline bool is_default_layout(const nirc_spec_t& sp) {
 }
 
 // Encodes one query row into x[48] (x[47] = 0 pad), bit-identical to
-// encode_batch (encoding.py:111-157).
+// encode_batch (encoding.py:111-157).  Levels < dl.n are gathered from the
+// CTA's dense shared-memory copies, the rest from the L2-resident tables.
+template <int ND>
 __device__ __forceinline__ void encode_default(const nirc_spec_t& sp,
                                                const float* __restrict__ theta, const double* p,
                                                const double* nrm, const double* alb,
-                                               double rough, const double* d, float* x) {
+                                               double rough, const double* d, float* x,
+                                               const DenseLevels& dl, const float2* dense) {
   const float ux = norm_coord(p[0], sp.bb_min[0], sp.bb_inv[0]);
   const float uy = norm_coord(p[1], sp.bb_min[1], sp.bb_inv[1]);
   const float uz = norm_coord(p[2], sp.bb_min[2], sp.bb_inv[2]);
@@ -68,7 +73,10 @@ __device__ __forceinline__ void encode_default(const nirc_spec_t& sp,
 #pragma unroll
   for (int lvl = 0; lvl < kL; ++lvl) {
     const LevelCell c = level_cell(ux, uy, uz, sp.res[lvl]);
-    const float2 f = level_features2(theta + (size_t)lvl * T * kF, c, T - 1u);
+    // ND is a compile-time count: the 12 levels stay straight-line code and
+    // the gathers of all levels overlap in flight
+    const float2 f = lvl < ND ? level_features2_dense(dense + dl.off[lvl], dl.R[lvl], c)
+                              : level_features2(theta + (size_t)lvl * T * kF, c, T - 1u);
     x[2 * lvl] = f.x;
     x[2 * lvl + 1] = f.y;
   }
@@ -84,16 +92,19 @@ __device__ __forceinline__ void encode_default(const nirc_spec_t& sp,
   x[47] = 0.0f;
 }
 
-template <class P, int NG>
+template <class P, int NG, int ND>
 __global__ void __launch_bounds__(NG * 128, 1)
     k_full_forward_tc(nirc_spec_t sp, tc::TcNet net, tc::TcSmem L,
                       const float* __restrict__ theta, const uint8_t* __restrict__ wimg,
                       const float* __restrict__ bias_g, const double* __restrict__ pos,
                       const double* __restrict__ nrm, const double* __restrict__ alb,
                       const double* __restrict__ rough, const double* __restrict__ dirs,
-                      int64_t n, float* __restrict__ Y) {
+                      int64_t n, float* __restrict__ Y, DenseLevels dl) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint32_t tmem_base;
+  // dense coarse levels live in the region after the group A buffers
+  float2* dense = reinterpret_cast<float2*>(smem + L.a_off + NG * L.abuf_bytes);
+  if (ND > 0) fill_dense_levels(sp, dl, theta, dense);
   tc::tc_prologue(smem, L, net, NG, wimg, bias_g, tmem_base);
   const uint32_t s0 = tc::smem_u32(smem);
   const int group = threadIdx.x >> 7;
@@ -113,8 +124,8 @@ __global__ void __launch_bounds__(NG * 128, 1)
     const int64_t row = tile * tc::kTileRows + tg;
     float x[kK0];
     if (row < n) {
-      encode_default(sp, theta, pos + 3 * row, nrm + 3 * row, alb + 3 * row, rough[row],
-                     dirs + 3 * row, x);
+      encode_default<ND>(sp, theta, pos + 3 * row, nrm + 3 * row, alb + 3 * row, rough[row],
+                         dirs + 3 * row, x, dl, dense);
     } else {
 #pragma unroll
       for (int k = 0; k < kK0; ++k) x[k] = 0.0f;
@@ -149,8 +160,9 @@ __global__ void k_full_forward_simt(nirc_spec_t sp, const float* __restrict__ th
   const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= n) return;
   float a[64], b[64];
-  encode_default(sp, theta, pos + 3 * row, nrm + 3 * row, alb + 3 * row, rough[row],
-                 dirs + 3 * row, a);
+  DenseLevels none{};
+  encode_default<0>(sp, theta, pos + 3 * row, nrm + 3 * row, alb + 3 * row, rough[row],
+                 dirs + 3 * row, a, none, nullptr);
   for (int l = 0; l < sp.n_layers; ++l) {
     const int din = sp.dims[l], dout = sp.dims[l + 1];
     const float* w = W + (sp.w_off[l] - sp.grid_len);
@@ -267,7 +279,14 @@ extern "C" int nirc_full_forward(const nirc_spec_t* spec, const float* theta, co
   float* bias;
   int st = pack_weights(*spec, net, theta, s, &img, &bias);
   if (st) return st;
-  const tc::TcSmem L = tc::tc_smem_layout(net, ng, 0);
+  // coarse levels as dense shared-memory arrays (levels 0..ND-1), if the
+  // plan leaves room; NIRC_DENSE_LEVELS overrides (0 = all from L2/L1)
+  int nd_want = kDenseLevels;
+  if (const char* e = getenv("NIRC_DENSE_LEVELS")) nd_want = atoi(e);
+  const uint32_t base_total = tc::tc_smem_layout(net, ng, 0).total;
+  DenseLevels dl = dense_levels_for(*spec, 227u * 1024u - 1024u - base_total, nd_want);
+  if (dl.n != 0 && dl.n != 4 && dl.n != 5) dl = dense_levels_for(*spec, 0, 0);
+  const tc::TcSmem L = tc::tc_smem_layout(net, ng, (uint32_t)dl.off[dl.n] * 8u);
   const int64_t ntiles = (n + tc::kTileRows - 1) / tc::kTileRows;
   const int64_t want = (ntiles + ng - 1) / ng;
   const int grid = (int)(want < sm_count() ? want : sm_count());
@@ -275,17 +294,19 @@ extern "C" int nirc_full_forward(const nirc_spec_t* spec, const float* theta, co
     NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)kern,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
     kern<<<grid, threads, L.total, s>>>(*spec, net, L, theta, img, bias, pos, normal, albedo,
-                                        rough, dirs, n, Y);
+                                        rough, dirs, n, Y, dl);
     return NIRC_OK;
   };
   if (prec == tc::PrecF16x2::kId) {
-    if (ng == 4) st = launch(k_full_forward_tc<tc::PrecF16x2, 4>, 512);
-    else if (ng == 3) st = launch(k_full_forward_tc<tc::PrecF16x2, 3>, 384);
-    else if (ng == 2) st = launch(k_full_forward_tc<tc::PrecF16x2, 2>, 256);
-    else st = launch(k_full_forward_tc<tc::PrecF16x2, 1>, 128);
+    if (ng == 4 && dl.n == 5) st = launch(k_full_forward_tc<tc::PrecF16x2, 4, 5>, 512);
+    else if (ng == 4 && dl.n == 4) st = launch(k_full_forward_tc<tc::PrecF16x2, 4, 4>, 512);
+    else if (ng == 4) st = launch(k_full_forward_tc<tc::PrecF16x2, 4, 0>, 512);
+    else if (ng == 3) st = launch(k_full_forward_tc<tc::PrecF16x2, 3, 0>, 384);
+    else if (ng == 2) st = launch(k_full_forward_tc<tc::PrecF16x2, 2, 0>, 256);
+    else st = launch(k_full_forward_tc<tc::PrecF16x2, 1, 0>, 128);
   } else {
-    if (ng == 2) st = launch(k_full_forward_tc<tc::PrecTF32x3, 2>, 256);
-    else st = launch(k_full_forward_tc<tc::PrecTF32x3, 1>, 128);
+    if (ng == 2) st = launch(k_full_forward_tc<tc::PrecTF32x3, 2, 0>, 256);
+    else st = launch(k_full_forward_tc<tc::PrecTF32x3, 1, 0>, 128);
   }
   if (st) return st;
   NIRC_LAUNCH_CHECK("k_full_forward_tc");

@@ -452,6 +452,57 @@ __global__ void k_adam_apply(float* __restrict__ theta, float* __restrict__ m,
   }
 }
 
+// Same update, 4 parameters per thread through 16-byte loads (all of theta,
+// m, v, g 16-byte aligned); the n % 4 tail is done by the first threads.
+__device__ __forceinline__ void adam_one(float& th, float& mi, float& vi, float gi, float c1,
+                                         float c2, float bc1, float bc2, float lr, float eps) {
+  mi = __fadd_rn(mi, __fmul_rn(c1, __fsub_rn(gi, mi)));
+  vi = __fadd_rn(vi, __fmul_rn(c2, __fsub_rn(__fmul_rn(gi, gi), vi)));
+  const float mh = __fdiv_rn(mi, bc1);
+  const float vh = __fdiv_rn(vi, bc2);
+  th = __fsub_rn(th, __fdiv_rn(__fmul_rn(lr, mh), __fadd_rn(__fsqrt_rn(vh), eps)));
+}
+
+__global__ void k_adam_apply4(float* __restrict__ theta, float* __restrict__ m,
+                              float* __restrict__ v, const float* __restrict__ g, int64_t n,
+                              int64_t* __restrict__ t, int64_t* __restrict__ skipped, float lr,
+                              double b1, double b2, float eps, const int32_t* __restrict__ bad,
+                              const int32_t* __restrict__ gate) {
+  if (gate && gate[0]) return;
+  if (bad[0]) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) skipped[0] += 1;
+    return;
+  }
+  const int64_t tn = t[0] + 1;  // read before block 0 publishes (see k_adam_tick)
+  const float c1 = (float)(1.0 - b1);
+  const float c2 = (float)(1.0 - b2);
+  const float bc1 = (float)(1.0 - pow(b1, (double)tn));
+  const float bc2 = (float)(1.0 - pow(b2, (double)tn));
+  const int64_t n4 = n >> 2;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t i = tid; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 th = reinterpret_cast<float4*>(theta)[i];
+    float4 mi = reinterpret_cast<float4*>(m)[i];
+    float4 vi = reinterpret_cast<float4*>(v)[i];
+    const float4 gi = reinterpret_cast<const float4*>(g)[i];
+    adam_one(th.x, mi.x, vi.x, gi.x, c1, c2, bc1, bc2, lr, eps);
+    adam_one(th.y, mi.y, vi.y, gi.y, c1, c2, bc1, bc2, lr, eps);
+    adam_one(th.z, mi.z, vi.z, gi.z, c1, c2, bc1, bc2, lr, eps);
+    adam_one(th.w, mi.w, vi.w, gi.w, c1, c2, bc1, bc2, lr, eps);
+    reinterpret_cast<float4*>(theta)[i] = th;
+    reinterpret_cast<float4*>(m)[i] = mi;
+    reinterpret_cast<float4*>(v)[i] = vi;
+  }
+  if (tid < (n & 3)) {
+    const int64_t i = 4 * n4 + tid;
+    float th = theta[i], mi = m[i], vi = v[i];
+    adam_one(th, mi, vi, g[i], c1, c2, bc1, bc2, lr, eps);
+    theta[i] = th;
+    m[i] = mi;
+    v[i] = vi;
+  }
+}
+
 __global__ void k_adam_tick(int64_t* __restrict__ t, const int32_t* __restrict__ bad,
                             const int32_t* __restrict__ gate) {
   if (gate && gate[0]) return;
@@ -475,100 +526,133 @@ constexpr int kSelBins = 16384;
 constexpr int kSelShift = 53 - 14;
 
 struct SelWs {
-  uint64_t* keys;      // (n,)
-  uint32_t* hist;      // (kSelBins,)
-  uint32_t* fill;      // (kSelBins,)
-  uint32_t* boff;      // (kSelBins + 1,) exclusive offsets
-  int32_t* bstar;      // [0] last bucket taken, [1] staged count
-  uint64_t* skey;      // staged keys (<= n)
-  int64_t* sidx;       // staged indices (<= n) -- the batch is sidx[0:B]
+  // one slice per optimizer step (blockIdx.y), strides n / kSelBins
+  uint64_t* keys;      // (steps, n)
+  uint32_t* hist;      // (steps, kSelBins)
+  uint32_t* fill;      // (steps, kSelBins)
+  uint32_t* boff;      // (steps, kSelBins + 1) exclusive offsets
+  int32_t* bstar;      // (steps, 2): [0] last bucket taken, [1] staged count
+  uint64_t* skey;      // (steps, n) staged keys
+  int64_t* sidx;       // (steps, n) staged indices -- step s's batch is sidx[s*n : s*n+B]
 };
 
+// keys of step s = blockIdx.y: dims offset + s*n + i (caches.py:327-328)
 __global__ void k_sel_hist(uint64_t K, uint64_t offset, int64_t n, SelWs w,
                            const int32_t* __restrict__ flags) {
   extern __shared__ uint32_t h[];  // kSelBins
   if (flags && (flags[0] & 3)) return;
+  const int s = blockIdx.y;
+  uint64_t* keys = w.keys + (int64_t)s * n;
+  uint32_t* hist = w.hist + (int64_t)s * kSelBins;
+  const uint64_t off = offset + (uint64_t)s * (uint64_t)n;
   for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) h[i] = 0;
   __syncthreads();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = shuffle_key(K, offset + i);
-    w.keys[i] = k;
+    const uint64_t k = shuffle_key(K, off + i);
+    keys[i] = k;
     atomicAdd(&h[k >> kSelShift], 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kSelBins; i += blockDim.x)
-    if (h[i]) atomicAdd(&w.hist[i], h[i]);
+    if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 
 __global__ void k_sel_scan(int64_t n, int B, SelWs w, const int32_t* __restrict__ flags) {
   __shared__ uint32_t part[1024];
   if (flags && (flags[0] & 3)) return;
+  const int sy = blockIdx.y;
+  const uint32_t* hist = w.hist + (int64_t)sy * kSelBins;
+  uint32_t* boff = w.boff + (int64_t)sy * (kSelBins + 1);
+  uint32_t* fill = w.fill + (int64_t)sy * kSelBins;
+  int32_t* bstar = w.bstar + 2 * sy;
   const int t = threadIdx.x;  // 1024 threads x 16 bins
   constexpr int kPer = kSelBins / 1024;
   uint32_t v[kPer], s = 0;
   for (int q = 0; q < kPer; ++q) {
-    v[q] = w.hist[t * kPer + q];
+    v[q] = hist[t * kPer + q];
     s += v[q];
   }
-  part[t] = s;
-  __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {  // inclusive Hillis-Steele scan
-    const uint32_t x = t >= off ? part[t - off] : 0u;
-    __syncthreads();
-    part[t] += x;
-    __syncthreads();
+  // block-wide inclusive scan of the per-thread sums (warp shuffles)
+  const int lane = t & 31, wid = t >> 5;
+  uint32_t x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
   }
-  uint32_t run = part[t] - s;
+  if (lane == 31) part[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t z = part[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    part[lane] = z;
+  }
+  __syncthreads();
+  uint32_t run = x - s + (wid > 0 ? part[wid - 1] : 0u);
   for (int q = 0; q < kPer; ++q) {
     const int b = t * kPer + q;
-    w.boff[b] = run;
-    w.fill[b] = 0;
+    boff[b] = run;
+    fill[b] = 0;
     // the bucket containing rank B-1 (or the last bucket when n <= B)
     if (run < (uint32_t)B && run + v[q] >= (uint32_t)B) {
-      w.bstar[0] = b;
-      w.bstar[1] = (int32_t)(run + v[q]);
+      bstar[0] = b;
+      bstar[1] = (int32_t)(run + v[q]);
     }
     run += v[q];
   }
-  if (t == 1023) w.boff[kSelBins] = run;
+  if (t == 1023) boff[kSelBins] = run;
   if (n <= B && t == 0) {
-    w.bstar[0] = kSelBins - 1;
-    w.bstar[1] = (int32_t)n;
+    bstar[0] = kSelBins - 1;
+    bstar[1] = (int32_t)n;
   }
 }
 
 __global__ void k_sel_scatter(int64_t n, SelWs w, const int32_t* __restrict__ flags) {
   if (flags && (flags[0] & 3)) return;
-  const int bs = w.bstar[0];
+  const int s = blockIdx.y;
+  const uint64_t* keys = w.keys + (int64_t)s * n;
+  const uint32_t* boff = w.boff + (int64_t)s * (kSelBins + 1);
+  uint32_t* fill = w.fill + (int64_t)s * kSelBins;
+  uint64_t* skey = w.skey + (int64_t)s * n;
+  int64_t* sidx = w.sidx + (int64_t)s * n;
+  const int bs = w.bstar[2 * s];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = w.keys[i];
+    const uint64_t k = keys[i];
     const int b = (int)(k >> kSelShift);
     if (b <= bs) {
-      const uint32_t pos = w.boff[b] + atomicAdd(&w.fill[b], 1u);
-      w.skey[pos] = k;
-      w.sidx[pos] = i;
+      const uint32_t pos = boff[b] + atomicAdd(&fill[b], 1u);
+      skey[pos] = k;
+      sidx[pos] = i;
     }
   }
 }
 
-__global__ void k_sel_sort(SelWs w, const int32_t* __restrict__ flags) {
+__global__ void k_sel_sort(int64_t n, SelWs w, const int32_t* __restrict__ flags) {
   if (flags && (flags[0] & 3)) return;
+  const int s = blockIdx.y;
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b > w.bstar[0]) return;
-  const uint32_t lo = w.boff[b], hi = w.boff[b + 1];
+  if (b > w.bstar[2 * s]) return;
+  const uint32_t* boff = w.boff + (int64_t)s * (kSelBins + 1);
+  uint64_t* skey = w.skey + (int64_t)s * n;
+  int64_t* sidx = w.sidx + (int64_t)s * n;
+  const uint32_t lo = boff[b], hi = boff[b + 1];
   for (uint32_t i = lo + 1; i < hi; ++i) {  // insertion sort by (key, index)
-    const uint64_t k = w.skey[i];
-    const int64_t x = w.sidx[i];
+    const uint64_t k = skey[i];
+    const int64_t x = sidx[i];
     uint32_t j = i;
-    while (j > lo && (w.skey[j - 1] > k || (w.skey[j - 1] == k && w.sidx[j - 1] > x))) {
-      w.skey[j] = w.skey[j - 1];
-      w.sidx[j] = w.sidx[j - 1];
+    while (j > lo && (skey[j - 1] > k || (skey[j - 1] == k && sidx[j - 1] > x))) {
+      skey[j] = skey[j - 1];
+      sidx[j] = sidx[j - 1];
       --j;
     }
-    w.skey[j] = k;
-    w.sidx[j] = x;
+    skey[j] = k;
+    sidx[j] = x;
   }
 }
 
@@ -760,6 +844,29 @@ extern "C" int nirc_loss(int32_t kind, const float* Y, const double* target, con
   return NIRC_OK;
 }
 
+// Dense Adam apply + tick; the non-finite check already ran (adam_bad).
+static int launch_adam(float* theta, float* m, float* v, const float* grad, int64_t n,
+                       int64_t* t, int64_t* skipped, float lr, const int32_t* bad,
+                       const int32_t* gate, cudaStream_t s, double b1 = 0.9, double b2 = 0.99,
+                       double eps = 1e-8) {
+  const bool aligned = ((reinterpret_cast<uintptr_t>(theta) | reinterpret_cast<uintptr_t>(m) |
+                         reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(grad)) &
+                        15u) == 0;
+  if (aligned) {
+    const int64_t n4 = (n >> 2) > 0 ? (n >> 2) : 1;
+    const int nb = (int)((n4 + 255) / 256 < 148 * 8 ? (n4 + 255) / 256 : 148 * 8);
+    k_adam_apply4<<<nb, 256, 0, s>>>(theta, m, v, grad, n, t, skipped, lr, b1, b2, (float)eps,
+                                     bad, gate);
+  } else {
+    k_adam_apply<<<148 * 4, 256, 0, s>>>(theta, m, v, grad, n, t, skipped, lr, b1, b2,
+                                         (float)eps, bad, gate);
+  }
+  NIRC_LAUNCH_CHECK("k_adam_apply");
+  k_adam_tick<<<1, 1, 0, s>>>(t, bad, gate);
+  NIRC_LAUNCH_CHECK("k_adam_tick");
+  return NIRC_OK;
+}
+
 extern "C" int nirc_adam_step(float* theta, float* m, float* v, const float* grad, int64_t n,
                               int64_t* t, int64_t* skipped, double lr, double beta1,
                               double beta2, double eps, const int32_t* gate_flags,
@@ -769,19 +876,14 @@ extern "C" int nirc_adam_step(float* theta, float* m, float* v, const float* gra
   const int nb = 148 * 4;
   k_adam_check<<<nb, 256, 0, S(stream)>>>(grad, n, scratch, gate_flags);
   NIRC_LAUNCH_CHECK("k_adam_check");
-  k_adam_apply<<<nb, 256, 0, S(stream)>>>(theta, m, v, grad, n, t, skipped, (float)lr, beta1,
-                                          beta2, (float)eps, scratch, gate_flags);
-  NIRC_LAUNCH_CHECK("k_adam_apply");
-  k_adam_tick<<<1, 1, 0, S(stream)>>>(t, scratch, gate_flags);
-  NIRC_LAUNCH_CHECK("k_adam_tick");
-  return NIRC_OK;
+  return launch_adam(theta, m, v, grad, n, t, skipped, (float)lr, scratch, gate_flags,
+                     S(stream), beta1, beta2, eps);
 }
 
 // ---------------------------------------------------------------- train --
 namespace {
 struct TrainWs {
   SelWs sel;
-  int64_t* idx;
   float *X, *zs, *Y, *dY, *dzs, *dX, *grad;
   double* partial;
   int32_t* adam_bad;
@@ -790,7 +892,9 @@ struct TrainWs {
   size_t bytes;
 };
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
-TrainWs carve_train(const nirc_spec_t& sp, int64_t n, int64_t B, void* base) {
+// `steps` selection slices (all optimizer steps of a frame are selected at
+// once: the batch never depends on theta).
+TrainWs carve_train(const nirc_spec_t& sp, int64_t n, int64_t B, int steps, void* base) {
   TrainWs w{};
   char* p = reinterpret_cast<char*>(base);
   size_t off = 0;
@@ -800,14 +904,13 @@ TrainWs carve_train(const nirc_spec_t& sp, int64_t n, int64_t B, void* base) {
     return r;
   };
   const int zw = zs_width(sp);
-  w.sel.keys = (uint64_t*)take(n * 8);
-  w.sel.hist = (uint32_t*)take(kSelBins * 4);
-  w.sel.fill = (uint32_t*)take(kSelBins * 4);
-  w.sel.boff = (uint32_t*)take((kSelBins + 1) * 4);
-  w.sel.bstar = (int32_t*)take(16);
-  w.sel.skey = (uint64_t*)take(n * 8);
-  w.sel.sidx = (int64_t*)take(n * 8);
-  w.idx = w.sel.sidx;
+  w.sel.keys = (uint64_t*)take(steps * n * 8);
+  w.sel.hist = (uint32_t*)take(steps * kSelBins * 4);
+  w.sel.fill = (uint32_t*)take(steps * kSelBins * 4);
+  w.sel.boff = (uint32_t*)take(steps * (kSelBins + 1) * 4);
+  w.sel.bstar = (int32_t*)take(steps * 8 + 8);
+  w.sel.skey = (uint64_t*)take(steps * n * 8);
+  w.sel.sidx = (int64_t*)take(steps * n * 8);
   w.X = (float*)take(B * sp.in_dim * 4);
   w.zs = (float*)take(B * zw * 4);
   w.Y = (float*)take(B * 3 * 4 + 16);
@@ -828,26 +931,32 @@ TrainWs carve_train(const nirc_spec_t& sp, int64_t n, int64_t B, void* base) {
 extern "C" int64_t nirc_train_workspace_bytes(const nirc_spec_t* spec, int64_t n_records,
                                               int32_t batch_cap) {
   const int64_t B = n_records < batch_cap ? n_records : batch_cap;
-  return (int64_t)carve_train(*spec, n_records, B, nullptr).bytes;
+  return (int64_t)carve_train(*spec, n_records, B, 1, nullptr).bytes;
 }
 
-// Batch selection of one optimizer step into w.idx (caches.py:327-329).
-static int select_batch(const TrainWs& w, uint64_t seed, int64_t frame, int32_t step, int64_t n,
-                        int64_t B, int32_t* status_flags, int64_t* batch_idx_out,
-                        cudaStream_t s) {
+extern "C" int64_t nirc_train_frame_workspace_bytes(const nirc_spec_t* spec, int64_t n_records,
+                                                    int32_t batch_cap, int32_t steps) {
+  const int64_t B = n_records < batch_cap ? n_records : batch_cap;
+  return (int64_t)carve_train(*spec, n_records, B, steps < 1 ? 1 : steps, nullptr).bytes;
+}
+
+// Batch selection of optimizer steps step0 .. step0+steps-1 (caches.py:
+// 327-329): slice s of w.sel.sidx holds argsort(keys of step step0+s)[:B].
+static int select_batches(const TrainWs& w, uint64_t seed, int64_t frame, int32_t step0,
+                          int32_t steps, int64_t n, int64_t B, int32_t* status_flags,
+                          cudaStream_t s) {
   const uint64_t K = stream_key(seed, P_SHUFFLE, 0, (uint64_t)frame, 0);
-  const uint64_t off = (uint64_t)step * (uint64_t)n;
-  NIRC_CUDA_TRY(cudaMemsetAsync(w.sel.hist, 0, kSelBins * 4, s));
-  const int sel_grid = (int)((n + 255) / 256 < 4 * 148 ? (n + 255) / 256 : 4 * 148);
+  const uint64_t off = (uint64_t)step0 * (uint64_t)n;
+  NIRC_CUDA_TRY(cudaMemsetAsync(w.sel.hist, 0, (size_t)steps * kSelBins * 4, s));
+  int sel_grid = (int)((n + 255) / 256 < 4 * 148 ? (n + 255) / 256 : 4 * 148);
+  sel_grid = (sel_grid + steps - 1) / steps;
   NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)k_sel_hist,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSelBins * 4));
-  k_sel_hist<<<sel_grid, 256, kSelBins * 4, s>>>(K, off, n, w.sel, status_flags);
-  k_sel_scan<<<1, 1024, 0, s>>>(n, (int)B, w.sel, status_flags);
-  k_sel_scatter<<<sel_grid, 256, 0, s>>>(n, w.sel, status_flags);
-  k_sel_sort<<<kSelBins / 128, 128, 0, s>>>(w.sel, status_flags);
+  k_sel_hist<<<dim3(sel_grid, steps), 256, kSelBins * 4, s>>>(K, off, n, w.sel, status_flags);
+  k_sel_scan<<<dim3(1, steps), 1024, 0, s>>>(n, (int)B, w.sel, status_flags);
+  k_sel_scatter<<<dim3(sel_grid, steps), 256, 0, s>>>(n, w.sel, status_flags);
+  k_sel_sort<<<dim3(kSelBins / 128, steps), 128, 0, s>>>(n, w.sel, status_flags);
   NIRC_LAUNCH_CHECK("k_sel_*");
-  if (batch_idx_out)
-    NIRC_CUDA_TRY(cudaMemcpyAsync(batch_idx_out, w.idx, B * 8, cudaMemcpyDeviceToDevice, s));
   return NIRC_OK;
 }
 
@@ -863,54 +972,42 @@ static int train_args_ok(const nirc_spec_t* spec, const nirc_records_t* rec, int
   return NIRC_OK;
 }
 
-extern "C" int nirc_train_step(const nirc_spec_t* spec, float* theta, float* m, float* v,
-                               int64_t* t, int64_t* skipped, const nirc_records_t* rec,
-                               uint64_t seed, int64_t frame, int32_t step, int32_t batch_cap,
-                               int32_t loss_kind, double loss_eps, double lr,
-                               double* running_mean, double* loss_out, int32_t* status_flags,
-                               int64_t* batch_idx_out, void* workspace,
-                               int64_t workspace_bytes, void* stream) {
-  int st = train_args_ok(spec, rec, batch_cap);
-  if (st) return st;
-  const int64_t n = rec->n;
-  const int64_t B = n < batch_cap ? n : batch_cap;
-  TrainWs w = carve_train(*spec, n, B, workspace);
-  if ((int64_t)w.bytes > workspace_bytes) {
-    set_last_error("train workspace too small (%lld < %lld)", (long long)workspace_bytes,
-                   (long long)w.bytes);
-    return NIRC_E_CONFIG;
-  }
+static bool use_fused(const nirc_spec_t& sp, int loss_kind) {
+  return (loss_kind == 0 || loss_kind == 1) && fused_supported(sp) &&
+         fused_smem_bytes(sp) <= 227 * 1024;
+}
+
+// One optimizer step on the batch rows idx[0:B] (caches.py:330-350).
+static int step_body(const nirc_spec_t* spec, float* theta, float* m, float* v, int64_t* t,
+                     int64_t* skipped, const nirc_records_t* rec, const int64_t* idx,
+                     int64_t B, int32_t loss_kind, double loss_eps, double lr,
+                     double* running_mean, double* loss_out, int32_t* status_flags,
+                     const TrainWs& w, void* stream) {
   cudaStream_t s = S(stream);
-  if ((st = select_batch(w, seed, frame, step, n, B, status_flags, batch_idx_out, s))) return st;
-  if ((loss_kind == 0 || loss_kind == 1) && fused_supported(*spec) &&
-      fused_smem_bytes(*spec) <= 227 * 1024) {
+  int st;
+  if (use_fused(*spec, loss_kind)) {
     // one fused kernel per step: encode, forward, loss, backward, scatter
     const int64_t ntiles = (B + kFusedTileRows - 1) / kFusedTileRows;
-    if ((st = launch_fused_train(*spec, theta, *rec, w.idx, B, loss_kind, loss_eps, w.grad,
+    if ((st = launch_fused_train(*spec, theta, *rec, idx, B, loss_kind, loss_eps, w.grad,
                                  w.fpart, w.floss, loss_out, status_flags, w.adam_bad, s, 0,
                                  ntiles, 0)))
       return st;
-    const int nb = 148 * 4;
-    k_adam_apply<<<nb, 256, 0, s>>>(theta, m, v, w.grad, spec->theta_len, t, skipped, (float)lr,
-                                    0.9, 0.99, (float)1e-8, w.adam_bad, status_flags);
-    NIRC_LAUNCH_CHECK("k_adam_apply");
-    k_adam_tick<<<1, 1, 0, s>>>(t, w.adam_bad, status_flags);
-    NIRC_LAUNCH_CHECK("k_adam_tick");
-    return NIRC_OK;
+    return launch_adam(theta, m, v, w.grad, spec->theta_len, t, skipped, (float)lr, w.adam_bad,
+                       status_flags, s);
   }
   const size_t sm = simt_smem_bytes(*spec);
   if ((st = set_smem((const void*)k_train_forward, sm))) return st;
   k_train_forward<<<blocks_for(B, kRowsPerBlock), kRowsPerBlock, sm, s>>>(
-      *spec, theta, *rec, w.idx, B, w.X, w.zs, w.Y, status_flags);
+      *spec, theta, *rec, idx, B, w.X, w.zs, w.Y, status_flags);
   NIRC_LAUNCH_CHECK("k_train_forward");
   const int nb = blocks_for(B, kLossThreads);
   if (loss_kind == 2) {  // variance: EMA of the residual mean first (caches.py:340-343)
     k_loss<<<nb, kLossThreads, 0, s>>>(loss_kind, w.Y, rec->target, rec->pdf, running_mean,
-                                        loss_eps, B, w.dY, w.partial, status_flags, w.idx, 1);
+                                        loss_eps, B, w.dY, w.partial, status_flags, idx, 1);
     k_loss_final<<<1, 32, 0, s>>>(w.partial, nb, B, loss_out, status_flags, running_mean, 1);
   }
   k_loss<<<nb, kLossThreads, 0, s>>>(loss_kind, w.Y, rec->target, rec->pdf, running_mean,
-                                      loss_eps, B, w.dY, w.partial, status_flags, w.idx, 0);
+                                      loss_eps, B, w.dY, w.partial, status_flags, idx, 0);
   NIRC_LAUNCH_CHECK("k_loss");
   k_loss_final<<<1, 32, 0, s>>>(w.partial, nb, B, loss_out, status_flags, nullptr, 0);
   NIRC_LAUNCH_CHECK("k_loss_final");
@@ -922,11 +1019,62 @@ extern "C" int nirc_train_step(const nirc_spec_t* spec, float* theta, float* m, 
   dim3 g(blocks_for(B, kDwRows), spec->n_layers, dw_zsplit(*spec));
   k_weight_grad<<<g, kDwThreads, 0, s>>>(*spec, w.X, w.zs, w.dzs, B, w.grad, status_flags);
   NIRC_LAUNCH_CHECK("k_weight_grad");
-  k_train_scatter<<<blocks_for(B * spec->levels, 256), 256, 0, s>>>(*spec, *rec, w.idx, B, w.dX,
+  k_train_scatter<<<blocks_for(B * spec->levels, 256), 256, 0, s>>>(*spec, *rec, idx, B, w.dX,
                                                                    w.grad, status_flags);
   NIRC_LAUNCH_CHECK("k_train_scatter");
   return nirc_adam_step(theta, m, v, w.grad, spec->theta_len, t, skipped, lr, 0.9, 0.99, 1e-8,
                         status_flags, w.adam_bad, stream);
+}
+
+extern "C" int nirc_train_step(const nirc_spec_t* spec, float* theta, float* m, float* v,
+                               int64_t* t, int64_t* skipped, const nirc_records_t* rec,
+                               uint64_t seed, int64_t frame, int32_t step, int32_t batch_cap,
+                               int32_t loss_kind, double loss_eps, double lr,
+                               double* running_mean, double* loss_out, int32_t* status_flags,
+                               int64_t* batch_idx_out, void* workspace,
+                               int64_t workspace_bytes, void* stream) {
+  int st = train_args_ok(spec, rec, batch_cap);
+  if (st) return st;
+  const int64_t n = rec->n;
+  const int64_t B = n < batch_cap ? n : batch_cap;
+  TrainWs w = carve_train(*spec, n, B, 1, workspace);
+  if ((int64_t)w.bytes > workspace_bytes) {
+    set_last_error("train workspace too small (%lld < %lld)", (long long)workspace_bytes,
+                   (long long)w.bytes);
+    return NIRC_E_CONFIG;
+  }
+  cudaStream_t s = S(stream);
+  if ((st = select_batches(w, seed, frame, step, 1, n, B, status_flags, s))) return st;
+  if (batch_idx_out)
+    NIRC_CUDA_TRY(cudaMemcpyAsync(batch_idx_out, w.sel.sidx, B * 8, cudaMemcpyDeviceToDevice, s));
+  return step_body(spec, theta, m, v, t, skipped, rec, w.sel.sidx, B, loss_kind, loss_eps, lr,
+                   running_mean, loss_out, status_flags, w, stream);
+}
+
+extern "C" int nirc_train_frame(const nirc_spec_t* spec, float* theta, float* m, float* v,
+                                int64_t* t, int64_t* skipped, const nirc_records_t* rec,
+                                uint64_t seed, int64_t frame, int32_t steps, int32_t batch_cap,
+                                int32_t loss_kind, double loss_eps, double lr,
+                                double* running_mean, double* loss_out, int32_t* status_flags,
+                                void* workspace, int64_t workspace_bytes, void* stream) {
+  int st = train_args_ok(spec, rec, batch_cap);
+  if (st) return st;
+  if (steps < 1) { set_last_error("steps must be positive"); return NIRC_E_CONFIG; }
+  const int64_t n = rec->n;
+  const int64_t B = n < batch_cap ? n : batch_cap;
+  TrainWs w = carve_train(*spec, n, B, steps, workspace);
+  if ((int64_t)w.bytes > workspace_bytes) {
+    set_last_error("train workspace too small (%lld < %lld)", (long long)workspace_bytes,
+                   (long long)w.bytes);
+    return NIRC_E_CONFIG;
+  }
+  if ((st = select_batches(w, seed, frame, 0, steps, n, B, status_flags, S(stream)))) return st;
+  for (int k = 0; k < steps; ++k)
+    if ((st = step_body(spec, theta, m, v, t, skipped, rec, w.sel.sidx + (int64_t)k * n, B,
+                        loss_kind, loss_eps, lr, running_mean, loss_out + k, status_flags, w,
+                        stream)))
+      return st;
+  return NIRC_OK;
 }
 
 // ---- multi-GPU split of nirc_train_step ------------------
@@ -945,8 +1093,7 @@ extern "C" int nirc_train_grad(const nirc_spec_t* spec, const float* theta,
                                void* stream) {
   int st = train_args_ok(spec, rec, batch_cap);
   if (st) return st;
-  if (!(loss_kind == 0 || loss_kind == 1) || !fused_supported(*spec) ||
-      fused_smem_bytes(*spec) > 227 * 1024) {
+  if (!use_fused(*spec, loss_kind)) {
     set_last_error("sharded training needs the fused l2 / relative_l2 path");
     return NIRC_E_UNSUPPORTED;
   }
@@ -958,15 +1105,17 @@ extern "C" int nirc_train_grad(const nirc_spec_t* spec, const float* theta,
                    (long long)tile_end, (long long)ntiles);
     return NIRC_E_CONFIG;
   }
-  TrainWs w = carve_train(*spec, n, B, workspace);
+  TrainWs w = carve_train(*spec, n, B, 1, workspace);
   if ((int64_t)w.bytes > workspace_bytes) {
     set_last_error("train workspace too small (%lld < %lld)", (long long)workspace_bytes,
                    (long long)w.bytes);
     return NIRC_E_CONFIG;
   }
   cudaStream_t s = S(stream);
-  if ((st = select_batch(w, seed, frame, step, n, B, status_flags, batch_idx_out, s))) return st;
-  return launch_fused_train(*spec, theta, *rec, w.idx, B, loss_kind, loss_eps, grad, w.fpart,
+  if ((st = select_batches(w, seed, frame, step, 1, n, B, status_flags, s))) return st;
+  if (batch_idx_out)
+    NIRC_CUDA_TRY(cudaMemcpyAsync(batch_idx_out, w.sel.sidx, B * 8, cudaMemcpyDeviceToDevice, s));
+  return launch_fused_train(*spec, theta, *rec, w.sel.sidx, B, loss_kind, loss_eps, grad, w.fpart,
                             w.floss, aux, status_flags, nullptr, s, tile_begin, tile_end, 1);
 }
 

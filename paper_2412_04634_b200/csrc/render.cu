@@ -1,6 +1,6 @@
 // Two-level (MLMC) frame estimator and training-record collection on
-// sm_100a.  Compiled with -fmad=false: the fp64 path walks follow the
-// reference's operation order.
+// sm_100a.  The fp64 path walks follow the reference's operation order (FMA
+// contraction allowed, as numba fastmath allows it; build.py NIRC_RENDER_FMAD).
 //
 // Frame pipeline (nirc_render, one stream, no host sync):
 //   K5  k_trace       one thread per (pixel, sample): fp64 path tracer
@@ -200,54 +200,257 @@ __device__ inline bool trace_vertex(const nirc_scene_t& scn, const nirc_render_c
   return p.v >= pt::MAXB;
 }
 
+// ---------------------------------------------------------------------
+// Training records: walk_record (kernels.py:85-286) driven by
+// collect_paths_kernel (:289-311).  Each path's vertices are kept in a
+// vertex-major staging area and the backward sweep runs when the path ends;
+// a scan turns per-path record counts into offsets and a compaction writes
+// the records in (path, vertex) order -- the reference's row order.  The
+// walk is written per lane (walk_start / walk_vertex / walk_finish) so the
+// persistent tracer can interleave training paths with camera paths.
+struct Stage {
+  // vertex-major: field[v * count + p]
+  double *pos, *ns, *alb, *rough, *wi, *pdf, *tgt, *tfull;
+  uint8_t* keep;
+  int32_t* nrec;   // per path
+  int32_t* nvert;  // per path
+  int64_t count;
+  int64_t path0;   // global index of local path 0 (multi-GPU path shards)
+};
+
+struct WalkLane {
+  V3 o, d, lns;
+  double prev_pdf;
+  uint64_t key;
+  int64_t p;
+  int v, esc;
+  double env_m[3], env_r[3];
+  // per-vertex backward-sweep inputs (local memory)
+  double mise[pt::MAXB][3], emit[pt::MAXB][3], nee[pt::MAXB][3], fcp[pt::MAXB][3];
+};
+
+__device__ inline void walk_start(WalkLane& w, const double* cam, uint64_t seed, uint64_t frame,
+                                  const Stage& st, int64_t p) {
+  w.p = p;
+  w.key = stream_key(seed, P_TRAIN, frame, (uint64_t)(st.path0 + p), 0);
+  const double sx = rand_uniform(w.key, DIM_JITTER_X) * cam[14];
+  const double sy = rand_uniform(w.key, DIM_JITTER_Y) * cam[15];
+  const int ix = (int)sx, iy = (int)sy;
+  pt::camera_ray(cam, ix, iy, sx - ix, sy - iy, w.o, w.d);
+  w.prev_pdf = -1.0;
+  w.lns = {0.0, 0.0, 0.0};
+  w.v = 0;
+  w.esc = 0;
+  for (int c = 0; c < 3; ++c) w.env_m[c] = w.env_r[c] = 0.0;
+}
+
+// One vertex of walk_record; returns true when the path ended (w.v = the
+// vertex count n).
+__device__ inline bool walk_vertex(const nirc_scene_t& scn, WalkLane& w, const Stage& st) {
+  const int v = w.v;
+  const int64_t C = st.count, p = w.p;
+  const pt::Hit hh = pt::intersect<false>(scn, w.o, w.d, pt::T_FAR);
+  if (hh.kind < 0) {
+    if (scn.env_kind != pt::ENV_NONE) {
+      const V3 e = pt::env_eval(scn, w.d);
+      w.env_r[0] = e.x; w.env_r[1] = e.y; w.env_r[2] = e.z;
+      double wgt = 1.0;
+      if (w.prev_pdf >= 0.0) {
+        const double pn = pt::nee_pdf_for_env(scn, w.lns, w.d);
+        wgt = w.prev_pdf / (w.prev_pdf + pn);
+      }
+      w.env_m[0] = wgt * e.x; w.env_m[1] = wgt * e.y; w.env_m[2] = wgt * e.z;
+    }
+    w.esc = 1;
+    return true;
+  }
+  const V3 wo = {-w.d.x, -w.d.y, -w.d.z};
+  const double flip = (hh.n.x * wo.x + hh.n.y * wo.y + hh.n.z * wo.z) >= 0.0 ? 1.0 : -1.0;
+  const V3 ns = {hh.n.x * flip, hh.n.y * flip, hh.n.z * flip};
+  const V3 em = pt::ld3(scn.mat_emit, hh.mid);
+  if (em.x > 0.0 || em.y > 0.0 || em.z > 0.0) {
+    double wgt = 1.0;
+    if (w.prev_pdf >= 0.0) {
+      const double pn = pt::nee_pdf_for_hit(scn, hh.kind, hh.prim, hh.t, w.d, hh.n);
+      wgt = w.prev_pdf / (w.prev_pdf + pn);
+    }
+    w.mise[v][0] = wgt * em.x; w.mise[v][1] = wgt * em.y; w.mise[v][2] = wgt * em.z;
+    w.emit[v][0] = em.x; w.emit[v][1] = em.y; w.emit[v][2] = em.z;
+  } else {
+    w.mise[v][0] = w.mise[v][1] = w.mise[v][2] = 0.0;
+    w.emit[v][0] = w.emit[v][1] = w.emit[v][2] = 0.0;
+  }
+  const int mkind = scn.mat_kind[hh.mid];
+  const int delta = mkind == pt::MAT_MIRROR ? 1 : 0;
+  const V3 alb = pt::ld3(scn.mat_albedo, hh.mid);
+  const double rough = scn.mat_rough[hh.mid];
+  const int64_t at = (int64_t)v * C + p;
+  st.pos[3 * at] = hh.p.x; st.pos[3 * at + 1] = hh.p.y; st.pos[3 * at + 2] = hh.p.z;
+  st.ns[3 * at] = ns.x; st.ns[3 * at + 1] = ns.y; st.ns[3 * at + 2] = ns.z;
+  st.alb[3 * at] = alb.x; st.alb[3 * at + 1] = alb.y; st.alb[3 * at + 2] = alb.z;
+  st.rough[at] = rough;
+  const int base = VERTEX_DIM_BASE + v * DIMS_PER_VERTEX;
+  const uint64_t key = w.key;
+  V3 q = {0.0, 0.0, 0.0};
+  if (delta == 0)
+    q = pt::nee_contrib(scn, hh.p, ns, hh.n, mkind, alb, rough, wo,
+                        rand_uniform(key, base + OFF_LIGHT_PICK),
+                        rand_uniform(key, base + OFF_LIGHT_U),
+                        rand_uniform(key, base + OFF_LIGHT_U + 1), 0);
+  w.nee[v][0] = q.x; w.nee[v][1] = q.y; w.nee[v][2] = q.z;
+  int alive = 1;
+  double rr_div = 1.0;
+  if (v >= pt::RR_START) {
+    if (rand_uniform(key, base + OFF_RR) >= pt::RR_SURVIVE) alive = 0;
+    else rr_div = pt::RR_SURVIVE;
+  }
+  int cont = 0;
+  double vpdf = 0.0;
+  V3 vwi = {0.0, 0.0, 0.0};
+  w.fcp[v][0] = w.fcp[v][1] = w.fcp[v][2] = 0.0;
+  if (alive == 1 && v < pt::MAXB - 1) {
+    const pt::BsdfSample b = pt::bsdf_sample(mkind, alb, rough, ns, wo,
+                                             rand_uniform(key, base + OFF_BSDF_U),
+                                             rand_uniform(key, base + OFF_BSDF_U + 1));
+    if (b.pdf > 0.0) {
+      const double ci = b.wi.x * ns.x + b.wi.y * ns.y + b.wi.z * ns.z;
+      if (ci > 0.0) {
+        const double inv = 1.0 / (b.pdf * rr_div);
+        vwi = b.wi;
+        vpdf = b.delta == 1 ? -1.0 : b.pdf;
+        w.fcp[v][0] = b.f.x * ci * inv;
+        w.fcp[v][1] = b.f.y * ci * inv;
+        w.fcp[v][2] = b.f.z * ci * inv;
+        w.prev_pdf = vpdf;
+        const double sg = (hh.n.x * b.wi.x + hh.n.y * b.wi.y + hh.n.z * b.wi.z) > 0.0 ? 1.0 : -1.0;
+        w.o = {hh.p.x + sg * scn.eps * hh.n.x, hh.p.y + sg * scn.eps * hh.n.y,
+               hh.p.z + sg * scn.eps * hh.n.z};
+        w.d = b.wi;
+        w.lns = ns;
+        cont = 1;
+      }
+    }
+  }
+  st.wi[3 * at] = vwi.x; st.wi[3 * at + 1] = vwi.y; st.wi[3 * at + 2] = vwi.z;
+  st.pdf[at] = vpdf;
+  st.keep[at] = (delta == 0 && vpdf > 0.0) ? 1 : 0;
+  w.v = v + 1;
+  return cont == 0;
+}
+
+// Backward sweep (kernels.py:249-277) over the path's w.v vertices.
+__device__ inline void walk_finish(const WalkLane& w, const Stage& st) {
+  const int64_t C = st.count, p = w.p;
+  const int n = w.v;
+  double lr = 0.0, lg = 0.0, lb = 0.0;
+  int nrec = 0;
+  for (int v = n - 1; v >= 0; --v) {
+    double cr, cg, cb, qr, qg, qb;
+    if (v == n - 1) {
+      cr = w.esc ? w.env_m[0] : 0.0; cg = w.esc ? w.env_m[1] : 0.0; cb = w.esc ? w.env_m[2] : 0.0;
+      qr = w.esc ? w.env_r[0] : 0.0; qg = w.esc ? w.env_r[1] : 0.0; qb = w.esc ? w.env_r[2] : 0.0;
+    } else {
+      cr = w.mise[v + 1][0] + lr; cg = w.mise[v + 1][1] + lg; cb = w.mise[v + 1][2] + lb;
+      qr = w.emit[v + 1][0] + lr; qg = w.emit[v + 1][1] + lg; qb = w.emit[v + 1][2] + lb;
+    }
+    const int64_t at = (int64_t)v * C + p;
+    st.tgt[3 * at] = cr; st.tgt[3 * at + 1] = cg; st.tgt[3 * at + 2] = cb;
+    st.tfull[3 * at] = qr; st.tfull[3 * at + 1] = qg; st.tfull[3 * at + 2] = qb;
+    lr = w.nee[v][0] + w.fcp[v][0] * cr;
+    lg = w.nee[v][1] + w.fcp[v][1] * cg;
+    lb = w.nee[v][2] + w.fcp[v][2] * cb;
+    nrec += st.keep[at];
+  }
+  st.nrec[p] = nrec;
+  st.nvert[p] = n;
+}
+
+// Stand-alone collection (Cache.collect without a render): one thread per path.
+__global__ void k_walk_record(nirc_scene_t scn, const double* __restrict__ cam, uint64_t seed,
+                              uint64_t frame, Stage st) {
+  __shared__ __align__(16) unsigned char scene_sm[pt::kSceneSmemBytes];
+  pt::stage_scene(scn, scene_sm);
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= st.count) return;
+  WalkLane w;
+  walk_start(w, cam, seed, frame, st, p);
+  while (!walk_vertex(scn, w, st)) {
+  }
+  walk_finish(w, st);
+}
+
 // K5: persistent path tracer.  Each lane owns one path at a time and pulls
 // the next (pixel, sample) from a global counter as soon as its path ends,
 // so lanes stay busy despite Russian-roulette path-length variance (a plain
 // one-thread-per-sample megakernel idles ~80% of each warp).
+// Training paths traced by the same persistent kernel (render + collect of
+// one frame in one launch): work items [0, n) are walk_record paths, taken
+// first so their long Russian-roulette tails overlap the camera paths.
+struct WalkJob {
+  Stage st;
+  uint64_t seed, frame;
+  int64_t n;  // 0: render only
+};
+
 __global__ void __launch_bounds__(128, 3) k_trace(nirc_scene_t scn, const double* __restrict__ cam,
-                                                  nirc_render_cfg_t cfg, TraceOut out) {
+                                                  nirc_render_cfg_t cfg, TraceOut out,
+                                                  WalkJob job) {
   __shared__ __align__(16) unsigned char scene_sm[pt::kSceneSmemBytes];
   pt::stage_scene(scn, scene_sm);
   const int64_t nsamp = (int64_t)(cfg.row1 - cfg.row0) * cfg.width * cfg.spp;
+  const int64_t nwork = job.n + nsamp;
   PathState p;
-  bool active = false;
-  int64_t sid = fetch_sample(out.counters + 2, true);
-  if (sid < nsamp) {
-    start_path(p, cam, cfg, sid);
+  WalkLane wl;
+  bool active = false, walking = false;
+  auto start = [&](int64_t item) {
+    if (item < job.n) {
+      walk_start(wl, cam, job.seed, job.frame, job.st, item);
+      walking = true;
+    } else {
+      start_path(p, cam, cfg, item - job.n);
+      walking = false;
+    }
     active = true;
-  }
+  };
+  int64_t item = fetch_sample(out.counters + 2, true);
+  if (item < nwork) start(item);
   while (__any_sync(0xffffffffu, active)) {
+    CacheVertex rec;
+    int pending = 0;
+    bool done = false;
     if (active) {
-      CacheVertex rec;
-      int pending;
-      const bool done = trace_vertex(scn, cfg, p, rec, pending);
-      // warp-aggregated append of the cache-vertex records and query counts
-      const unsigned pm = __ballot_sync(__activemask(), pending);
-      if (pending) {
-        const int lane = threadIdx.x & 31;
-        const int leader = __ffs(pm) - 1;
-        unsigned long long base = 0;
-        const unsigned q = __reduce_add_sync(pm, (unsigned)(rec.ncq + rec.has_res));
-        if (lane == leader) {
-          base = atomicAdd(out.counters, (unsigned long long)__popc(pm));
-          atomicAdd(out.counters + 1, (unsigned long long)q);
-        }
-        base = __shfl_sync(pm, base, leader);
-        out.cv[base + __popc(pm & ((1u << lane) - 1u))] = rec;
+      if (walking) {
+        done = walk_vertex(scn, wl, job.st);
+        if (done) walk_finish(wl, job.st);
+      } else {
+        done = trace_vertex(scn, cfg, p, rec, pending);
       }
-      if (done) {
+    }
+    // warp-aggregated append of the cache-vertex records and query counts
+    const unsigned pm = __ballot_sync(0xffffffffu, pending);
+    if (pending) {
+      const int lane = threadIdx.x & 31;
+      const int leader = __ffs(pm) - 1;
+      unsigned long long base = 0;
+      const unsigned q = __reduce_add_sync(pm, (unsigned)(rec.ncq + rec.has_res));
+      if (lane == leader) {
+        base = atomicAdd(out.counters, (unsigned long long)__popc(pm));
+        atomicAdd(out.counters + 1, (unsigned long long)q);
+      }
+      base = __shfl_sync(pm, base, leader);
+      out.cv[base + __popc(pm & ((1u << lane) - 1u))] = rec;
+    }
+    if (active && done) {
+      if (!walking) {
         out.acc[3 * p.sid] = p.ar;
         out.acc[3 * p.sid + 1] = p.ag;
         out.acc[3 * p.sid + 2] = p.ab;
         out.term[p.sid] = p.term;
-        active = false;
       }
+      active = false;
     }
     const int64_t nxt = fetch_sample(out.counters + 2, !active);
-    if (!active && nxt < nsamp) {
-      start_path(p, cam, cfg, nxt);
-      active = true;
-    }
+    if (!active && nxt < nwork) start(nxt);
   }
 }
 
@@ -677,154 +880,6 @@ __global__ void k_accumulate(nirc_render_cfg_t cfg, const double* __restrict__ a
   tsum[pix] = ts;
 }
 
-// ---------------------------------------------------------------------
-// Training records: walk_record (kernels.py:85-286) driven by
-// collect_paths_kernel (:289-311).  Pass 1 walks every path, keeps its
-// per-vertex rows in a vertex-major staging area and runs the backward
-// sweep; a single-CTA scan turns per-path record counts into offsets; pass 3
-// compacts the records in (path, vertex) order -- the reference's row order.
-struct Stage {
-  // vertex-major: field[v * count + p]
-  double *pos, *ns, *alb, *rough, *wi, *pdf, *tgt, *tfull;
-  uint8_t* keep;
-  int32_t* nrec;   // per path
-  int32_t* nvert;  // per path
-  int64_t count;
-  int64_t path0;   // global index of local path 0 (multi-GPU path shards)
-};
-
-__global__ void k_walk_record(nirc_scene_t scn, const double* __restrict__ cam, uint64_t seed,
-                              uint64_t frame, Stage st) {
-  __shared__ __align__(16) unsigned char scene_sm[pt::kSceneSmemBytes];
-  pt::stage_scene(scn, scene_sm);
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= st.count) return;
-  const int64_t C = st.count;
-  const uint64_t key = stream_key(seed, P_TRAIN, frame, (uint64_t)(st.path0 + p), 0);
-  const double w = cam[14], h = cam[15];
-  const double sx = rand_uniform(key, DIM_JITTER_X) * w;
-  const double sy = rand_uniform(key, DIM_JITTER_Y) * h;
-  const int ix = (int)sx, iy = (int)sy;
-  V3 o, d;
-  pt::camera_ray(cam, ix, iy, sx - ix, sy - iy, o, d);
-  // per-vertex backward-sweep inputs live in local memory
-  double mise[pt::MAXB][3], emit[pt::MAXB][3], nee[pt::MAXB][3], fcp[pt::MAXB][3];
-  int n = 0, esc = 0;
-  double env_m[3] = {0.0, 0.0, 0.0}, env_r[3] = {0.0, 0.0, 0.0};
-  double prev_pdf = -1.0;
-  V3 lns = {0.0, 0.0, 0.0};
-  for (int v = 0; v < pt::MAXB; ++v) {
-    const pt::Hit hh = pt::intersect<false>(scn, o, d, pt::T_FAR);
-    if (hh.kind < 0) {
-      if (scn.env_kind != pt::ENV_NONE) {
-        const V3 e = pt::env_eval(scn, d);
-        env_r[0] = e.x; env_r[1] = e.y; env_r[2] = e.z;
-        double wgt = 1.0;
-        if (prev_pdf >= 0.0) {
-          const double pn = pt::nee_pdf_for_env(scn, lns, d);
-          wgt = prev_pdf / (prev_pdf + pn);
-        }
-        env_m[0] = wgt * e.x; env_m[1] = wgt * e.y; env_m[2] = wgt * e.z;
-      }
-      esc = 1;
-      break;
-    }
-    const V3 wo = {-d.x, -d.y, -d.z};
-    const double flip = (hh.n.x * wo.x + hh.n.y * wo.y + hh.n.z * wo.z) >= 0.0 ? 1.0 : -1.0;
-    const V3 ns = {hh.n.x * flip, hh.n.y * flip, hh.n.z * flip};
-    const V3 em = pt::ld3(scn.mat_emit, hh.mid);
-    if (em.x > 0.0 || em.y > 0.0 || em.z > 0.0) {
-      double wgt = 1.0;
-      if (prev_pdf >= 0.0) {
-        const double pn = pt::nee_pdf_for_hit(scn, hh.kind, hh.prim, hh.t, d, hh.n);
-        wgt = prev_pdf / (prev_pdf + pn);
-      }
-      mise[v][0] = wgt * em.x; mise[v][1] = wgt * em.y; mise[v][2] = wgt * em.z;
-      emit[v][0] = em.x; emit[v][1] = em.y; emit[v][2] = em.z;
-    } else {
-      mise[v][0] = mise[v][1] = mise[v][2] = 0.0;
-      emit[v][0] = emit[v][1] = emit[v][2] = 0.0;
-    }
-    const int mkind = scn.mat_kind[hh.mid];
-    const int delta = mkind == pt::MAT_MIRROR ? 1 : 0;
-    const V3 alb = pt::ld3(scn.mat_albedo, hh.mid);
-    const double rough = scn.mat_rough[hh.mid];
-    const int64_t at = (int64_t)v * C + p;
-    st.pos[3 * at] = hh.p.x; st.pos[3 * at + 1] = hh.p.y; st.pos[3 * at + 2] = hh.p.z;
-    st.ns[3 * at] = ns.x; st.ns[3 * at + 1] = ns.y; st.ns[3 * at + 2] = ns.z;
-    st.alb[3 * at] = alb.x; st.alb[3 * at + 1] = alb.y; st.alb[3 * at + 2] = alb.z;
-    st.rough[at] = rough;
-    const int base = VERTEX_DIM_BASE + v * DIMS_PER_VERTEX;
-    V3 q = {0.0, 0.0, 0.0};
-    if (delta == 0)
-      q = pt::nee_contrib(scn, hh.p, ns, hh.n, mkind, alb, rough, wo,
-                          rand_uniform(key, base + OFF_LIGHT_PICK),
-                          rand_uniform(key, base + OFF_LIGHT_U),
-                          rand_uniform(key, base + OFF_LIGHT_U + 1), 0);
-    nee[v][0] = q.x; nee[v][1] = q.y; nee[v][2] = q.z;
-    int alive = 1;
-    double rr_div = 1.0;
-    if (v >= pt::RR_START) {
-      if (rand_uniform(key, base + OFF_RR) >= pt::RR_SURVIVE) alive = 0;
-      else rr_div = pt::RR_SURVIVE;
-    }
-    int cont = 0;
-    double vpdf = 0.0;
-    V3 vwi = {0.0, 0.0, 0.0};
-    fcp[v][0] = fcp[v][1] = fcp[v][2] = 0.0;
-    if (alive == 1 && v < pt::MAXB - 1) {
-      const pt::BsdfSample b = pt::bsdf_sample(mkind, alb, rough, ns, wo,
-                                               rand_uniform(key, base + OFF_BSDF_U),
-                                               rand_uniform(key, base + OFF_BSDF_U + 1));
-      if (b.pdf > 0.0) {
-        const double ci = b.wi.x * ns.x + b.wi.y * ns.y + b.wi.z * ns.z;
-        if (ci > 0.0) {
-          const double inv = 1.0 / (b.pdf * rr_div);
-          vwi = b.wi;
-          vpdf = b.delta == 1 ? -1.0 : b.pdf;
-          fcp[v][0] = b.f.x * ci * inv;
-          fcp[v][1] = b.f.y * ci * inv;
-          fcp[v][2] = b.f.z * ci * inv;
-          prev_pdf = vpdf;
-          const double sg = (hh.n.x * b.wi.x + hh.n.y * b.wi.y + hh.n.z * b.wi.z) > 0.0 ? 1.0 : -1.0;
-          o = {hh.p.x + sg * scn.eps * hh.n.x, hh.p.y + sg * scn.eps * hh.n.y,
-               hh.p.z + sg * scn.eps * hh.n.z};
-          d = b.wi;
-          lns = ns;
-          cont = 1;
-        }
-      }
-    }
-    st.wi[3 * at] = vwi.x; st.wi[3 * at + 1] = vwi.y; st.wi[3 * at + 2] = vwi.z;
-    st.pdf[at] = vpdf;
-    st.keep[at] = (delta == 0 && vpdf > 0.0) ? 1 : 0;
-    n = v + 1;
-    if (cont == 0) break;
-  }
-  // backward sweep (kernels.py:249-277)
-  double lr = 0.0, lg = 0.0, lb = 0.0;
-  int nrec = 0;
-  for (int v = n - 1; v >= 0; --v) {
-    double cr, cg, cb, qr, qg, qb;
-    if (v == n - 1) {
-      cr = esc ? env_m[0] : 0.0; cg = esc ? env_m[1] : 0.0; cb = esc ? env_m[2] : 0.0;
-      qr = esc ? env_r[0] : 0.0; qg = esc ? env_r[1] : 0.0; qb = esc ? env_r[2] : 0.0;
-    } else {
-      cr = mise[v + 1][0] + lr; cg = mise[v + 1][1] + lg; cb = mise[v + 1][2] + lb;
-      qr = emit[v + 1][0] + lr; qg = emit[v + 1][1] + lg; qb = emit[v + 1][2] + lb;
-    }
-    const int64_t at = (int64_t)v * C + p;
-    st.tgt[3 * at] = cr; st.tgt[3 * at + 1] = cg; st.tgt[3 * at + 2] = cb;
-    st.tfull[3 * at] = qr; st.tfull[3 * at + 1] = qg; st.tfull[3 * at + 2] = qb;
-    lr = nee[v][0] + fcp[v][0] * cr;
-    lg = nee[v][1] + fcp[v][1] * cg;
-    lb = nee[v][2] + fcp[v][2] * cb;
-    nrec += st.keep[at];
-  }
-  st.nrec[p] = nrec;
-  st.nvert[p] = n;
-}
-
 // Exclusive scan of per-path record counts (one CTA; count is ~5e4).
 __global__ void k_scan_counts(const int32_t* __restrict__ cnt, int64_t n, int64_t* __restrict__ off,
                               int64_t* __restrict__ total) {
@@ -853,27 +908,36 @@ __global__ void k_scan_counts(const int32_t* __restrict__ cnt, int64_t n, int64_
   }
 }
 
+// One warp per path: lanes take the path's vertices (<= 64, two rounds),
+// ballot the kept ones and write them in vertex order at off[p] + rank --
+// the reference's (path, vertex) row order with coalesced stores.
 __global__ void k_compact_records(Stage st, const int64_t* __restrict__ off, int kind,
                                   nirc_records_out_t out) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (p >= st.count) return;
   int64_t o = off[p];
   const int n = st.nvert[p];
-  for (int v = 0; v < n; ++v) {
+  for (int v0 = 0; v0 < n; v0 += 32) {
+    const int v = v0 + lane;
     const int64_t at = (int64_t)v * st.count + p;
-    if (!st.keep[at]) continue;
-    if (o < out.cap) {
-      for (int c = 0; c < 3; ++c) {
-        out.pos[3 * o + c] = st.pos[3 * at + c];
-        out.ns[3 * o + c] = st.ns[3 * at + c];
-        out.alb[3 * o + c] = st.alb[3 * at + c];
-        out.dirs[3 * o + c] = st.wi[3 * at + c];
-        out.target[3 * o + c] = kind == 1 ? st.tfull[3 * at + c] : st.tgt[3 * at + c];
+    const bool keep = v < n && st.keep[at];
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const int64_t q = o + __popc(m & ((1u << lane) - 1u));
+      if (q < out.cap) {
+        for (int c = 0; c < 3; ++c) {
+          out.pos[3 * q + c] = st.pos[3 * at + c];
+          out.ns[3 * q + c] = st.ns[3 * at + c];
+          out.alb[3 * q + c] = st.alb[3 * at + c];
+          out.dirs[3 * q + c] = st.wi[3 * at + c];
+          out.target[3 * q + c] = kind == 1 ? st.tfull[3 * at + c] : st.tgt[3 * at + c];
+        }
+        out.rough[q] = st.rough[at];
+        out.pdf[q] = st.pdf[at];
       }
-      out.rough[o] = st.rough[at];
-      out.pdf[o] = st.pdf[at];
     }
-    ++o;
+    o += __popc(m);
   }
 }
 
@@ -926,17 +990,40 @@ RenderWs carve_render(const nirc_render_cfg_t& c, void* base) {
 }
 }  // namespace
 
+namespace {
+Stage carve_stage(int64_t count, void* base, size_t* bytes) {
+  Stage st{};
+  char* p = reinterpret_cast<char*>(base);
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    char* r = p ? p + off : nullptr;
+    off += aup(b);
+    return r;
+  };
+  const int64_t V = (int64_t)pt::MAXB * count;
+  st.pos = (double*)take(V * 24);
+  st.ns = (double*)take(V * 24);
+  st.alb = (double*)take(V * 24);
+  st.rough = (double*)take(V * 8);
+  st.wi = (double*)take(V * 24);
+  st.pdf = (double*)take(V * 8);
+  st.tgt = (double*)take(V * 24);
+  st.tfull = (double*)take(V * 24);
+  st.keep = (uint8_t*)take(V);
+  st.nrec = (int32_t*)take(count * 4);
+  st.nvert = (int32_t*)take(count * 4);
+  take(count * 8);  // offsets
+  st.count = count;
+  *bytes = off;
+  return st;
+}
+}  // namespace
+
 extern "C" int64_t nirc_render_workspace_bytes(const nirc_render_cfg_t* cfg) {
   return (int64_t)carve_render(*cfg, nullptr).bytes;
 }
 
-extern "C" int nirc_render(const nirc_scene_t* scene, const double* cam,
-                           const nirc_render_cfg_t* cfg, const nirc_spec_t* spec,
-                           const float* theta, double* img, double* img2, double* term,
-                           int64_t* queries_out, void* workspace, int64_t workspace_bytes,
-                           void* stream) {
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const nirc_render_cfg_t& c = *cfg;
+static int check_render_cfg(const nirc_render_cfg_t& c) {
   if (c.mode != 0 && c.mode != 1) {
     set_last_error("nirc_render supports the pt and two-level modes");
     return NIRC_E_UNSUPPORTED;
@@ -950,11 +1037,15 @@ extern "C" int nirc_render(const nirc_scene_t* scene, const double* cam,
       set_last_error("nc entry outside 0..28");
       return NIRC_E_CONFIG;
     }
-  RenderWs w = carve_render(c, workspace);
-  if ((int64_t)w.bytes > workspace_bytes) {
-    set_last_error("render workspace too small");
-    return NIRC_E_CONFIG;
-  }
+  return NIRC_OK;
+}
+
+// The frame pipeline: K5 trace (+ the training walks of `job`), fused
+// inference/combine, accumulation.
+static int render_impl(const nirc_scene_t* scene, const double* cam, const nirc_render_cfg_t& c,
+                       const nirc_spec_t* spec, const float* theta, double* img, double* img2,
+                       double* term, int64_t* queries_out, const RenderWs& w, const WalkJob& job,
+                       cudaStream_t s) {
   const bool tl = c.mode == 1 && c.cache_on;
   const int64_t ns = (int64_t)(c.row1 - c.row0) * c.width * c.spp;
   NIRC_CUDA_TRY(cudaMemsetAsync(w.counters, 0, 64, s));
@@ -966,10 +1057,10 @@ extern "C" int nirc_render(const nirc_scene_t* scene, const double* cam,
                                                                 128, 0));
     if (trace_blocks_per_sm < 1) trace_blocks_per_sm = 1;
   }
-  const int64_t tgrid_max = (ns + 127) / 128;
+  const int64_t tgrid_max = (ns + job.n + 127) / 128;
   const int64_t tgrid_pers = (int64_t)sm_count() * trace_blocks_per_sm;
   k_trace<<<(int)(tgrid_max < tgrid_pers ? tgrid_max : tgrid_pers), 128, 0, s>>>(*scene, cam, c,
-                                                                                  to);
+                                                                                  to, job);
   NIRC_LAUNCH_CHECK("k_trace");
   if (tl) {
     if (!spec || !theta) return NIRC_E_CONFIG;
@@ -1033,34 +1124,67 @@ extern "C" int nirc_render(const nirc_scene_t* scene, const double* cam,
   return NIRC_OK;
 }
 
-namespace {
-Stage carve_stage(int64_t count, void* base, size_t* bytes) {
-  Stage st{};
-  char* p = reinterpret_cast<char*>(base);
-  size_t off = 0;
-  auto take = [&](size_t b) {
-    char* r = p ? p + off : nullptr;
-    off += aup(b);
-    return r;
-  };
-  const int64_t V = (int64_t)pt::MAXB * count;
-  st.pos = (double*)take(V * 24);
-  st.ns = (double*)take(V * 24);
-  st.alb = (double*)take(V * 24);
-  st.rough = (double*)take(V * 8);
-  st.wi = (double*)take(V * 24);
-  st.pdf = (double*)take(V * 8);
-  st.tgt = (double*)take(V * 24);
-  st.tfull = (double*)take(V * 24);
-  st.keep = (uint8_t*)take(V);
-  st.nrec = (int32_t*)take(count * 4);
-  st.nvert = (int32_t*)take(count * 4);
-  take(count * 8);  // offsets
-  st.count = count;
-  *bytes = off;
-  return st;
+extern "C" int nirc_render(const nirc_scene_t* scene, const double* cam,
+                           const nirc_render_cfg_t* cfg, const nirc_spec_t* spec,
+                           const float* theta, double* img, double* img2, double* term,
+                           int64_t* queries_out, void* workspace, int64_t workspace_bytes,
+                           void* stream) {
+  int st = check_render_cfg(*cfg);
+  if (st) return st;
+  RenderWs w = carve_render(*cfg, workspace);
+  if ((int64_t)w.bytes > workspace_bytes) {
+    set_last_error("render workspace too small");
+    return NIRC_E_CONFIG;
+  }
+  WalkJob job{};
+  return render_impl(scene, cam, *cfg, spec, theta, img, img2, term, queries_out, w, job,
+                     reinterpret_cast<cudaStream_t>(stream));
 }
-}  // namespace
+
+extern "C" int64_t nirc_render_collect_workspace_bytes(const nirc_render_cfg_t* cfg,
+                                                       int64_t count) {
+  size_t b = 0;
+  carve_stage(count, nullptr, &b);
+  return (int64_t)(aup(carve_render(*cfg, nullptr).bytes) + b);
+}
+
+extern "C" int nirc_render_collect(const nirc_scene_t* scene, const double* cam,
+                                   const nirc_render_cfg_t* cfg, const nirc_spec_t* spec,
+                                   const float* theta, double* img, double* img2, double* term,
+                                   int64_t* queries_out, uint64_t train_seed,
+                                   uint64_t train_frame, int64_t path0, int64_t count,
+                                   int32_t kind, const nirc_records_out_t* out, int64_t* n_out,
+                                   void* workspace, int64_t workspace_bytes, void* stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int st = check_render_cfg(*cfg);
+  if (st) return st;
+  if (count <= 0 || path0 < 0) {
+    set_last_error("count must be positive and path0 non-negative");
+    return NIRC_E_CONFIG;
+  }
+  if (kind != 0 && kind != 1) {
+    set_last_error("record kind %d unsupported on the device (nirc=0, nirc_full=1)", kind);
+    return NIRC_E_UNSUPPORTED;
+  }
+  RenderWs w = carve_render(*cfg, workspace);
+  size_t sb = 0;
+  Stage stg = carve_stage(count, reinterpret_cast<char*>(workspace) + aup(w.bytes), &sb);
+  if ((int64_t)(aup(w.bytes) + sb) > workspace_bytes) {
+    set_last_error("render+collect workspace too small");
+    return NIRC_E_CONFIG;
+  }
+  stg.path0 = path0;
+  WalkJob job{stg, train_seed, train_frame, count};
+  if ((st = render_impl(scene, cam, *cfg, spec, theta, img, img2, term, queries_out, w, job, s)))
+    return st;
+  int64_t* off = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(stg.nvert) + aup(count * 4));
+  k_scan_counts<<<1, 1024, 0, s>>>(stg.nrec, count, off, n_out);
+  NIRC_LAUNCH_CHECK("k_scan_counts");
+  k_compact_records<<<(int)((count * 32 + 255) / 256), 256, 0, s>>>(stg, off, kind, *out);
+  NIRC_LAUNCH_CHECK("k_compact_records");
+  return NIRC_OK;
+}
+
 
 extern "C" int64_t nirc_collect_workspace_bytes(int64_t count) {
   size_t b = 0;
@@ -1093,7 +1217,7 @@ extern "C" int nirc_collect_range(const nirc_scene_t* scene, const double* cam, 
   NIRC_LAUNCH_CHECK("k_walk_record");
   k_scan_counts<<<1, 1024, 0, s>>>(st.nrec, count, off, n_out);
   NIRC_LAUNCH_CHECK("k_scan_counts");
-  k_compact_records<<<(int)((count + 127) / 128), 128, 0, s>>>(st, off, kind, *out);
+  k_compact_records<<<(int)((count * 32 + 255) / 256), 256, 0, s>>>(st, off, kind, *out);
   NIRC_LAUNCH_CHECK("k_compact_records");
   return NIRC_OK;
 }

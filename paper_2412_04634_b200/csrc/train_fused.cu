@@ -6,7 +6,7 @@
 //   backward (mlp.py:125-154, ReLU' = z >= 0) -> hash-grid scatter
 //   (encoding.py:160-167) straight from registers,
 // keeping every activation in shared memory.  Weight/bias gradients are
-// written as per-CTA partials and summed in CTA order by k_reduce_grad
+// written as per-CTA partials and summed in a fixed order by k_reduce_grad
 // (deterministic), which also folds the loss, flags a non-finite loss
 // (DivergenceError) or gradient (Adam skip) and feeds the dense Adam kernels.
 //
@@ -392,13 +392,28 @@ __global__ void k_reduce_grad(nirc_spec_t sp, const float* __restrict__ partials
                               int32_t* __restrict__ flags, int32_t* __restrict__ adam_bad,
                               int mode) {
   if (mode == 0 && (flags[0] & 3)) return;
+  // block = 8 warps x 32 consecutive parameters; warp w sums a contiguous
+  // chunk of tiles, the 8 chunk sums are added in warp order (deterministic)
+  __shared__ float part[8][33];
   const int np = (int)(sp.theta_len - sp.grid_len);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int per = (ntiles + 7) / 8;
+  const int t0 = wid * per, t1 = min(ntiles, t0 + per);
   int bad = 0;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x) {
+  for (int pb = blockIdx.x * 32; pb < np; pb += gridDim.x * 32) {
+    const int p = pb + lane;
     float s = 0.0f;
-    for (int t = 0; t < ntiles; ++t) s += partials[(int64_t)t * np + p];
-    grad[sp.grid_len + p] = s;
-    bad |= !isfinite(s);
+    if (p < np)
+      for (int t = t0; t < t1; ++t) s += partials[(int64_t)t * np + p];
+    part[wid][lane] = s;
+    __syncthreads();
+    if (wid == 0 && p < np) {
+      float tot = part[0][lane];
+      for (int w = 1; w < 8; ++w) tot += part[w][lane];
+      grad[sp.grid_len + p] = tot;
+      bad |= !isfinite(tot);
+    }
+    __syncthreads();
   }
   if (mode == 1) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -445,8 +460,9 @@ int launch_fused_train(const nirc_spec_t& sp, const float* theta, const nirc_rec
                                          partials, loss_part, flags, tile0);
     NIRC_LAUNCH_CHECK("k_train_tile");
   }
-  k_reduce_grad<<<64, 256, 0, s>>>(sp, partials, ntiles, loss_part, B, grad, loss_out, flags,
-                                   adam_bad, mode);
+  const int np = (int)(sp.theta_len - sp.grid_len);
+  k_reduce_grad<<<(np + 31) / 32, 256, 0, s>>>(sp, partials, ntiles, loss_part, B, grad, loss_out,
+                                               flags, adam_bad, mode);
   NIRC_LAUNCH_CHECK("k_reduce_grad");
   return NIRC_OK;
 }

@@ -293,19 +293,27 @@ def gather_image(t, rows, comm):
 def run_frame_sharded(scene, cache, config, comm, seed, frame, spp=1, steps=4, batch=None,
                       train_fraction=0.025, out=None, ops=None):
     """One frame of the online two-level renderer on `comm.world` GPUs:
-    render this rank's band with θ_f, collect the path shard, all-gather the
-    records and train with all-reduced gradients (θ_{f+1} on every rank).
+    render this rank's row band with θ_f and walk its training-path shard in
+    the same trace launch (nirc_render_collect), all-gather the records and
+    train with all-reduced gradients (θ_{f+1} on every rank).
     Returns ((img, img2, term) band sums, rows, stats dict)."""
     from .caches import default_train_count
+    from .estimators import render_and_collect
 
-    img, img2, term, q, rows = render_band(scene, config, cache, comm, seed, spp, frame, out)
-    stats = {"rows": rows, "queries": q}
-    if cache is not None:
-        rec = collect_sharded(cache, comm, default_train_count(scene, train_fraction), frame,
-                              ops)
-        stats["records"] = len(rec)
-        if len(rec):
-            stats["trace"] = train_frame_sharded(cache, rec, comm, steps, batch, ops)
+    if cache is None:
+        img, img2, term, q, rows = render_band(scene, config, cache, comm, seed, spp, frame, out)
+        return (img, img2, term), rows, {"rows": rows, "queries": q}
+    h = int(scene.camera[15])
+    rows = split_range(h, comm.world, comm.rank)
+    count = default_train_count(scene, train_fraction)
+    paths = split_range(count, comm.world, comm.rank)
+    img, img2, term, q, local = render_and_collect(scene, config, cache, seed, spp, frame,
+                                                   count=count, rows=rows, paths=paths, out=out)
+    packed = pack_records({k: getattr(local, k) for k, _ in REC_COLS})
+    rec = unpack_records(comm.all_gather_rows(packed), cache.record_kind, frame)
+    stats = {"rows": rows, "queries": q, "records": len(rec)}
+    if len(rec):
+        stats["trace"] = train_frame_sharded(cache, rec, comm, steps, batch, ops)
     return (img, img2, term), rows, stats
 
 

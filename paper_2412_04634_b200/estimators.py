@@ -146,6 +146,56 @@ def render_device(scene, config=None, cache=None, seed=0, spp=1, frame=0, force_
     return img, img2, term, queries
 
 
+def render_and_collect(scene, config, cache, seed=0, spp=1, frame=0, count=None,
+                       train_frame=None, rows=None, paths=None, out=None, precision=None):
+    """render_device + cache.collect of the same frame in ONE device pass
+    (C ABI nirc_render_collect: the training walks are the first work items
+    of the persistent path tracer).  Equivalent to calling render_device and
+    then collect_training_records(scene, cache.seed, count, cache.record_kind,
+    train_frame).  ``paths`` = (p0, p1) collects a path shard (multi-GPU).
+    Returns (img, img2, term, queries, records_packed_or_Records)."""
+    from .caches import Records, default_train_count
+    from .records import _KIND, _check_kind, record_buffers
+
+    if config is None:
+        config = EstimatorConfig()
+    mode = MODES[config.mode]
+    if mode > 1:
+        raise NotImplementedError(f"mode '{config.mode}' is outside the two-level hot path")
+    _check_kind(scene, cache.record_kind)
+    if count is None:
+        count = default_train_count(scene)
+    if train_frame is None:
+        train_frame = frame
+    p0, p1 = (0, int(count)) if paths is None else (int(paths[0]), int(paths[1]))
+    w, h = int(scene.camera[14]), int(scene.camera[15])
+    cache_on = 1 if (mode == 1 and not cache.is_zero) else 0
+    cfg = _c_cfg(config, scene, spp, seed, frame, cache_on, rows, precision)
+    lib = _lib.load()
+    ds = scene.device()
+    if out is None:
+        img = _dev.zeros((h, w, 3), torch.float64)
+        img2 = _dev.zeros((h, w, 3), torch.float64)
+        term = _dev.zeros((h, w), torch.float64)
+    else:
+        img, img2, term = out
+    queries = _dev.zeros((1,), torch.int64)
+    n_out = _dev.zeros((1,), torch.int64)
+    rec_out, ro = record_buffers(max(p1 - p0, 1))
+    ws = _RenderWs.get(lib.nirc_render_collect_workspace_bytes(C.byref(cfg), max(p1 - p0, 1)))
+    cs = _lib.make_c_spec(cache.spec)
+    _lib.check(lib.nirc_render_collect(
+        ds.ptr(), _dev.ptr(ds.cam), C.byref(cfg), C.byref(cs) if cache_on else None,
+        _dev.ptr(cache.theta) if cache_on else None, _dev.ptr(img), _dev.ptr(img2),
+        _dev.ptr(term), _dev.ptr(queries), int(cache.seed), int(train_frame), p0,
+        max(p1 - p0, 1), _KIND[cache.record_kind], C.byref(ro), _dev.ptr(n_out), _dev.ptr(ws),
+        int(ws.numel()), _dev.stream()), "nirc_render_collect")
+    n = int(n_out.item()) if p1 > p0 else 0
+    rec = Records(kind=cache.record_kind, frame=train_frame, n=n,
+                  **{k: v[:n] for k, v in rec_out.items()})
+    return img, img2, term, queries, rec
+
+
 def render(scene, config=None, cache=None, seed=0, spp=1, frame=0, v1_map=None,
            force_cache=False, precision=None):
     """Render with the configured estimator (estimators.py:173-217)."""

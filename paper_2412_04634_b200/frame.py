@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import torch
 
 from .caches import default_train_count, train_frame
-from .estimators import EstimatorConfig, render_device
+from .estimators import EstimatorConfig, render_and_collect, render_device
 
 
 @dataclass
@@ -28,11 +28,15 @@ def run_frame(scene, cache, config, seed, frame, spp=1, train_fraction=0.025, st
               batch=None, out=None):
     """Render frame `frame` and train the cache on it; returns
     ((img, img2, term) device sums, FrameStats)."""
-    img, img2, term, queries = render_device(scene, config, cache, seed, spp, frame, out=out)
     loss = math.nan
     nrec = 0
-    if cache is not None:
-        rec = cache.collect(count=default_train_count(scene, train_fraction), frame=frame)
+    if cache is None:
+        img, img2, term, queries = render_device(scene, config, cache, seed, spp, frame, out=out)
+    else:
+        # render + training walks in one persistent trace launch
+        img, img2, term, queries, rec = render_and_collect(
+            scene, config, cache, seed, spp, frame,
+            count=default_train_count(scene, train_fraction), out=out)
         nrec = len(rec)
         if nrec:
             trace = train_frame(cache, rec, steps=steps, batch=batch)

@@ -28,15 +28,18 @@ class _CollectWs:
         return cls.buf
 
 
-def collect_training_records(scene, seed, count, kind="nirc", frame=0):
+def _check_kind(scene, kind):
     if kind not in RECORD_KINDS:
         raise ConfigError(f"unknown record kind '{kind}'")
     if kind in ("nvc", "nirc_env") and scene.pack.env_kind == 0:
         raise ConfigError(f"record kind '{kind}' needs an environment light")
     if kind not in _KIND:
         raise NotImplementedError(f"record kind '{kind}' is outside the NIRC hot path")
-    count = int(count)
-    cap = count * 63
+
+
+def record_buffers(count):
+    """Output columns for `count` training paths (<= 63 records each)."""
+    cap = int(count) * 63
     out = {k: _dev.empty((cap, 3), torch.float64) for k in ("pos", "ns", "alb", "dirs", "target")}
     out["rough"] = _dev.empty((cap,), torch.float64)
     out["pdf"] = _dev.empty((cap,), torch.float64)
@@ -44,6 +47,13 @@ def collect_training_records(scene, seed, count, kind="nirc", frame=0):
     for k, t in out.items():
         setattr(ro, k, t.data_ptr())
     ro.cap = cap
+    return out, ro
+
+
+def collect_training_records(scene, seed, count, kind="nirc", frame=0):
+    _check_kind(scene, kind)
+    count = int(count)
+    out, ro = record_buffers(count)
     n_out = _dev.zeros((1,), torch.int64)
     lib = _lib.load()
     ws = _CollectWs.get(lib.nirc_collect_workspace_bytes(count))
