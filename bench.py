@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--n", type=int, default=N_QUERIES)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-frame", action="store_true")
+    ap.add_argument("--no-extra-frames", action="store_true")
     ap.add_argument("--frame-steps", type=int, default=10)
     return ap.parse_args()
 
@@ -178,7 +179,7 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------- frame leg -------
-def frame_bench(frames, warmup, width=1920, height=1080, nc=(16,), comm=None):
+def frame_bench(frames, warmup, width=1920, height=1080, nc=(16,), comm=None, name="cfg3"):
     """BASELINE config 3: Cornell at 1920x1080, two-level with nc=(16,) at
     the first cache vertex, spp 1, D = 4 cache; then collect ceil(0.025 W H)
     training paths and 4 Adam steps of 16384 records.  Device time per
@@ -249,7 +250,7 @@ def frame_bench(frames, warmup, width=1920, height=1080, nc=(16,), comm=None):
         same = True
     med = {k: sorted(v)[len(v) // 2] for k, v in phases.items()}
     return {
-        "metric": "ms_per_frame_1080p", "value": med["frame"], "unit": "ms/frame",
+        "metric": f"ms_per_frame_{width}x{height}", "value": med["frame"], "unit": "ms/frame",
         "higher_is_better": False, "frames": frames, "warmup": warmup, "n_gpus": world,
         "render_collect_ms": med["render"], "record_allgather_ms": med["collect"],
         "train_ms": med["train"],
@@ -261,8 +262,8 @@ def frame_bench(frames, warmup, width=1920, height=1080, nc=(16,), comm=None):
                   "training walks as its first work items, fused inference, accumulation, "
                   "record compaction); record_allgather = multi-GPU record exchange",
         "replicas_identical": same,
-        "config": "cfg3: cornell 1920x1080, two-level nc=(16,), spp 1, D=4 cache, "
-                  "collect 51,840 paths, 4 x 16384 train steps"
+        "config": f"{name}: cornell {width}x{height}, two-level nc={tuple(nc)}, spp 1, D=4 "
+                  f"cache, collect {count:,} paths, 4 x min(16384, records) train steps"
                   + (f"; sharded over {world} GPUs (row bands, path shards, "
                      "NCCL gradient all-reduce)" if world > 1 else ""),
         "reference_cpu_context": "SURVEY.md 6: 122.6 s/frame on 1 core (not re-timed here)",
@@ -357,7 +358,19 @@ def run_b200(args, rank, world, local_rank):
     if not args.no_frame:
         from paper_2412_04634_b200 import distributed as D
 
-        fb = frame_bench(args.frame_steps, 3, comm=D.Comm() if world > 1 else None)
+        comm = D.Comm() if world > 1 else None
+        fb = frame_bench(args.frame_steps, 3, comm=comm)
+        if not args.no_extra_frames:
+            # BASELINE cfg5 (4K, 32 NIRC samples/pixel as nc=(16,16): the
+            # reference caps N_c at 28 per vertex) and cfg1 (the reference's
+            # CPU-runnable 128^2 frame), both sharded like cfg3 when N > 1
+            fb["cfg5_4k"] = frame_bench(max(3, args.frame_steps // 2), 2, 3840, 2160, (16, 16),
+                                        comm=comm, name="cfg5")
+            fb["cfg1_128"] = frame_bench(args.frame_steps, 3, 128, 128, (8,), comm=comm,
+                                         name="cfg1")
+            fb["cfg1_128"]["reference_cpu_context"] = (
+                "SURVEY.md 6: 1.28 s/frame for cfg1 on 1 core (render 1084 + collect 12 + "
+                "train 179 ms)")
     if rank != 0:
         return
     import json as _json

@@ -82,7 +82,9 @@ typedef struct nirc_scene {
  * (pkg/src/nirclab/estimators.py:49-84) as consumed by render_kernel
  * (pkg/src/nirclab/kernels.py:723-759). */
 typedef struct nirc_render_cfg {
-  int32_t mode;          /* 0 = pt, 1 = two-level */
+  int32_t mode;          /* 0 = pt, 1 = two-level, 2 = biased-nirc-bth,
+                            3 = biased-nirc-sph, 4 = biased-nrc-sph
+                            (kernels.py:37-41) */
   int32_t spp;
   int32_t cache_on;      /* 0: cache skipped (is_zero and not forced) */
   int32_t max_cv;
@@ -94,7 +96,10 @@ typedef struct nirc_render_cfg {
   int32_t row0, row1;    /* pixel-row band [row0, row1) rendered by this call */
   int32_t precision;     /* network arithmetic: 0 tcgen05 3xTF32, 1 fp32 SIMT,
                             2 tcgen05 2xFP16 split (default) */
-  int32_t pad;
+  int32_t nbias;         /* cache directions at a biased stop vertex (1..28) */
+  double sph_c;          /* spread threshold of the *_sph / bth stop tests */
+  const uint8_t* v1;     /* (height*width) per-pixel first-vertex stop flags of
+                            the *_sph modes, or NULL (all zero) */
 } nirc_render_cfg_t;
 
 /* ---- library / introspection ------------------------------------------ */

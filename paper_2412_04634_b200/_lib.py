@@ -93,7 +93,8 @@ class NircRenderCfg(C.Structure):
         ("seed", C.c_uint64), ("frame", C.c_uint64),
         ("width", C.c_int32), ("height", C.c_int32),
         ("row0", C.c_int32), ("row1", C.c_int32),
-        ("precision", C.c_int32), ("pad", C.c_int32),
+        ("precision", C.c_int32), ("nbias", C.c_int32),
+        ("sph_c", C.c_double), ("v1", C.c_void_p),
     ]
 
 

@@ -58,6 +58,10 @@ def _compile(src, verbose):
     cmd = [_nvcc(), *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
     if src in _NO_FMA:
         cmd.insert(1, "-fmad=false")
+    if os.environ.get("NIRC_TRACE_MINB"):  # tuning experiments only
+        cmd.insert(1, "-DNIRC_TRACE_MINB=" + os.environ["NIRC_TRACE_MINB"])
+    for d in os.environ.get("NIRC_NVCC_DEFS", "").split():  # tuning experiments only
+        cmd.insert(1, d)
     if verbose:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -109,6 +109,45 @@ NIRC_D void sh_eval(double x, double y, double z, int bands,
   }
 }
 
+// Real SH (bands = 4), the scalar-path recurrences of sh.py:36-76 in fp32.
+NIRC_D void sh4_f32(float x, float y, float z, const double* sh_k, float* out) {
+  const float s = sqrtf(x * x + y * y);
+  float cphi = 1.0f, sphi = 0.0f;
+  if (s > 0.0f) {
+    cphi = x / s;
+    sphi = y / s;
+  }
+  float cm = 1.0f, sm = 0.0f, pmm = 1.0f;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    if (m > 0) {
+      pmm = pmm * ((2.0f * m - 1.0f) * s);
+      const float cn = cm * cphi - sm * sphi;
+      const float sn = sm * cphi + cm * sphi;
+      cm = cn;
+      sm = sn;
+    }
+    float p2 = 0.0f, p1 = 0.0f;
+#pragma unroll
+    for (int l = m; l < 4; ++l) {
+      float p;
+      if (l == m) p = pmm;
+      else if (l == m + 1) p = z * (2.0f * m + 1.0f) * pmm;
+      else p = ((2.0f * l - 1.0f) * z * p1 - (l + m - 1.0f) * p2) / (float)(l - m);
+      p2 = p1;
+      p1 = p;
+      const int base = l * l + l;
+      if (m == 0) {
+        out[base] = (float)sh_k[l * 8] * p;
+      } else {
+        const float kk = (float)sh_k[l * 8 + m] * p;
+        out[base + m] = kk * cm;
+        out[base - m] = kk * sm;
+      }
+    }
+  }
+}
+
 // ----------------------------------------------------------- hash grid ---
 // encoding.py:38-42: (x*1 ^ y*P1 ^ z*P2) & (T-1).  The mask is < 2^32 so
 // the low 32 bits of the u64 products decide the slot; u32 math is exact.

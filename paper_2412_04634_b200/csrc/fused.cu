@@ -50,6 +50,11 @@ __global__ void k_pack_weights(nirc_spec_t sp, TcNet net, const float* __restric
 // The default NIRC input layout (test_default_layout_dimensions,
 // tests/test_neural.py:81-88): 12 levels x 2 feats, 4 SH bands, 7 aux.
 constexpr int kL = 12, kF = 2, kBands = 4, kIn = 47, kK0 = 48;
+#ifdef NIRC_FF_F64SH
+constexpr bool kFusedF32Sh = false;
+#else
+constexpr bool kFusedF32Sh = true;  // SH block in fp32 (<= 5e-7 abs) in the fused kernel
+#endif
 constexpr int kDenseLevels = 4;  // dense coarse levels of the cfg2 kernel (measured best)
 
 __host__ __device__ inline bool is_default_layout(const nirc_spec_t& sp) {
@@ -57,10 +62,13 @@ __host__ __device__ inline bool is_default_layout(const nirc_spec_t& sp) {
          sp.dims[0] == kIn;
 }
 
-// Encodes one query row into x[48] (x[47] = 0 pad), bit-identical to
-// encode_batch (encoding.py:111-157).  Levels < dl.n are gathered from the
-// CTA's dense shared-memory copies, the rest from the L2-resident tables.
-template <int ND>
+// Encodes one query row into x[48] (x[47] = 0 pad) as encode_batch
+// (encoding.py:111-157): hash + aux blocks bit-identical; the SH block
+// bit-identical with the f64 recurrences (F32SH = false) or within 5e-7 abs
+// in fp32 (F32SH = true, the fused inference kernel).  Levels < ND are
+// gathered from the CTA's dense shared-memory copies, the rest from the
+// L2-resident tables.
+template <int ND, bool F32SH>
 __device__ __forceinline__ void encode_default(const nirc_spec_t& sp,
                                                const float* __restrict__ theta, const double* p,
                                                const double* nrm, const double* alb,
@@ -80,8 +88,11 @@ __device__ __forceinline__ void encode_default(const nirc_spec_t& sp,
     x[2 * lvl] = f.x;
     x[2 * lvl + 1] = f.y;
   }
-  sh_eval<true>(d[0], d[1], d[2], kBands, sp.sh_k,
-                [&](int i, double v) { x[24 + i] = __double2float_rn(v); });
+  if (F32SH)
+    sh4_f32((float)d[0], (float)d[1], (float)d[2], sp.sh_k, x + 24);
+  else
+    sh_eval<true>(d[0], d[1], d[2], kBands, sp.sh_k,
+                  [&](int i, double v) { x[24 + i] = __double2float_rn(v); });
   x[40] = __double2float_rn(dmul(dadd(nrm[0], 1.0), 0.5));
   x[41] = __double2float_rn(dmul(dadd(nrm[1], 1.0), 0.5));
   x[42] = __double2float_rn(dmul(dadd(nrm[2], 1.0), 0.5));
@@ -124,8 +135,23 @@ __global__ void __launch_bounds__(NG * 128, 1)
     const int64_t row = tile * tc::kTileRows + tg;
     float x[kK0];
     if (row < n) {
-      encode_default<ND>(sp, theta, pos + 3 * row, nrm + 3 * row, alb + 3 * row, rough[row],
-                         dirs + 3 * row, x, dl, dense);
+#ifdef NIRC_FF_NOSTREAM
+      encode_default<ND, kFusedF32Sh>(sp, theta, pos + 3 * row, nrm + 3 * row, alb + 3 * row,
+                                      rough[row], dirs + 3 * row, x, dl, dense);
+#else
+      // the query rows are read once: streaming loads keep them from evicting
+      // hash-table lines out of L1
+      double pr[3], nr[3], ar[3], dr[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        pr[c] = __ldcs(pos + 3 * row + c);
+        nr[c] = __ldcs(nrm + 3 * row + c);
+        ar[c] = __ldcs(alb + 3 * row + c);
+        dr[c] = __ldcs(dirs + 3 * row + c);
+      }
+      encode_default<ND, kFusedF32Sh>(sp, theta, pr, nr, ar, __ldcs(rough + row), dr, x, dl,
+                                      dense);
+#endif
     } else {
 #pragma unroll
       for (int k = 0; k < kK0; ++k) x[k] = 0.0f;
@@ -161,7 +187,7 @@ __global__ void k_full_forward_simt(nirc_spec_t sp, const float* __restrict__ th
   if (row >= n) return;
   float a[64], b[64];
   DenseLevels none{};
-  encode_default<0>(sp, theta, pos + 3 * row, nrm + 3 * row, alb + 3 * row, rough[row],
+  encode_default<0, false>(sp, theta, pos + 3 * row, nrm + 3 * row, alb + 3 * row, rough[row],
                  dirs + 3 * row, a, none, nullptr);
   for (int l = 0; l < sp.n_layers; ++l) {
     const int din = sp.dims[l], dout = sp.dims[l + 1];

@@ -30,6 +30,7 @@ __device__ inline V3 ld3(const double* a, int i) { return {a[3 * i], a[3 * i + 1
 __device__ inline double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
 
 // ---------------------------------------------------------- geometry ----
+// ray_tri (geometry.py:19-44), Moller-Trumbore in f64.
 __device__ inline double ray_tri(V3 o, V3 d, V3 v0, V3 e1, V3 e2) {
   const double px = d.y * e2.z - d.z * e2.y;
   const double py = d.z * e2.x - d.x * e2.z;

@@ -41,6 +41,7 @@ struct CacheVertex {
   double wc[3];   // continuation direction w_cont
   uint64_t key;
   int32_t base, ncq, mkind, has_res;
+  int32_t nrc, pad;  // nrc: one query at wo, added with +T (biased-nrc-sph stop)
   int64_t slot;   // sample * max_cv + cu
 };
 
@@ -55,9 +56,10 @@ struct TraceOut {
 struct PathState {
   V3 o, d, lns;
   double ar, ag, ab, tr, tg, tb, prev_pdf;
+  double a0, a_sp;  // footprint spread state of the biased modes
   uint64_t key;
   int64_t sid;
-  int v, cu, term;
+  int v, cu, term, v1;
 };
 
 // Warp-aggregated fetch of the next sample index for the lanes in `want`.
@@ -90,6 +92,193 @@ __device__ inline void start_path(PathState& p, const double* cam, const nirc_re
   p.prev_pdf = -1.0;
   p.lns = {0.0, 0.0, 0.0};
   p.v = p.cu = p.term = 0;
+  p.a0 = 0.0;
+  p.a_sp = 1.0;
+  p.v1 = cfg.v1 ? cfg.v1[pix] : 0;
+}
+
+__device__ inline void fill_stop_vertex(CacheVertex& rec, const PathState& p, V3 pos, V3 ns,
+                                        V3 alb, double rough, V3 wo, int base, int mkind,
+                                        int ncq, int nrc, int max_cv) {
+  rec.pos[0] = pos.x; rec.pos[1] = pos.y; rec.pos[2] = pos.z;
+  rec.ns[0] = ns.x; rec.ns[1] = ns.y; rec.ns[2] = ns.z;
+  rec.alb[0] = alb.x; rec.alb[1] = alb.y; rec.alb[2] = alb.z;
+  rec.rough = rough;
+  rec.wo[0] = wo.x; rec.wo[1] = wo.y; rec.wo[2] = wo.z;
+  rec.T[0] = p.tr; rec.T[1] = p.tg; rec.T[2] = p.tb;
+  rec.key = p.key;
+  rec.base = base;
+  rec.ncq = ncq;
+  rec.mkind = mkind;
+  rec.has_res = 0;
+  rec.nrc = nrc;
+  rec.pad = 0;
+  rec.slot = p.sid * max_cv;
+  rec.Tp[0] = rec.Tp[1] = rec.Tp[2] = 0.0;
+  rec.wc[0] = rec.wc[1] = 0.0;
+  rec.wc[2] = 1.0;
+}
+
+// One vertex of trace_sample's biased family (kernels.py:609-720): the
+// spread / stochastic-brdf / first-vertex stop tests; the stop vertex is
+// shaded by NEE + the cache integral over nbias directions (NIRC modes) or
+// one NRC query at wo, deferred to the inference pass like the two-level
+// cache vertices.  Returns true when the path ended.
+__device__ inline bool trace_vertex_biased(const nirc_scene_t& scn, const nirc_render_cfg_t& cfg,
+                                           PathState& p, CacheVertex& rec, int& pending) {
+  pending = 0;
+  const int v = p.v;
+  const pt::Hit h = pt::intersect<false>(scn, p.o, p.d, pt::T_FAR);
+  if (h.kind < 0) {
+    if (scn.env_kind != pt::ENV_NONE) {
+      const V3 e = pt::env_eval(scn, p.d);
+      double w = 1.0;
+      if (p.prev_pdf >= 0.0) {
+        const double pn = pt::nee_pdf_for_env(scn, p.lns, p.d);
+        w = p.prev_pdf / (p.prev_pdf + pn);
+      }
+      p.ar += p.tr * w * e.x;
+      p.ag += p.tg * w * e.y;
+      p.ab += p.tb * w * e.z;
+    }
+    return true;
+  }
+  p.term = v + 1;
+  const V3 wo = {-p.d.x, -p.d.y, -p.d.z};
+  const double flip = (h.n.x * wo.x + h.n.y * wo.y + h.n.z * wo.z) >= 0.0 ? 1.0 : -1.0;
+  const V3 ns = {h.n.x * flip, h.n.y * flip, h.n.z * flip};
+  const V3 em = pt::ld3(scn.mat_emit, h.mid);
+  if (em.x > 0.0 || em.y > 0.0 || em.z > 0.0) {
+    double w = 1.0;
+    if (p.prev_pdf >= 0.0) {
+      const double pn = pt::nee_pdf_for_hit(scn, h.kind, h.prim, h.t, p.d, h.n);
+      w = p.prev_pdf / (p.prev_pdf + pn);
+    }
+    p.ar += p.tr * w * em.x;
+    p.ag += p.tg * w * em.y;
+    p.ab += p.tb * w * em.z;
+  }
+  const int mkind = scn.mat_kind[h.mid];
+  const V3 alb = pt::ld3(scn.mat_albedo, h.mid);
+  const double rough = scn.mat_rough[h.mid];
+  const int base = VERTEX_DIM_BASE + v * DIMS_PER_VERTEX;
+  const uint64_t key = p.key;
+  if (mkind == pt::MAT_MIRROR) {  // delta vertex: no stop tests (kernels.py:520-548)
+    double rr_div = 1.0;
+    if (v >= pt::RR_START) {
+      if (rand_uniform(key, base + OFF_RR) >= cfg.rr_survive) return true;
+      rr_div = cfg.rr_survive;
+    }
+    const pt::BsdfSample b = pt::bsdf_sample(mkind, alb, rough, ns, wo,
+                                             rand_uniform(key, base + OFF_BSDF_U),
+                                             rand_uniform(key, base + OFF_BSDF_U + 1));
+    if (b.pdf <= 0.0) return true;
+    const double ci = b.wi.x * ns.x + b.wi.y * ns.y + b.wi.z * ns.z;
+    if (ci <= 0.0) return true;
+    const double inv = 1.0 / (b.pdf * rr_div);
+    p.tr *= b.f.x * ci * inv;
+    p.tg *= b.f.y * ci * inv;
+    p.tb *= b.f.z * ci * inv;
+    p.prev_pdf = -1.0;
+    const double sg = (h.n.x * b.wi.x + h.n.y * b.wi.y + h.n.z * b.wi.z) > 0.0 ? 1.0 : -1.0;
+    p.o = {h.p.x + sg * scn.eps * h.n.x, h.p.y + sg * scn.eps * h.n.y,
+           h.p.z + sg * scn.eps * h.n.z};
+    p.d = b.wi;
+    p.lns = ns;
+    p.v = v + 1;
+    return p.v >= pt::MAXB;
+  }
+  // relative-footprint state (kernels.py:612-618)
+  const double cs_arr = wo.x * ns.x + wo.y * ns.y + wo.z * ns.z;
+  if (v == 0) {
+    if (cs_arr > 0.0) p.a0 = h.t * h.t / (4.0 * pt::PI * cs_arr);
+  } else if (p.prev_pdf > 0.0 && cs_arr > 0.0) {
+    const double fac = h.t / (p.prev_pdf * cs_arr);
+    p.a_sp *= fac * fac;
+  }
+  const double nb = (double)cfg.nbias;
+  int stop = 0, have_cont = 0;
+  pt::BsdfSample b;
+  b.pdf = 0.0;
+  if (cs_arr <= 0.0) {
+    stop = 1;
+  } else if (cfg.mode == 2) {  // MODE_BTH
+    if (v >= 1 && p.a_sp > cfg.sph_c * p.a0) {
+      stop = 1;
+    } else {
+      b = pt::bsdf_sample(mkind, alb, rough, ns, wo, rand_uniform(key, base + OFF_BSDF_U),
+                          rand_uniform(key, base + OFF_BSDF_U + 1));
+      double ps = 0.0;
+      if (b.pdf > 0.0 && b.delta == 0) {
+        const double ci = b.wi.x * ns.x + b.wi.y * ns.y + b.wi.z * ns.z;
+        if (ci > 0.0) {
+          have_cont = 1;
+          ps = b.pdf / (b.pdf + nb / pt::PI);
+        }
+      }
+      if (rand_uniform(key, base + OFF_TERM) > ps) stop = 1;
+    }
+  } else {
+    if (v == 0) {
+      if (p.v1 == 1 && (cfg.mode == 3 || rough >= cfg.rough_cut)) stop = 1;
+    } else if (p.a_sp > cfg.sph_c * p.a0) {
+      stop = 1;
+    }
+  }
+  if (stop == 1) {
+    if (cfg.mode == 4) {  // MODE_NRC_SPH: one outgoing-radiance query at wo
+      if (cfg.cache_on == 1) {
+        pending = 1;
+        fill_stop_vertex(rec, p, h.p, ns, alb, rough, wo, base, mkind, 0, 1, cfg.max_cv);
+      }
+    } else {
+      const V3 q = pt::nee_contrib(scn, h.p, ns, h.n, mkind, alb, rough, wo,
+                                   rand_uniform(key, base + OFF_LIGHT_PICK),
+                                   rand_uniform(key, base + OFF_LIGHT_U),
+                                   rand_uniform(key, base + OFF_LIGHT_U + 1), 0);
+      p.ar += p.tr * q.x;
+      p.ag += p.tg * q.y;
+      p.ab += p.tb * q.z;
+      if (cfg.cache_on == 1) {
+        pending = 1;
+        fill_stop_vertex(rec, p, h.p, ns, alb, rough, wo, base, mkind, cfg.nbias, 0,
+                         cfg.max_cv);
+      }
+    }
+    return true;
+  }
+  const V3 q = pt::nee_contrib(scn, h.p, ns, h.n, mkind, alb, rough, wo,
+                               rand_uniform(key, base + OFF_LIGHT_PICK),
+                               rand_uniform(key, base + OFF_LIGHT_U),
+                               rand_uniform(key, base + OFF_LIGHT_U + 1), 0);
+  p.ar += p.tr * q.x;
+  p.ag += p.tg * q.y;
+  p.ab += p.tb * q.z;
+  double rr_div = 1.0;
+  if (v >= pt::RR_START) {
+    if (rand_uniform(key, base + OFF_RR) >= cfg.rr_survive) return true;
+    rr_div = cfg.rr_survive;
+  }
+  if (have_cont == 0) {
+    b = pt::bsdf_sample(mkind, alb, rough, ns, wo, rand_uniform(key, base + OFF_BSDF_U),
+                        rand_uniform(key, base + OFF_BSDF_U + 1));
+    if (b.pdf <= 0.0) return true;
+    const double ci = b.wi.x * ns.x + b.wi.y * ns.y + b.wi.z * ns.z;
+    if (ci <= 0.0) return true;
+  }
+  const double ci = b.wi.x * ns.x + b.wi.y * ns.y + b.wi.z * ns.z;
+  const double inv = 1.0 / (b.pdf * rr_div);
+  p.tr *= b.f.x * ci * inv;
+  p.tg *= b.f.y * ci * inv;
+  p.tb *= b.f.z * ci * inv;
+  p.prev_pdf = b.pdf;
+  const double sg = (h.n.x * b.wi.x + h.n.y * b.wi.y + h.n.z * b.wi.z) > 0.0 ? 1.0 : -1.0;
+  p.o = {h.p.x + sg * scn.eps * h.n.x, h.p.y + sg * scn.eps * h.n.y,
+         h.p.z + sg * scn.eps * h.n.z};
+  p.d = b.wi;
+  p.lns = ns;
+  p.v = v + 1;
+  return p.v >= pt::MAXB;
 }
 
 // One vertex of trace_sample (kernels.py:481-608) for MODE_PT / MODE_TL.
@@ -97,6 +286,7 @@ __device__ inline void start_path(PathState& p, const double* cam, const nirc_re
 // `rec` (pending == 1) instead of being evaluated inline.
 __device__ inline bool trace_vertex(const nirc_scene_t& scn, const nirc_render_cfg_t& cfg,
                                     PathState& p, CacheVertex& rec, int& pending) {
+  if (cfg.mode >= 2) return trace_vertex_biased(scn, cfg, p, rec, pending);
   pending = 0;
   const int v = p.v;
   const pt::Hit h = pt::intersect<false>(scn, p.o, p.d, pt::T_FAR);
@@ -164,6 +354,8 @@ __device__ inline bool trace_vertex(const nirc_scene_t& scn, const nirc_render_c
         rec.ncq = ncq;
         rec.mkind = mkind;
         rec.has_res = 0;
+        rec.nrc = 0;
+        rec.pad = 0;
         rec.slot = p.sid * cfg.max_cv + (p.cu - 1);
         rec.Tp[0] = rec.Tp[1] = rec.Tp[2] = 0.0;
         rec.wc[0] = rec.wc[1] = 0.0;
@@ -392,7 +584,10 @@ struct WalkJob {
   int64_t n;  // 0: render only
 };
 
-__global__ void __launch_bounds__(128, 3) k_trace(nirc_scene_t scn, const double* __restrict__ cam,
+#ifndef NIRC_TRACE_MINB
+#define NIRC_TRACE_MINB 4  // measured: 4 CTAs (16 warps) per SM beat 3 and 2
+#endif
+__global__ void __launch_bounds__(128, NIRC_TRACE_MINB) k_trace(nirc_scene_t scn, const double* __restrict__ cam,
                                                   nirc_render_cfg_t cfg, TraceOut out,
                                                   WalkJob job) {
   __shared__ __align__(16) unsigned char scene_sm[pt::kSceneSmemBytes];
@@ -432,7 +627,7 @@ __global__ void __launch_bounds__(128, 3) k_trace(nirc_scene_t scn, const double
       const int lane = threadIdx.x & 31;
       const int leader = __ffs(pm) - 1;
       unsigned long long base = 0;
-      const unsigned q = __reduce_add_sync(pm, (unsigned)(rec.ncq + rec.has_res));
+      const unsigned q = __reduce_add_sync(pm, (unsigned)(rec.ncq + rec.has_res + rec.nrc));
       if (lane == leader) {
         base = atomicAdd(out.counters, (unsigned long long)__popc(pm));
         atomicAdd(out.counters + 1, (unsigned long long)q);
@@ -486,6 +681,9 @@ __device__ inline RowDir row_direction(const CacheVertex& r, int k) {
   } else if (k == r.ncq && r.has_res) {
     o.kind = 2;
     o.wi = {r.wc[0], r.wc[1], r.wc[2]};
+  } else if (k == 0 && r.nrc) {  // NRC stop: outgoing radiance along wo
+    o.kind = 3;
+    o.wi = {r.wo[0], r.wo[1], r.wo[2]};
   }
   return o;
 }
@@ -551,45 +749,6 @@ __device__ inline RowDir row_direction_fast(const CacheVertex& r, int k) {
   return o;
 }
 
-// Real SH (bands = 4), the scalar-path recurrences of sh.py:36-76 in fp32.
-__device__ inline void sh4_f32(float x, float y, float z, const double* sh_k, float* out) {
-  const float s = sqrtf(x * x + y * y);
-  float cphi = 1.0f, sphi = 0.0f;
-  if (s > 0.0f) {
-    cphi = x / s;
-    sphi = y / s;
-  }
-  float cm = 1.0f, sm = 0.0f, pmm = 1.0f;
-#pragma unroll
-  for (int m = 0; m < 4; ++m) {
-    if (m > 0) {
-      pmm = pmm * ((2.0f * m - 1.0f) * s);
-      const float cn = cm * cphi - sm * sphi;
-      const float sn = sm * cphi + cm * sphi;
-      cm = cn;
-      sm = sn;
-    }
-    float p2 = 0.0f, p1 = 0.0f;
-#pragma unroll
-    for (int l = m; l < 4; ++l) {
-      float p;
-      if (l == m) p = pmm;
-      else if (l == m + 1) p = z * (2.0f * m + 1.0f) * pmm;
-      else p = ((2.0f * l - 1.0f) * z * p1 - (l + m - 1.0f) * p2) / (float)(l - m);
-      p2 = p1;
-      p1 = p;
-      const int base = l * l + l;
-      if (m == 0) {
-        out[base] = (float)sh_k[l * 8] * p;
-      } else {
-        const float kk = (float)sh_k[l * 8 + m] * p;
-        out[base + m] = kk * cm;
-        out[base - m] = kk * sm;
-      }
-    }
-  }
-}
-
 __device__ inline void build_row_fast(const float* feat, const CacheVertex& r, V3 wi,
                                       const double* sh_k, float* x) {
 #pragma unroll
@@ -614,6 +773,34 @@ struct InferArgs {
   int verts_per_tile;   // S = 128 / R
   long long* dbg;       // optional phase timestamps (CTA 0, group 0, thread 0)
 };
+
+// Deferred vertex term from its rows' contributions (row k at rows[3k]):
+// two-level / biased NIRC: T * (1/N_c) sum_k n(w_k) f cos/pdf in k order
+// (cache_lc_s, kernels.py:424-448), minus T' * n(w_cont) for the residual
+// (:593-601); NRC stop: T * n(wo) (:660-670).
+__device__ inline void vertex_result(const CacheVertex& r, const double* rows, double* o) {
+  if (r.nrc) {
+    o[0] = r.T[0] * rows[0];
+    o[1] = r.T[1] * rows[1];
+    o[2] = r.T[2] * rows[2];
+    return;
+  }
+  double sr = 0.0, sg = 0.0, sb = 0.0;
+  for (int k = 0; k < r.ncq; ++k) {
+    sr += rows[3 * k];
+    sg += rows[3 * k + 1];
+    sb += rows[3 * k + 2];
+  }
+  const double inv = 1.0 / r.ncq;
+  o[0] = r.T[0] * (sr * inv);
+  o[1] = r.T[1] * (sg * inv);
+  o[2] = r.T[2] * (sb * inv);
+  if (r.has_res) {
+    o[0] -= r.Tp[0] * rows[3 * r.ncq];
+    o[1] -= r.Tp[1] * rows[3 * r.ncq + 1];
+    o[2] -= r.Tp[2] * rows[3 * r.ncq + 2];
+  }
+}
 
 constexpr int kMaxVertsPerTile = 64;
 
@@ -710,7 +897,7 @@ __global__ void __launch_bounds__(NG * 128, 1)
       c0 = (double)y[0] * rd.f.x * rd.s;
       c1 = (double)y[1] * rd.f.y * rd.s;
       c2 = (double)y[2] * rd.f.z * rd.s;
-    } else if (rd.kind == 2) {
+    } else if (rd.kind >= 2) {  // residual row / NRC row: the prediction itself
       c0 = (double)y[0];
       c1 = (double)y[1];
       c2 = (double)y[2];
@@ -721,23 +908,11 @@ __global__ void __launch_bounds__(NG * 128, 1)
     tc::named_bar_sync(1 + group, tc::kGroupThreads);
     if (tg < S && v0 + tg < nverts) {
       const CacheVertex& r = s_cv[tg];
-      double sr = 0.0, sg = 0.0, sb = 0.0;
-      for (int kk = 0; kk < r.ncq; ++kk) {  // kernels.py:444-446, k order
-        sr += s_con[3 * (tg * R + kk)];
-        sg += s_con[3 * (tg * R + kk) + 1];
-        sb += s_con[3 * (tg * R + kk) + 2];
-      }
-      const double inv = 1.0 / r.ncq;
-      double o0 = r.T[0] * (sr * inv), o1 = r.T[1] * (sg * inv), o2 = r.T[2] * (sb * inv);
-      if (r.has_res) {  // kernels.py:593-601
-        const double* q = s_con + 3 * (tg * R + r.ncq);
-        o0 -= r.Tp[0] * q[0];
-        o1 -= r.Tp[1] * q[1];
-        o2 -= r.Tp[2] * q[2];
-      }
-      a.result[3 * r.slot] = o0;
-      a.result[3 * r.slot + 1] = o1;
-      a.result[3 * r.slot + 2] = o2;
+      double o[3];
+      vertex_result(r, s_con + 3 * (tg * R), o);
+      a.result[3 * r.slot] = o[0];
+      a.result[3 * r.slot + 1] = o[1];
+      a.result[3 * r.slot + 2] = o[2];
     }
     tc::named_bar_sync(1 + group, tc::kGroupThreads);
     if (pb) pb[4] = clock64();
@@ -820,23 +995,11 @@ __global__ void k_combine_rows(InferArgs a) {
   if (vid >= (int64_t)a.counters[0]) return;
   const CacheVertex& r = a.cv[vid];
   const int R = a.rows_per_vertex;
-  const double* rb = a.rowbuf + 3 * vid * R;
-  double sr = 0.0, sg = 0.0, sb = 0.0;
-  for (int k = 0; k < r.ncq; ++k) {
-    sr += rb[3 * k];
-    sg += rb[3 * k + 1];
-    sb += rb[3 * k + 2];
-  }
-  const double inv = 1.0 / r.ncq;
-  double o0 = r.T[0] * (sr * inv), o1 = r.T[1] * (sg * inv), o2 = r.T[2] * (sb * inv);
-  if (r.has_res) {
-    o0 -= r.Tp[0] * rb[3 * r.ncq];
-    o1 -= r.Tp[1] * rb[3 * r.ncq + 1];
-    o2 -= r.Tp[2] * rb[3 * r.ncq + 2];
-  }
-  a.result[3 * r.slot] = o0;
-  a.result[3 * r.slot + 1] = o1;
-  a.result[3 * r.slot + 2] = o2;
+  double o[3];
+  vertex_result(r, a.rowbuf + 3 * vid * R, o);
+  a.result[3 * r.slot] = o[0];
+  a.result[3 * r.slot + 1] = o[1];
+  a.result[3 * r.slot + 2] = o[2];
 }
 
 // render_kernel accumulation (kernels.py:753-759): per pixel, samples in
@@ -962,7 +1125,11 @@ struct RenderWs {
   size_t bytes;
 };
 
+// Inference rows per deferred vertex: N_c + the residual (two-level),
+// nbias (biased NIRC stop), 1 (NRC stop).
 int rows_per_vertex(const nirc_render_cfg_t& c) {
+  if (c.mode == 4) return 1;
+  if (c.mode >= 2) return c.nbias;
   int m = 0;
   for (int i = 0; i < c.max_cv && i < 8; ++i) m = c.nc[i] > m ? c.nc[i] : m;
   return m + 1;
@@ -978,7 +1145,7 @@ RenderWs carve_render(const nirc_render_cfg_t& c, void* base) {
     return r;
   };
   const int64_t ns = (int64_t)(c.row1 - c.row0) * c.width * c.spp;
-  const int64_t ncv = c.mode == 1 && c.cache_on ? ns * c.max_cv : 0;
+  const int64_t ncv = c.mode >= 1 && c.cache_on ? ns * c.max_cv : 0;
   w.acc = (double*)take(ns * 24);
   w.term = (int32_t*)take(ns * 4);
   w.result = (double*)take(ncv * 24 + 24);
@@ -1024,9 +1191,13 @@ extern "C" int64_t nirc_render_workspace_bytes(const nirc_render_cfg_t* cfg) {
 }
 
 static int check_render_cfg(const nirc_render_cfg_t& c) {
-  if (c.mode != 0 && c.mode != 1) {
-    set_last_error("nirc_render supports the pt and two-level modes");
+  if (c.mode < 0 || c.mode > 4) {
+    set_last_error("unknown render mode %d", c.mode);
     return NIRC_E_UNSUPPORTED;
+  }
+  if (c.mode >= 2 && (c.nbias < 1 || c.nbias > 28 || !(c.sph_c > 0.0) || c.max_cv < 1)) {
+    set_last_error("biased modes need 1 <= nbias <= 28, sph_c > 0 and max_cv >= 1");
+    return NIRC_E_CONFIG;
   }
   if (c.spp < 1 || c.row0 < 0 || c.row1 > c.height || c.row0 >= c.row1 || c.max_cv > 8) {
     set_last_error("bad render configuration");
@@ -1046,7 +1217,7 @@ static int render_impl(const nirc_scene_t* scene, const double* cam, const nirc_
                        const nirc_spec_t* spec, const float* theta, double* img, double* img2,
                        double* term, int64_t* queries_out, const RenderWs& w, const WalkJob& job,
                        cudaStream_t s) {
-  const bool tl = c.mode == 1 && c.cache_on;
+  const bool tl = c.mode >= 1 && c.cache_on;  // deferred cache vertices exist
   const int64_t ns = (int64_t)(c.row1 - c.row0) * c.width * c.spp;
   NIRC_CUDA_TRY(cudaMemsetAsync(w.counters, 0, 64, s));
   if (tl) NIRC_CUDA_TRY(cudaMemsetAsync(w.result, 0, ns * c.max_cv * 24, s));

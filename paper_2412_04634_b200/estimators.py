@@ -1,11 +1,12 @@
-"""Rendering estimators on the B200 (drop-in for the plain and two-level
-modes of pkg/src/nirclab/estimators.py).
+"""Rendering estimators on the B200 (drop-in for pkg/src/nirclab/estimators.py:
+render, render_two_level, render_biased, EstimatorConfig, RenderResult).
 
-``render`` / ``render_two_level`` run the device frame pipeline
-(C-ABI ``nirc_render``): fp64 path tracing with deferred cache vertices,
-the fused tcgen05 inference + MLMC combine, and per-pixel accumulation.
-The biased early-stop modes are outside the MLMC hot path
-and raise NotImplementedError.
+``render`` runs the device frame pipeline (C-ABI ``nirc_render``): fp64 path
+tracing with deferred cache vertices, the fused tcgen05 inference + MLMC
+combine, and per-pixel accumulation.  The biased early-stop modes
+(biased-nirc-bth / -sph, biased-nrc-sph, kernels.py:609-720) run through the
+same kernels: their stop vertex is a deferred cache vertex with nbias
+directions (or one NRC query at wo).
 """
 
 from __future__ import annotations
@@ -87,15 +88,20 @@ class _RenderWs:
         return cls.buf
 
 
-def _c_cfg(config, scene, spp, seed, frame, cache_on, rows=None, precision=None):
+def _c_cfg(config, scene, spp, seed, frame, cache_on, rows=None, precision=None, v1=None):
     mode = MODES[config.mode]
     c = _lib.NircRenderCfg()
+    c.nbias = int(config.nbias)
+    c.sph_c = float(config.sph_c)
+    c.v1 = v1.data_ptr() if v1 is not None else None
     c.mode = mode
     c.spp = int(spp)
     c.cache_on = int(cache_on)
     c.max_cv = int(config.max_cache_vertices)
     if c.max_cv > 8:
         raise ConfigError("at most 8 cache vertices are supported")
+    if mode >= 2:
+        c.max_cv = max(c.max_cv, 1)  # one stop vertex per path (result slot 0)
     for i in range(c.max_cv):
         c.nc[i] = int(config.nc[i])
     c.rough_cut = float(config.roughness_cutoff)
@@ -110,21 +116,29 @@ def _c_cfg(config, scene, spp, seed, frame, cache_on, rows=None, precision=None)
     return c
 
 
+def _v1_device(v1_map, w, h):
+    if v1_map is None:
+        return None
+    a = np.ascontiguousarray(np.asarray(v1_map, np.uint8).reshape(w * h))
+    return _dev.dev(a.astype(np.int32), torch.int32).to(torch.uint8)
+
+
 def render_device(scene, config=None, cache=None, seed=0, spp=1, frame=0, force_cache=False,
-                  rows=None, out=None, precision=None):
+                  rows=None, out=None, precision=None, v1_map=None):
     """Device-resident render: returns (img, img2, term, queries) CUDA
     tensors of sums (callers divide by spp).  ``rows`` renders a band of
-    pixel rows (multi-GPU tiles); ``out`` accumulates into given buffers."""
+    pixel rows (multi-GPU tiles); ``out`` accumulates into given buffers;
+    ``v1_map`` flags the pixels where the *_sph modes may stop at the first
+    vertex (estimators.py:173-217)."""
     if config is None:
         config = EstimatorConfig()
     mode = MODES[config.mode]
-    if mode > 1:
-        raise NotImplementedError(f"mode '{config.mode}' is outside the two-level hot path")
     w, h = int(scene.camera[14]), int(scene.camera[15])
     cache_on = 0
-    if mode == 1 and cache is not None and (force_cache or not cache.is_zero):
+    if mode >= 1 and cache is not None and (force_cache or not cache.is_zero):
         cache_on = 1
-    cfg = _c_cfg(config, scene, spp, seed, frame, cache_on, rows, precision)
+    v1 = _v1_device(v1_map, w, h) if mode in (3, 4) else None
+    cfg = _c_cfg(config, scene, spp, seed, frame, cache_on, rows, precision, v1)
     lib = _lib.load()
     ds = scene.device()
     if out is None:
@@ -160,8 +174,6 @@ def render_and_collect(scene, config, cache, seed=0, spp=1, frame=0, count=None,
     if config is None:
         config = EstimatorConfig()
     mode = MODES[config.mode]
-    if mode > 1:
-        raise NotImplementedError(f"mode '{config.mode}' is outside the two-level hot path")
     _check_kind(scene, cache.record_kind)
     if count is None:
         count = default_train_count(scene)
@@ -169,7 +181,7 @@ def render_and_collect(scene, config, cache, seed=0, spp=1, frame=0, count=None,
         train_frame = frame
     p0, p1 = (0, int(count)) if paths is None else (int(paths[0]), int(paths[1]))
     w, h = int(scene.camera[14]), int(scene.camera[15])
-    cache_on = 1 if (mode == 1 and not cache.is_zero) else 0
+    cache_on = 1 if (mode >= 1 and not cache.is_zero) else 0
     cfg = _c_cfg(config, scene, spp, seed, frame, cache_on, rows, precision)
     lib = _lib.load()
     ds = scene.device()
@@ -204,7 +216,7 @@ def render(scene, config=None, cache=None, seed=0, spp=1, frame=0, v1_map=None,
     if v1_map is not None and MODES[config.mode] <= 1:
         v1_map = None  # only the *_sph modes read it
     img, img2, term, queries = render_device(scene, config, cache, seed, spp, frame,
-                                             force_cache, precision=precision)
+                                             force_cache, precision=precision, v1_map=v1_map)
     img = img.cpu().numpy()
     img2 = img2.cpu().numpy()
     term = term.cpu().numpy()
@@ -224,3 +236,11 @@ def render_two_level(scene, cache, seed=0, spp=1, frame=0, config=None, force_ca
     if config.mode != "two-level":
         raise ConfigError(f"config mode '{config.mode}' is not two-level")
     return render(scene, config, cache, seed, spp, frame, force_cache=force_cache)
+
+
+def render_biased(scene, cache, config, seed=0, spp=1, frame=0, v1_map=None):
+    """Early-stop render shading stop vertices from the cache
+    (estimators.py:231-237)."""
+    if not config.mode.startswith("biased-"):
+        raise ConfigError(f"config mode '{config.mode}' is not biased")
+    return render(scene, config, cache, seed, spp, frame, v1_map=v1_map, force_cache=True)

@@ -255,7 +255,78 @@ def golden_collect():
     np.savez_compressed(os.path.join(HERE, "collect.npz"), **out)
 
 
+def teleport_text(res=128):
+    """The builtin teleport scene (lamp jumps at frame 40) at res x res."""
+    import nirclab
+
+    path = os.path.join(os.path.dirname(nirclab.__file__), "data", "teleport.scene")
+    return open(path).read().replace("resolution 48 48", f"resolution {res} {res}")
+
+
+CONV = dict(frames=64, ref_spp=128, res=128)
+
+
+def golden_convergence():
+    """BASELINE config 4 at CPU scale: run_experiment (experiment.py:122-213)
+    on teleport at 128^2, two-level with the default nc=(15,5,5), 64 frames of
+    online training across the frame-40 light jump; per-frame MRSE against a
+    128-spp PT reference, rVar, path length and training loss."""
+    import tempfile
+
+    from nirclab.config import RunConfig
+    from nirclab.experiment import run_experiment
+    from nirclab.scene import load_scene
+
+    sc = load_scene(teleport_text(CONV["res"]))
+    with tempfile.TemporaryDirectory() as d:
+        cfg = RunConfig(scene="teleport", mode="two-level", frames=CONV["frames"], seed=0,
+                        out=os.path.join(d, "out"), ref_dir=os.path.join(d, "ref"),
+                        ref_spp=CONV["ref_spp"])
+        res = run_experiment(cfg, scene=sc)
+    rows = res.rows
+    np.savez_compressed(os.path.join(HERE, "convergence.npz"),
+                        mrse=np.array([r["mrse"] for r in rows]),
+                        rvar=np.array([r["rvar"] for r in rows]),
+                        plen=np.array([r["avg_path_length"] for r in rows]),
+                        loss=np.array([r["train_loss"] for r in rows]),
+                        final_image=res.final.image, frames=CONV["frames"],
+                        ref_spp=CONV["ref_spp"], res=CONV["res"])
+
+
+def golden_biased():
+    """The biased early-stop family (kernels.py:609-720) through render /
+    render_biased: BTH and SPH with a NIRC cache, SPH with an NRC cache, a
+    v1 first-vertex map; images, variances and path lengths."""
+    from nirclab.caches import Cache
+    from nirclab.estimators import EstimatorConfig, render_biased
+    from nirclab.scene import load_builtin, load_scene
+
+    out = {}
+    box = load_scene(BOX)
+    mixed = load_scene(MIXED)
+    corn = load_builtin("cornell")
+    jobs = []
+    for tag, sc, seed in (("box", box, 4), ("mixed", mixed, 6), ("corn", corn, 1)):
+        w, h = int(sc.camera[14]), int(sc.camera[15])
+        v1 = (np.arange(w * h) % 3 == 0).astype(np.uint8)
+        nirc = Cache.create("nirc", sc, seed=seed, init="random")
+        nrc = Cache.create("nrc", sc, seed=seed + 1, init="random")
+        jobs += [(f"{tag}_bth", sc, EstimatorConfig(mode="biased-nirc-bth", nbias=5), nirc, None),
+                 (f"{tag}_nsph", sc, EstimatorConfig(mode="biased-nirc-sph", nbias=7), nirc, v1),
+                 (f"{tag}_rsph", sc, EstimatorConfig(mode="biased-nrc-sph"), nrc, v1)]
+    for tag, sc, cfg, cache, v1 in jobs:
+        r = render_biased(sc, cache, cfg, seed=3, spp=2, frame=1, v1_map=v1)
+        out[f"{tag}_image"] = r.image
+        out[f"{tag}_var"] = r.sample_var
+        out[f"{tag}_plen"] = r.path_length
+    np.savez_compressed(os.path.join(HERE, "biased.npz"), **out)
+
+
 if __name__ == "__main__" and len(sys.argv) > 1:
+    if "biased" in sys.argv:
+        golden_biased()
+    if "convergence" in sys.argv:
+        golden_convergence()
     if "scenes" in sys.argv:
         golden_scenes()
     if "render" in sys.argv:
