@@ -400,14 +400,20 @@ __device__ inline bool trace_vertex(const nirc_scene_t& scn, const nirc_render_c
 // the records in (path, vertex) order -- the reference's row order.  The
 // walk is written per lane (walk_start / walk_vertex / walk_finish) so the
 // persistent tracer can interleave training paths with camera paths.
+// Record kinds (caches.py:87-131): 0 nirc, 1 nirc_full, 2 nrc, 3 nvc, 4 nirc_env.
+constexpr int REC_NIRC = 0, REC_NIRC_FULL = 1, REC_NRC = 2, REC_NVC = 3, REC_NIRC_ENV = 4;
+
 struct Stage {
-  // vertex-major: field[v * count + p]
-  double *pos, *ns, *alb, *rough, *wi, *pdf, *tgt, *tfull;
+  // vertex-major: field[v * count + p]; one candidate record per vertex,
+  // already in the requested kind's (dirs, pdf, target) form
+  double *pos, *ns, *alb, *rough, *wi, *pdf, *tgt;
   uint8_t* keep;
   int32_t* nrec;   // per path
   int32_t* nvert;  // per path
   int64_t count;
   int64_t path0;   // global index of local path 0 (multi-GPU path shards)
+  int32_t kind;    // REC_*
+  int32_t pad;
 };
 
 struct WalkLane {
@@ -490,6 +496,41 @@ __device__ inline bool walk_vertex(const nirc_scene_t& scn, WalkLane& w, const S
                         rand_uniform(key, base + OFF_LIGHT_U),
                         rand_uniform(key, base + OFF_LIGHT_U + 1), 0);
   w.nee[v][0] = q.x; w.nee[v][1] = q.y; w.nee[v][2] = q.z;
+  const int kind = st.kind;
+  if (kind == REC_NVC || kind == REC_NIRC_ENV) {
+    // environment-visibility record (kernels.py:183-210)
+    uint8_t ok = 0;
+    if (delta == 0 && scn.env_kind != pt::ENV_NONE) {
+      const pt::Cosine c = pt::cosine_dir(rand_uniform(key, base + OFF_CACHE),
+                                          rand_uniform(key, base + OFF_CACHE + 1));
+      if (c.pdf > 0.0) {
+        const Onb b = onb(ns.x, ns.y, ns.z);
+        const V3 e = {b.tx * c.x + b.bx * c.y + ns.x * c.z, b.ty * c.x + b.by * c.y + ns.y * c.z,
+                      b.tz * c.x + b.bz * c.y + ns.z * c.z};
+        const double sg = (hh.n.x * e.x + hh.n.y * e.y + hh.n.z * e.z) > 0.0 ? 1.0 : -1.0;
+        const V3 so = {hh.p.x + sg * scn.eps * hh.n.x, hh.p.y + sg * scn.eps * hh.n.y,
+                       hh.p.z + sg * scn.eps * hh.n.z};
+        const double vis = pt::occluded(scn, so, e, pt::T_FAR) ? 0.0 : 1.0;
+        const V3 er = pt::env_eval(scn, e);
+        st.wi[3 * at] = e.x; st.wi[3 * at + 1] = e.y; st.wi[3 * at + 2] = e.z;
+        st.pdf[at] = c.pdf;
+        if (kind == REC_NVC) {
+          st.tgt[3 * at] = st.tgt[3 * at + 1] = st.tgt[3 * at + 2] = vis;
+        } else {
+          st.tgt[3 * at] = vis * er.x; st.tgt[3 * at + 1] = vis * er.y;
+          st.tgt[3 * at + 2] = vis * er.z;
+        }
+        ok = 1;
+      }
+    }
+    st.keep[at] = ok;
+  } else if (kind == REC_NRC) {
+    // keyed at the vertex the sampled segment landed on (caches.py:107-116):
+    // direction = -w_i of the previous vertex = wo, pdf of that segment
+    st.wi[3 * at] = wo.x; st.wi[3 * at + 1] = wo.y; st.wi[3 * at + 2] = wo.z;
+    st.pdf[at] = w.prev_pdf;
+    st.keep[at] = (v >= 1 && delta == 0 && w.prev_pdf > 0.0) ? 1 : 0;
+  }
   int alive = 1;
   double rr_div = 1.0;
   if (v >= pt::RR_START) {
@@ -523,17 +564,22 @@ __device__ inline bool walk_vertex(const nirc_scene_t& scn, WalkLane& w, const S
       }
     }
   }
-  st.wi[3 * at] = vwi.x; st.wi[3 * at + 1] = vwi.y; st.wi[3 * at + 2] = vwi.z;
-  st.pdf[at] = vpdf;
-  st.keep[at] = (delta == 0 && vpdf > 0.0) ? 1 : 0;
+  if (kind == REC_NIRC || kind == REC_NIRC_FULL) {
+    st.wi[3 * at] = vwi.x; st.wi[3 * at + 1] = vwi.y; st.wi[3 * at + 2] = vwi.z;
+    st.pdf[at] = vpdf;
+    st.keep[at] = (delta == 0 && vpdf > 0.0) ? 1 : 0;
+  }
   w.v = v + 1;
   return cont == 0;
 }
 
-// Backward sweep (kernels.py:249-277) over the path's w.v vertices.
+// Backward sweep (kernels.py:249-277) over the path's w.v vertices: the
+// incident-radiance targets (MIS-weighted emission for nirc, raw emission
+// for nirc_full) and the outgoing radiance at each vertex (nrc).
 __device__ inline void walk_finish(const WalkLane& w, const Stage& st) {
   const int64_t C = st.count, p = w.p;
   const int n = w.v;
+  const int kind = st.kind;
   double lr = 0.0, lg = 0.0, lb = 0.0;
   int nrec = 0;
   for (int v = n - 1; v >= 0; --v) {
@@ -546,11 +592,17 @@ __device__ inline void walk_finish(const WalkLane& w, const Stage& st) {
       qr = w.emit[v + 1][0] + lr; qg = w.emit[v + 1][1] + lg; qb = w.emit[v + 1][2] + lb;
     }
     const int64_t at = (int64_t)v * C + p;
-    st.tgt[3 * at] = cr; st.tgt[3 * at + 1] = cg; st.tgt[3 * at + 2] = cb;
-    st.tfull[3 * at] = qr; st.tfull[3 * at + 1] = qg; st.tfull[3 * at + 2] = qb;
+    if (kind == REC_NIRC) {
+      st.tgt[3 * at] = cr; st.tgt[3 * at + 1] = cg; st.tgt[3 * at + 2] = cb;
+    } else if (kind == REC_NIRC_FULL) {
+      st.tgt[3 * at] = qr; st.tgt[3 * at + 1] = qg; st.tgt[3 * at + 2] = qb;
+    }
     lr = w.nee[v][0] + w.fcp[v][0] * cr;
     lg = w.nee[v][1] + w.fcp[v][1] * cg;
     lb = w.nee[v][2] + w.fcp[v][2] * cb;
+    if (kind == REC_NRC) {
+      st.tgt[3 * at] = lr; st.tgt[3 * at + 1] = lg; st.tgt[3 * at + 2] = lb;
+    }
     nrec += st.keep[at];
   }
   st.nrec[p] = nrec;
@@ -1074,7 +1126,7 @@ __global__ void k_scan_counts(const int32_t* __restrict__ cnt, int64_t n, int64_
 // One warp per path: lanes take the path's vertices (<= 64, two rounds),
 // ballot the kept ones and write them in vertex order at off[p] + rank --
 // the reference's (path, vertex) row order with coalesced stores.
-__global__ void k_compact_records(Stage st, const int64_t* __restrict__ off, int kind,
+__global__ void k_compact_records(Stage st, const int64_t* __restrict__ off,
                                   nirc_records_out_t out) {
   const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -1094,7 +1146,7 @@ __global__ void k_compact_records(Stage st, const int64_t* __restrict__ off, int
           out.ns[3 * q + c] = st.ns[3 * at + c];
           out.alb[3 * q + c] = st.alb[3 * at + c];
           out.dirs[3 * q + c] = st.wi[3 * at + c];
-          out.target[3 * q + c] = kind == 1 ? st.tfull[3 * at + c] : st.tgt[3 * at + c];
+          out.target[3 * q + c] = st.tgt[3 * at + c];
         }
         out.rough[q] = st.rough[at];
         out.pdf[q] = st.pdf[at];
@@ -1175,7 +1227,6 @@ Stage carve_stage(int64_t count, void* base, size_t* bytes) {
   st.wi = (double*)take(V * 24);
   st.pdf = (double*)take(V * 8);
   st.tgt = (double*)take(V * 24);
-  st.tfull = (double*)take(V * 24);
   st.keep = (uint8_t*)take(V);
   st.nrec = (int32_t*)take(count * 4);
   st.nvert = (int32_t*)take(count * 4);
@@ -1333,9 +1384,9 @@ extern "C" int nirc_render_collect(const nirc_scene_t* scene, const double* cam,
     set_last_error("count must be positive and path0 non-negative");
     return NIRC_E_CONFIG;
   }
-  if (kind != 0 && kind != 1) {
-    set_last_error("record kind %d unsupported on the device (nirc=0, nirc_full=1)", kind);
-    return NIRC_E_UNSUPPORTED;
+  if (kind < 0 || kind > 4) {
+    set_last_error("unknown record kind %d", kind);
+    return NIRC_E_CONFIG;
   }
   RenderWs w = carve_render(*cfg, workspace);
   size_t sb = 0;
@@ -1345,13 +1396,14 @@ extern "C" int nirc_render_collect(const nirc_scene_t* scene, const double* cam,
     return NIRC_E_CONFIG;
   }
   stg.path0 = path0;
+  stg.kind = kind;
   WalkJob job{stg, train_seed, train_frame, count};
   if ((st = render_impl(scene, cam, *cfg, spec, theta, img, img2, term, queries_out, w, job, s)))
     return st;
   int64_t* off = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(stg.nvert) + aup(count * 4));
   k_scan_counts<<<1, 1024, 0, s>>>(stg.nrec, count, off, n_out);
   NIRC_LAUNCH_CHECK("k_scan_counts");
-  k_compact_records<<<(int)((count * 32 + 255) / 256), 256, 0, s>>>(stg, off, kind, *out);
+  k_compact_records<<<(int)((count * 32 + 255) / 256), 256, 0, s>>>(stg, off, *out);
   NIRC_LAUNCH_CHECK("k_compact_records");
   return NIRC_OK;
 }
@@ -1372,9 +1424,9 @@ extern "C" int nirc_collect_range(const nirc_scene_t* scene, const double* cam, 
     set_last_error("count must be positive and path0 non-negative");
     return NIRC_E_CONFIG;
   }
-  if (kind != 0 && kind != 1) {
-    set_last_error("record kind %d unsupported on the device (nirc=0, nirc_full=1)", kind);
-    return NIRC_E_UNSUPPORTED;
+  if (kind < 0 || kind > 4) {
+    set_last_error("unknown record kind %d", kind);
+    return NIRC_E_CONFIG;
   }
   size_t need = 0;
   Stage st = carve_stage(count, workspace, &need);
@@ -1383,12 +1435,13 @@ extern "C" int nirc_collect_range(const nirc_scene_t* scene, const double* cam, 
     return NIRC_E_CONFIG;
   }
   st.path0 = path0;
+  st.kind = kind;
   int64_t* off = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(st.nvert) + aup(count * 4));
   k_walk_record<<<(int)((count + 63) / 64), 64, 0, s>>>(*scene, cam, seed, frame, st);
   NIRC_LAUNCH_CHECK("k_walk_record");
   k_scan_counts<<<1, 1024, 0, s>>>(st.nrec, count, off, n_out);
   NIRC_LAUNCH_CHECK("k_scan_counts");
-  k_compact_records<<<(int)((count * 32 + 255) / 256), 256, 0, s>>>(st, off, kind, *out);
+  k_compact_records<<<(int)((count * 32 + 255) / 256), 256, 0, s>>>(st, off, *out);
   NIRC_LAUNCH_CHECK("k_compact_records");
   return NIRC_OK;
 }

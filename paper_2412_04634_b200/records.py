@@ -15,7 +15,7 @@ from . import _dev, _lib
 from .caches import RECORD_KINDS, Records
 from .errors import ConfigError
 
-_KIND = {"nirc": 0, "nirc_full": 1}
+_KIND = {"nirc": 0, "nirc_full": 1, "nrc": 2, "nvc": 3, "nirc_env": 4}
 
 
 class _CollectWs:

@@ -248,7 +248,11 @@ def golden_collect():
             ("box", load_scene(BOX), 40, 5, 3, "nirc"),
             ("boxfull", load_scene(BOX), 40, 5, 3, "nirc_full"),
             ("mixed", load_scene(MIXED), 60, 2, 1, "nirc"),
-            ("corn", load_builtin("cornell"), 103, 0, 0, "nirc")):
+            ("corn", load_builtin("cornell"), 103, 0, 0, "nirc"),
+            ("boxnrc", load_scene(BOX), 40, 5, 3, "nrc"),
+            ("mixednrc", load_scene(MIXED), 60, 2, 1, "nrc"),
+            ("mixednvc", load_scene(MIXED), 60, 2, 1, "nvc"),
+            ("mixedenv", load_scene(MIXED), 60, 7, 2, "nirc_env")):
         rec = collect_training_records(sc, seed, count, kind=kind, frame=frame)
         for k in ("pos", "ns", "alb", "rough", "dirs", "target", "pdf"):
             out[f"{tag}_{k}"] = getattr(rec, k)
@@ -322,7 +326,24 @@ def golden_biased():
     np.savez_compressed(os.path.join(HERE, "biased.npz"), **out)
 
 
+def golden_snapshot():
+    """NNCACHE1 files written by the reference's Cache.save
+    (caches.py:256-295, snapshot.py:31-49) for a small cache on the BOX:
+    fresh, and after one collect + train_frame (m, v, t, frame non-trivial)."""
+    from nirclab.caches import Cache
+    from nirclab.scene import load_scene
+
+    box = load_scene(BOX)
+    c = Cache.create("nirc", box, seed=11, table_log2=10, depth=2)
+    c.save(os.path.join(HERE, "snapshot_fresh.nncache"))
+    rec = c.collect(count=40, frame=0)
+    c.train_frame(rec, steps=2)
+    c.save(os.path.join(HERE, "snapshot_trained.nncache"))
+
+
 if __name__ == "__main__" and len(sys.argv) > 1:
+    if "snapshot" in sys.argv:
+        golden_snapshot()
     if "biased" in sys.argv:
         golden_biased()
     if "convergence" in sys.argv:

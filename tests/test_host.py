@@ -121,3 +121,22 @@ def test_make_spec_and_init_theta_match_oracle():
         assert np.array_equal(init_theta(s, seed=1, out_scale=0.1),
                               O.init_theta(o, seed=1, out_scale=0.1))
     assert make_spec().in_dim == 47 and make_spec().theta_len == 802179
+
+
+def test_reference_snapshots_roundtrip_bytes():
+    """NNCACHE1 files written by the reference's Cache.save parse with the
+    host reader and re-serialise byte for byte (snapshot.py:31-77)."""
+    from paper_2412_04634_b200.snapshot import load_snapshot, save_snapshot
+
+    for name in ("snapshot_fresh", "snapshot_trained"):
+        path = os.path.join(GOLDEN, name + ".nncache")
+        d = load_snapshot(path)
+        assert {"theta", "m", "v", "t", "frame", "net", "bb_min", "bb_ext"} <= set(d)
+        import tempfile
+
+        with tempfile.TemporaryDirectory() as td:
+            out = os.path.join(td, "x.nncache")
+            save_snapshot(out, d)
+            assert open(out, "rb").read() == open(path, "rb").read(), name
+    t = load_snapshot(os.path.join(GOLDEN, "snapshot_trained.nncache"))
+    assert int(t["t"]) == 2 and int(t["frame"]) == 1 and np.any(t["m"] != 0)
