@@ -50,11 +50,6 @@ __global__ void k_pack_weights(nirc_spec_t sp, TcNet net, const float* __restric
 // The default NIRC input layout (test_default_layout_dimensions,
 // tests/test_neural.py:81-88): 12 levels x 2 feats, 4 SH bands, 7 aux.
 constexpr int kL = 12, kF = 2, kBands = 4, kIn = 47, kK0 = 48;
-#ifdef NIRC_FF_F64SH
-constexpr bool kFusedF32Sh = false;
-#else
-constexpr bool kFusedF32Sh = true;  // SH block in fp32 (<= 5e-7 abs) in the fused kernel
-#endif
 constexpr int kDenseLevels = 4;  // dense coarse levels of the cfg2 kernel (measured best)
 
 __host__ __device__ inline bool is_default_layout(const nirc_spec_t& sp) {
@@ -64,8 +59,9 @@ __host__ __device__ inline bool is_default_layout(const nirc_spec_t& sp) {
 
 // Encodes one query row into x[48] (x[47] = 0 pad) as encode_batch
 // (encoding.py:111-157): hash + aux blocks bit-identical; the SH block
-// bit-identical with the f64 recurrences (F32SH = false) or within 5e-7 abs
-// in fp32 (F32SH = true, the fused inference kernel).  Levels < ND are
+// bit-identical with the f64 recurrences (F32SH = false; measured faster in
+// the fused kernel too: the f64 pipe is otherwise idle there) or within
+// 5e-7 abs in fp32 (F32SH = true).  Levels < ND are
 // gathered from the CTA's dense shared-memory copies, the rest from the
 // L2-resident tables.
 template <int ND, bool F32SH>
@@ -135,23 +131,8 @@ __global__ void __launch_bounds__(NG * 128, 1)
     const int64_t row = tile * tc::kTileRows + tg;
     float x[kK0];
     if (row < n) {
-#ifdef NIRC_FF_NOSTREAM
-      encode_default<ND, kFusedF32Sh>(sp, theta, pos + 3 * row, nrm + 3 * row, alb + 3 * row,
-                                      rough[row], dirs + 3 * row, x, dl, dense);
-#else
-      // the query rows are read once: streaming loads keep them from evicting
-      // hash-table lines out of L1
-      double pr[3], nr[3], ar[3], dr[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        pr[c] = __ldcs(pos + 3 * row + c);
-        nr[c] = __ldcs(nrm + 3 * row + c);
-        ar[c] = __ldcs(alb + 3 * row + c);
-        dr[c] = __ldcs(dirs + 3 * row + c);
-      }
-      encode_default<ND, kFusedF32Sh>(sp, theta, pr, nr, ar, __ldcs(rough + row), dr, x, dl,
-                                      dense);
-#endif
+      encode_default<ND, false>(sp, theta, pos + 3 * row, nrm + 3 * row, alb + 3 * row,
+                                rough[row], dirs + 3 * row, x, dl, dense);
     } else {
 #pragma unroll
       for (int k = 0; k < kK0; ++k) x[k] = 0.0f;
