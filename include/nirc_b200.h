@@ -76,6 +76,8 @@ typedef struct nirc_scene {
   double bbox_min[3], bbox_inv_ext[3];
   const double *bvh_lo, *bvh_hi;
   const int32_t *bvh_a, *bvh_b, *bvh_prim;
+  const float* tri_f32;  /* kernel-private scratch (the staged fp32 triangle
+                            filter table); callers pass NULL */
 } nirc_scene_t;
 
 /* Two-level estimator knobs; mirrors EstimatorConfig

@@ -82,6 +82,7 @@ class NircScene(C.Structure):
         ("bbox_min", C.c_double * 3), ("bbox_inv_ext", C.c_double * 3),
         ("bvh_lo", C.c_void_p), ("bvh_hi", C.c_void_p),
         ("bvh_a", C.c_void_p), ("bvh_b", C.c_void_p), ("bvh_prim", C.c_void_p),
+        ("tri_f32", C.c_void_p),
     ]
 
 

@@ -108,12 +108,90 @@ struct Hit {
 // to the same primitive.
 constexpr int kLinearMaxPrims = 64;
 
+// Conservative fp32 pre-test of one scan-order triangle (the linear-scan
+// path): returns false only when ray_tri's f64 result is certainly rejected
+// by the caller's window t in (t_lo, t_hi).  The fp32 evaluation of
+// ray_tri's numerators (det, u*det, v*det, t*det) differs from the f64 one
+// by at most ~9 unit roundoffs of the magnitude bounds below (inputs
+// rounded to fp32 included); K = 16 u gives 2x headroom, and the 1e-9
+// thresholds carry a 1e-12 relative slack for ray_tri's own rounding of
+// 1/det and the products.  Rows of T (48 B per triangle, 16 B aligned):
+//   (v0.xyz, |e1|_1), (e1.xyz, |e2|_1), (e2.xyz, |v0|_1).
+constexpr float kFilterK = 16.0f * 5.9604645e-8f * 1.0001f;  // 16 unit roundoffs
+struct RayF32 {
+  float ox, oy, oz, dx, dy, dz, kd, no;  // kd = K * |d|_1, no = |o|_1
+};
+__device__ inline RayF32 ray_f32(V3 o, V3 d) {
+  RayF32 r;
+  r.ox = (float)o.x; r.oy = (float)o.y; r.oz = (float)o.z;
+  r.dx = (float)d.x; r.dy = (float)d.y; r.dz = (float)d.z;
+  r.kd = kFilterK * (fabsf(r.dx) + fabsf(r.dy) + fabsf(r.dz)) * 1.0001f;
+  r.no = (fabsf(r.ox) + fabsf(r.oy) + fabsf(r.oz)) * 1.0001f;
+  return r;
+}
+__device__ inline bool tri_candidate(const RayF32& r, const float4* T, float t_lo, float t_hi) {
+  const float4 A = T[0], B = T[1], C = T[2];
+  const float px = r.dy * C.z - r.dz * C.y;
+  const float py = r.dz * C.x - r.dx * C.z;
+  const float pz = r.dx * C.y - r.dy * C.x;
+  const float det = B.x * px + B.y * py + B.z * pz;
+  const float tx = r.ox - A.x, ty = r.oy - A.y, tz = r.oz - A.z;
+  const float un = tx * px + ty * py + tz * pz;
+  const float qx = ty * B.z - tz * B.y;
+  const float qy = tz * B.x - tx * B.z;
+  const float qz = tx * B.y - ty * B.x;
+  const float vn = r.dx * qx + r.dy * qy + r.dz * qz;
+  const float tn = C.x * qx + C.y * qy + C.z * qz;
+  // magnitude bounds: |e1|_1 |d|_1 |e2|_1 etc., |t|_1 <= |o|_1 + |v0|_1
+  const float nt = (r.no + C.w) * 1.0001f;
+  const float Ed = r.kd * A.w * B.w;
+  const float Eu = r.kd * nt * B.w;
+  const float Ev = r.kd * nt * A.w;
+  const float Et = kFilterK * nt * A.w * B.w;
+  const float ad = fabsf(det);
+  if (!(ad > Ed)) return true;  // sign of det uncertain: exact test decides
+  const float sgn = det > 0.0f ? 1.0f : -1.0f;
+  const float u = un * sgn, v = vn * sgn, t = tn * sgn;
+  const float hi = ad + Ed, lo = ad - Ed;
+  if (u + Eu < -1.000001e-9f * hi) return false;       // u < -1e-9
+  if (u - Eu > 1.000001f * hi) return false;           // u > 1 + 1e-9
+  if (v + Ev < -1.000001e-9f * hi) return false;       // v < -1e-9
+  if (u + v - Eu - Ev > 1.000001f * hi) return false;  // u + v > 1 + 1e-9
+  if (t + Et < t_lo * lo * 0.999999f) return false;    // t <= t_lo (t_lo > 0)
+  if (t - Et > t_hi * hi * 1.000001f) return false;    // t >= t_hi (inf: never)
+  return true;
+}
+
 template <bool AnyHit>
 __device__ inline Hit intersect(const nirc_scene_t& s, V3 o, V3 d, double t_max) {
   const double eps = s.eps;
   double best = t_max;
   int kind = -1, prim = -1;
-  if (s.n_tri + s.n_sph <= kLinearMaxPrims && s.n_sph == 0) {
+  if (s.tri_f32 && s.n_sph == 0 && s.n_tri <= kLinearMaxPrims) {
+    // warp-uniform fp32 pre-test over the scan order, then ray_tri (f64,
+    // the reference's arithmetic) on each lane's own candidates in scan
+    // order: the accepted hit (and any-hit boolean) equal the full scan's
+    const int np = s.n_tri;
+    const RayF32 r = ray_f32(o, d);
+    const float4* T = reinterpret_cast<const float4*>(s.tri_f32);
+    const float f_lo = (float)eps;
+    const float f_hi = t_max < 1e29 ? (float)t_max : __int_as_float(0x7f800000);
+    uint64_t cand = 0;
+    for (int k = 0; k < np; ++k)
+      if (tri_candidate(r, T + 3 * k, f_lo, f_hi)) cand |= 1ull << k;
+    while (cand) {
+      const int k = __ffsll((long long)cand) - 1;
+      cand &= cand - 1;
+      const int pid = s.bvh_prim[k];
+      const double t = ray_tri(o, d, ld3(s.tri_v0, pid), ld3(s.tri_e1, pid), ld3(s.tri_e2, pid));
+      if (t > eps && t < best) {
+        best = t;
+        kind = 0;
+        prim = pid;
+        if (AnyHit) break;
+      }
+    }
+  } else if (s.n_tri + s.n_sph <= kLinearMaxPrims && s.n_sph == 0) {
     const int np = s.n_tri;
     for (int k = 0; k < np; ++k) {
       const int pid = s.bvh_prim[k];
@@ -513,7 +591,8 @@ constexpr int kSceneSmemBytes = 40 * 1024;
 
 __host__ __device__ inline size_t scene_smem_bytes(const nirc_scene_t& s) {
   return (size_t)s.n_tri * (4 * 3 * 8 + 4) + (size_t)s.n_sph * (4 * 8 + 4) +
-         (size_t)s.n_bvh * (6 * 8 + 8) + (size_t)(s.n_tri + s.n_sph) * 4 + 64;
+         (size_t)s.n_bvh * (6 * 8 + 8) + (size_t)(s.n_tri + s.n_sph) * 4 + 64 +
+         (size_t)s.n_tri * 48 + 16;  // fp32 filter table
 }
 
 __device__ inline void stage_scene(nirc_scene_t& s, unsigned char* sm) {
@@ -545,6 +624,31 @@ __device__ inline void stage_scene(nirc_scene_t& s, unsigned char* sm) {
   s.bvh_a = cpi(s.bvh_a, s.n_bvh);
   s.bvh_b = cpi(s.bvh_b, s.n_bvh);
   s.bvh_prim = cpi(s.bvh_prim, s.n_tri + s.n_sph);
+  s.tri_f32 = nullptr;
+  if (s.n_sph == 0 && s.n_tri <= kLinearMaxPrims) {
+    // fp32 filter table in scan order (16-byte aligned after the int arrays)
+    uintptr_t a = reinterpret_cast<uintptr_t>(ip);
+    a = (a + 15) & ~(uintptr_t)15;
+    float* f = reinterpret_cast<float*>(a);
+    __syncthreads();  // the staged doubles / prim order are read below
+    for (int k = threadIdx.x; k < s.n_tri; k += blockDim.x) {
+      const int pid = s.bvh_prim[k];
+      const double* v0 = s.tri_v0 + 3 * pid;
+      const double* e1 = s.tri_e1 + 3 * pid;
+      const double* e2 = s.tri_e2 + 3 * pid;
+      float* row = f + 12 * k;
+      for (int c = 0; c < 3; ++c) {
+        row[c] = (float)v0[c];
+        row[4 + c] = (float)e1[c];
+        row[8 + c] = (float)e2[c];
+      }
+      // L1 norms of the fp32-rounded vectors, rounded up
+      row[3] = (fabsf(row[4]) + fabsf(row[5]) + fabsf(row[6])) * 1.0001f;
+      row[7] = (fabsf(row[8]) + fabsf(row[9]) + fabsf(row[10])) * 1.0001f;
+      row[11] = (fabsf(row[0]) + fabsf(row[1]) + fabsf(row[2])) * 1.0001f;
+    }
+    s.tri_f32 = f;
+  }
   __syncthreads();
 }
 

@@ -1458,3 +1458,57 @@ extern "C" int nirc_collect(const nirc_scene_t* scene, const double* cam, uint64
 // stamps of CTA 0 / group 0 of the next k_infer_tc launches into `buf`
 // (device, >= 64*8 int64), or disable with NULL.
 extern "C" void nirc_debug_infer_probe(long long* buf) { nirc::g_infer_probe = buf; }
+
+// Tools/tests only (not part of include/nirc_b200.h): the fp32 pre-filtered
+// triangle scan against the plain f64 scan on n random rays through the
+// scene (origins inside its box, random directions; a third of the rays aimed
+// exactly at triangle vertices / edge points; occlusion windows at the hit
+// distance and one ulp either side).  counts[0] = mismatches (hit kind,
+// primitive or t bit pattern, or occlusion boolean), counts[1] = hits.
+namespace nirc {
+__global__ void k_debug_intersect(nirc_scene_t scn, int64_t n, uint64_t seed,
+                                  unsigned long long* counts) {
+  __shared__ __align__(16) unsigned char scene_sm[pt::kSceneSmemBytes];
+  pt::stage_scene(scn, scene_sm);
+  nirc_scene_t plain = scn;
+  plain.tri_f32 = nullptr;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = stream_key(seed, 77, 0, (uint64_t)i, 0);
+    auto U = [&](int dim) { return rand_uniform(key, dim); };
+    const double ext = 1.0 / scn.bbox_inv_ext[0];
+    V3 o = {scn.bbox_min[0] + U(0) / scn.bbox_inv_ext[0], scn.bbox_min[1] + U(1) / scn.bbox_inv_ext[1],
+            scn.bbox_min[2] + U(2) / scn.bbox_inv_ext[2]};
+    V3 d = {U(3) - 0.5, U(4) - 0.5, U(5) - 0.5};
+    if (U(6) < 0.33 && scn.n_tri > 0) {  // aim at a vertex or an edge point of a triangle
+      const int t = (int)(U(7) * scn.n_tri) % scn.n_tri;
+      const V3 v0 = pt::ld3(scn.tri_v0, t), e1 = pt::ld3(scn.tri_e1, t), e2 = pt::ld3(scn.tri_e2, t);
+      const double a = U(8) < 0.5 ? 0.0 : U(9), b = U(10) < 0.5 ? 0.0 : 1.0 - a;
+      const V3 tp = {v0.x + a * e1.x + b * e2.x, v0.y + a * e1.y + b * e2.y,
+                     v0.z + a * e1.z + b * e2.z};
+      d = {tp.x - o.x, tp.y - o.y, tp.z - o.z};
+    }
+    const double dl = sqrt(d.x * d.x + d.y * d.y + d.z * d.z);
+    if (!(dl > 0.0)) continue;
+    d = {d.x / dl, d.y / dl, d.z / dl};
+    (void)ext;
+    const pt::Hit a = pt::intersect<false>(scn, o, d, pt::T_FAR);
+    const pt::Hit b = pt::intersect<false>(plain, o, d, pt::T_FAR);
+    bool bad = a.kind != b.kind || a.prim != b.prim ||
+               (a.kind >= 0 && __double_as_longlong(a.t) != __double_as_longlong(b.t));
+    if (b.kind >= 0) {
+      atomicAdd(counts + 1, 1ull);
+      const double tm[3] = {b.t, nextafter(b.t, 0.0), nextafter(b.t, 1e300)};
+      for (int q = 0; q < 3; ++q)
+        bad |= pt::occluded(scn, o, d, tm[q]) != pt::occluded(plain, o, d, tm[q]);
+    }
+    if (bad) atomicAdd(counts, 1ull);
+  }
+}
+}  // namespace nirc
+
+extern "C" int nirc_debug_intersect_check(const nirc_scene_t* scene, int64_t n, uint64_t seed,
+                                          unsigned long long* counts) {
+  nirc::k_debug_intersect<<<148 * 4, 128>>>(*scene, n, seed, counts);
+  return cudaGetLastError() == cudaSuccess ? 0 : 5;
+}
