@@ -149,17 +149,17 @@ __device__ inline bool tri_candidate(const RayF32& r, const float4* T, float t_l
   const float Ev = r.kd * nt * A.w;
   const float Et = kFilterK * nt * A.w * B.w;
   const float ad = fabsf(det);
-  if (!(ad > Ed)) return true;  // sign of det uncertain: exact test decides
   const float sgn = det > 0.0f ? 1.0f : -1.0f;
   const float u = un * sgn, v = vn * sgn, t = tn * sgn;
   const float hi = ad + Ed, lo = ad - Ed;
-  if (u + Eu < -1.000001e-9f * hi) return false;       // u < -1e-9
-  if (u - Eu > 1.000001f * hi) return false;           // u > 1 + 1e-9
-  if (v + Ev < -1.000001e-9f * hi) return false;       // v < -1e-9
-  if (u + v - Eu - Ev > 1.000001f * hi) return false;  // u + v > 1 + 1e-9
-  if (t + Et < t_lo * lo * 0.999999f) return false;    // t <= t_lo (t_lo > 0)
-  if (t - Et > t_hi * hi * 1.000001f) return false;    // t >= t_hi (inf: never)
-  return true;
+  // branch-free: every condition is a predicate, the scan loop stays straight
+  const bool out = (u + Eu < -1.000001e-9f * hi) |        // u < -1e-9
+                   (u - Eu > 1.000001f * hi) |            // u > 1 + 1e-9
+                   (v + Ev < -1.000001e-9f * hi) |        // v < -1e-9
+                   (u + v - Eu - Ev > 1.000001f * hi) |   // u + v > 1 + 1e-9
+                   (t + Et < t_lo * lo * 0.999999f) |     // t <= t_lo (t_lo > 0)
+                   (t - Et > t_hi * hi * 1.000001f);      // t >= t_hi (inf: never)
+  return !(ad > Ed) | !out;  // sign of det uncertain: the exact test decides
 }
 
 template <bool AnyHit>
@@ -177,8 +177,9 @@ __device__ inline Hit intersect(const nirc_scene_t& s, V3 o, V3 d, double t_max)
     const float f_lo = (float)eps;
     const float f_hi = t_max < 1e29 ? (float)t_max : __int_as_float(0x7f800000);
     uint64_t cand = 0;
+#pragma unroll 4
     for (int k = 0; k < np; ++k)
-      if (tri_candidate(r, T + 3 * k, f_lo, f_hi)) cand |= 1ull << k;
+      cand |= (uint64_t)tri_candidate(r, T + 3 * k, f_lo, f_hi) << k;
     while (cand) {
       const int k = __ffsll((long long)cand) - 1;
       cand &= cand - 1;

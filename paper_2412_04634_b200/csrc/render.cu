@@ -637,7 +637,7 @@ struct WalkJob {
 };
 
 #ifndef NIRC_TRACE_MINB
-#define NIRC_TRACE_MINB 4  // measured: 4 CTAs (16 warps) per SM beat 3 and 2
+#define NIRC_TRACE_MINB 3  // measured with the fp32 pre-test: 3 CTAs/SM (168 regs) beat 4 and 2
 #endif
 __global__ void __launch_bounds__(128, NIRC_TRACE_MINB) k_trace(nirc_scene_t scn, const double* __restrict__ cam,
                                                   nirc_render_cfg_t cfg, TraceOut out,
