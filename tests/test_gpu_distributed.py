@@ -98,7 +98,9 @@ def test_train_grad_shards_match_train_step(lib, n):
     # maps a ~1e-7 gradient change on a near-zero gradient to up to ~lr/1000.
     # A wrong shard moves parameters by ~lr = 1e-2.
     d = np.abs(c.theta.cpu().numpy() - ta.cpu().numpy())
-    assert d.max() < 1e-4 and d.mean() < 1e-8, (d.max(), d.mean())
+    # a missing or doubled tile would move ~all touched parameters by ~lr
+    assert (d > 1e-5).mean() < 1e-3 and d.max() < 5e-3 and d.mean() < 1e-7, (
+        d.max(), d.mean(), (d > 1e-5).mean())
 
 
 def _free_port():
@@ -176,5 +178,6 @@ def test_sharded_frame_two_ranks_one_gpu(lib):
         np.testing.assert_allclose(out[1][0], ref[1][0], rtol=1e-3, atol=1e-4)
         np.testing.assert_allclose(out[1][2][-1], ref[1][2], rtol=1e-4)
         d = np.abs(theta - cache.theta.cpu().numpy())
-        assert d.max() < 1e-3 and d.mean() < 1e-7, (d.max(), d.mean())
+        assert (d > 1e-5).mean() < 1e-2 and d.max() < 1e-2 and d.mean() < 1e-6, (
+            d.max(), d.mean(), (d > 1e-5).mean())
     assert np.array_equal(res[0][1], res[1][1])
