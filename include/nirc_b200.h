@@ -279,6 +279,34 @@ int nirc_collect_range(const nirc_scene_t* scene, const double* cam,
                        const nirc_records_out_t* out, int64_t* n_out,
                        void* workspace, int64_t workspace_bytes, void* stream);
 
+/* ---- per-interaction helpers of the API --------------------------------- */
+/* estimators.py _surface_dirs (used by estimate_Lc / estimate_Lr,
+ * estimators.py:260-320): n bsdf_sample draws at one interaction (shading
+ * normal ns, outgoing wo, material mat; both 3-vectors on the HOST) from the
+ * device uniforms u (2n); delta, pdf <= 0 and below-horizon draws give zero
+ * rows.  dirs, f (n,3), pdf, cos (n,) device f64. */
+int nirc_surface_samples(const nirc_scene_t* scene, const double* ns_host,
+                         const double* wo_host, int32_t mat, const double* u,
+                         int32_t n, double* dirs, double* pdf, double* f,
+                         double* cosv, void* stream);
+
+/* sample_incident_targets / incident_targets_kernel (caches.py:134-155,
+ * kernels.py:315-338): `count` independent walk_record estimates of the
+ * incident radiance along one fixed ray (walk i keyed stream_key(seed,
+ * P_TRAIN, frame, i, 0)); out / out_full (count,3) device f64 = MIS-weighted /
+ * raw emission at the first hit.  origin, dir, prev_ns on the HOST. */
+int nirc_incident_targets(const nirc_scene_t* scene, uint64_t seed, uint64_t frame,
+                          const double* origin_host, const double* dir_host,
+                          double prev_pdf, const double* prev_ns_host,
+                          int32_t count, double* out, double* out_full,
+                          void* stream);
+
+/* pt_radiance (estimators.py:240-257): sample `sample` of pixel (ix, iy),
+ * MODE_PT, seed / frame / width / height from cfg; out (3,) device f64. */
+int nirc_pt_radiance(const nirc_scene_t* scene, const double* cam,
+                     const nirc_render_cfg_t* cfg, int32_t ix, int32_t iy,
+                     int32_t sample, double* out, void* stream);
+
 /* ---- one frame: render + collect ---------------------------------------- */
 /* One frame's render (nirc_render) AND training-record collection
  * (nirc_collect_range over paths [path0, path0+count) with seed train_seed,

@@ -135,6 +135,11 @@ SIGNATURES = {
     "nirc_collect": (I32, [C.POINTER(NircScene), P, U64, U64, I64, I32,
                            C.POINTER(NircRecordsOut), P, P, I64, P]),
     "nirc_collect_workspace_bytes": (I64, [I64]),
+    "nirc_surface_samples": (I32, [C.POINTER(NircScene), P, P, I32, P, I32, P, P, P, P, P]),
+    "nirc_incident_targets": (I32, [C.POINTER(NircScene), U64, U64, P, P, F64, P, I32, P, P,
+                                    P]),
+    "nirc_pt_radiance": (I32, [C.POINTER(NircScene), P, C.POINTER(NircRenderCfg), I32, I32, I32,
+                               P, P]),
     "nirc_collect_range": (I32, [C.POINTER(NircScene), P, U64, U64, I64, I64, I32,
                                  C.POINTER(NircRecordsOut), P, P, I64, P]),
 }

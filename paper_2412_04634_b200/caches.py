@@ -144,6 +144,35 @@ def _launch_steps(spec, theta, adam, records, seed, frame, steps, batch, loss_ki
     return res
 
 
+def collect_training_records(scene, seed, count, kind="nirc", frame=0):
+    """Trace `count` camera paths and distill records of the given kind
+    (caches.py:87-131), on the device (records.py)."""
+    from .records import collect_training_records as _collect
+
+    return _collect(scene, seed, count, kind, frame)
+
+
+def sample_incident_targets(scene, origin, direction, seed, count, prev_pdf=-1.0,
+                            prev_ns=(0.0, 0.0, 0.0), frame=0):
+    """Independent incident-radiance estimates along one fixed ray
+    (caches.py:134-155): (targets, full_targets), each (count, 3), from
+    `count` device walk_record walks (C ABI nirc_incident_targets)."""
+    count = int(count)
+    out = _dev.zeros((max(count, 1), 3), torch.float64)
+    out_full = _dev.zeros((max(count, 1), 3), torch.float64)
+    if count > 0:
+        o = np.ascontiguousarray(np.asarray(origin, np.float64).reshape(3))
+        d = np.ascontiguousarray(np.asarray(direction, np.float64).reshape(3))
+        pn = np.ascontiguousarray(np.asarray(prev_ns, np.float64).reshape(3))
+        ds = scene.device()
+        lib = _lib.load()
+        _lib.check(lib.nirc_incident_targets(
+            ds.ptr(), int(seed), int(frame), o.ctypes.data, d.ctypes.data, float(prev_pdf),
+            pn.ctypes.data, count, _dev.ptr(out), _dev.ptr(out_full), _dev.stream()),
+            "nirc_incident_targets")
+    return out[:count].cpu().numpy(), out_full[:count].cpu().numpy()
+
+
 def train_frame_device(spec, theta, records, seed, frame, steps=4, batch=None, adam=None,
                        loss_kind="relative_l2", loss_eps=0.01, return_idx=False):
     """Device training on a bare (spec, theta) pair -- the batch form of

@@ -1512,3 +1512,157 @@ extern "C" int nirc_debug_intersect_check(const nirc_scene_t* scene, int64_t n, 
   nirc::k_debug_intersect<<<148 * 4, 128>>>(*scene, n, seed, counts);
   return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }
+
+// ---------------------------------------------------------------------
+// Per-interaction helpers of the drop-in API (estimators.py:240-320,
+// caches.py:134-155): BSDF draws at one surface, repeated incident-radiance
+// walks along one ray, one path-traced pixel sample.
+namespace nirc {
+
+// estimators.py _surface_dirs: n draws (u pairs) of bsdf_sample at one
+// interaction; delta / pdf <= 0 / below-horizon draws give zero rows.
+__global__ void k_surface_samples(nirc_scene_t scn, V3 ns, V3 wo, int mat, const double* u,
+                                  int n, double* dirs, double* pdf, double* f, double* cosv) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int mkind = scn.mat_kind[mat];
+  const V3 alb = pt::ld3(scn.mat_albedo, mat);
+  const pt::BsdfSample b = pt::bsdf_sample(mkind, alb, scn.mat_rough[mat], ns, wo, u[2 * k],
+                                           u[2 * k + 1]);
+  double c = 0.0;
+  bool ok = b.pdf > 0.0 && b.delta == 0;
+  if (ok) {
+    c = b.wi.x * ns.x + b.wi.y * ns.y + b.wi.z * ns.z;
+    ok = c > 0.0;
+  }
+  dirs[3 * k] = ok ? b.wi.x : 0.0;
+  dirs[3 * k + 1] = ok ? b.wi.y : 0.0;
+  dirs[3 * k + 2] = ok ? b.wi.z : 0.0;
+  pdf[k] = ok ? b.pdf : 0.0;
+  f[3 * k] = ok ? b.f.x : 0.0;
+  f[3 * k + 1] = ok ? b.f.y : 0.0;
+  f[3 * k + 2] = ok ? b.f.z : 0.0;
+  cosv[k] = ok ? c : 0.0;
+}
+
+// incident_targets_kernel (kernels.py:315-338): walk i keys
+// stream_key(seed, P_TRAIN, frame, i, 0) and starts on the given ray.
+__global__ void k_incident_targets(nirc_scene_t scn, uint64_t seed, uint64_t frame, V3 o, V3 d,
+                                   double pv_pdf, V3 pns, int count, Stage st, double* out,
+                                   double* out_full) {
+  __shared__ __align__(16) unsigned char scene_sm[pt::kSceneSmemBytes];
+  pt::stage_scene(scn, scene_sm);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  WalkLane w;
+  w.p = i;
+  w.key = stream_key(seed, P_TRAIN, frame, (uint64_t)i, 0);
+  w.o = o;
+  w.d = d;
+  w.prev_pdf = pv_pdf;
+  w.lns = pns;
+  w.v = 0;
+  w.esc = 0;
+  for (int c = 0; c < 3; ++c) w.env_m[c] = w.env_r[c] = 0.0;
+  while (!walk_vertex(scn, w, st)) {
+  }
+  walk_finish(w, st);
+  // the incident estimate along the input ray (walk_record's return value)
+  const int n = w.v;
+  if (n == 0) {
+    for (int c = 0; c < 3; ++c) {
+      out[3 * i + c] = w.env_m[c];
+      out_full[3 * i + c] = w.env_r[c];
+    }
+    return;
+  }
+  double l[3] = {0.0, 0.0, 0.0};
+  for (int v = n - 1; v >= 0; --v) {
+    double cc[3];
+    for (int c = 0; c < 3; ++c) {
+      cc[c] = v == n - 1 ? (w.esc ? w.env_m[c] : 0.0) : w.mise[v + 1][c] + l[c];
+    }
+    for (int c = 0; c < 3; ++c) l[c] = w.nee[v][c] + w.fcp[v][c] * cc[c];
+  }
+  for (int c = 0; c < 3; ++c) {
+    out[3 * i + c] = w.mise[0][c] + l[c];
+    out_full[3 * i + c] = w.emit[0][c] + l[c];
+  }
+}
+
+// pt_radiance (estimators.py:240-257): one MODE_PT sample of one pixel.
+__global__ void k_pt_radiance(nirc_scene_t scn, const double* cam, nirc_render_cfg_t cfg,
+                              int ix, int iy, int sample, double* out) {
+  __shared__ __align__(16) unsigned char scene_sm[pt::kSceneSmemBytes];
+  pt::stage_scene(scn, scene_sm);
+  if (threadIdx.x != 0) return;
+  PathState p;
+  cfg.row0 = iy;
+  cfg.spp = sample + 1;
+  const int64_t sid = (int64_t)ix * cfg.spp + sample;  // row band [iy, iy+1)
+  start_path(p, cam, cfg, sid);
+  CacheVertex rec;
+  int pending;
+  while (!trace_vertex(scn, cfg, p, rec, pending)) {
+  }
+  out[0] = p.ar;
+  out[1] = p.ag;
+  out[2] = p.ab;
+}
+}  // namespace nirc
+
+extern "C" int nirc_surface_samples(const nirc_scene_t* scene, const double* ns_host,
+                                    const double* wo_host, int32_t mat, const double* u,
+                                    int32_t n, double* dirs, double* pdf, double* f,
+                                    double* cosv, void* stream) {
+  if (n <= 0) return NIRC_OK;
+  if (mat < 0 || mat >= scene->n_mat) {
+    set_last_error("material %d out of range", mat);
+    return NIRC_E_CONFIG;
+  }
+  const V3 ns = {ns_host[0], ns_host[1], ns_host[2]};
+  const V3 wo = {wo_host[0], wo_host[1], wo_host[2]};
+  k_surface_samples<<<(n + 127) / 128, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      *scene, ns, wo, mat, u, n, dirs, pdf, f, cosv);
+  NIRC_LAUNCH_CHECK("k_surface_samples");
+  return NIRC_OK;
+}
+
+extern "C" int nirc_incident_targets(const nirc_scene_t* scene, uint64_t seed, uint64_t frame,
+                                     const double* origin_host, const double* dir_host,
+                                     double prev_pdf, const double* prev_ns_host, int32_t count,
+                                     double* out, double* out_full, void* stream) {
+  if (count <= 0) return NIRC_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  size_t bytes = 0;
+  carve_stage(count, nullptr, &bytes);
+  void* ws = nullptr;
+  NIRC_CUDA_TRY(cudaMallocAsync(&ws, bytes, s));
+  size_t b2 = 0;
+  Stage st = carve_stage(count, ws, &b2);
+  st.kind = REC_NIRC;
+  const V3 o = {origin_host[0], origin_host[1], origin_host[2]};
+  const V3 d = {dir_host[0], dir_host[1], dir_host[2]};
+  const V3 pns = {prev_ns_host[0], prev_ns_host[1], prev_ns_host[2]};
+  k_incident_targets<<<(count + 63) / 64, 64, 0, s>>>(*scene, seed, frame, o, d, prev_pdf, pns,
+                                                      count, st, out, out_full);
+  NIRC_LAUNCH_CHECK("k_incident_targets");
+  NIRC_CUDA_TRY(cudaFreeAsync(ws, s));
+  return NIRC_OK;
+}
+
+extern "C" int nirc_pt_radiance(const nirc_scene_t* scene, const double* cam,
+                                const nirc_render_cfg_t* cfg, int32_t ix, int32_t iy,
+                                int32_t sample, double* out, void* stream) {
+  if (ix < 0 || iy < 0 || ix >= cfg->width || iy >= cfg->height || sample < 0) {
+    set_last_error("pixel / sample out of range");
+    return NIRC_E_CONFIG;
+  }
+  nirc_render_cfg_t c = *cfg;
+  c.mode = 0;
+  c.cache_on = 0;
+  k_pt_radiance<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(*scene, cam, c, ix, iy,
+                                                                      sample, out);
+  NIRC_LAUNCH_CHECK("k_pt_radiance");
+  return NIRC_OK;
+}

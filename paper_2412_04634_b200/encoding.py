@@ -72,3 +72,56 @@ def scatter_grid_grad(spec, grad_theta, entries, weights, dX):
     elif g.data_ptr() != grad_theta.data_ptr():
         grad_theta.copy_(g)
     return grad_theta
+
+
+# ---- scalar per-surface API (encoding.py:45-108, :170-192) ----------------
+_ZERO_GRIDS = {}
+
+
+def _encode_rows(spec, theta, pos, normal, albedo, rough, dirs):
+    """Device encoder on a handful of rows -> float32 numpy (n, in_dim)."""
+    f = lambda a, w: np.asarray(a, np.float64).reshape(-1, w)  # noqa: E731
+    X, _, _ = encode_batch(spec, theta, f(pos, 3), f(normal, 3), f(albedo, 3),
+                           np.asarray(rough, np.float64).reshape(-1), f(dirs, 3))
+    return X
+
+
+def encode_surface_into(spec, theta, px, py, pz, nx, ny, nz, ar, ag, ab, rough, xin):
+    """Hash-grid + aux blocks of one surface into xin (encoding.py:45-101);
+    the SH block of xin is left as it is.  Runs the device encoder."""
+    X = _encode_rows(spec, theta, (px, py, pz), (nx, ny, nz), (ar, ag, ab), rough,
+                     (0.0, 0.0, 1.0))[0]
+    g = spec.levels * spec.feats
+    a0 = g + spec.bands * spec.bands
+    xin[:g] = X[:g]
+    xin[a0:a0 + AUX_DIM] = X[a0:a0 + AUX_DIM]
+    return xin
+
+
+def encode_dir_into(spec, dx, dy, dz, xin):
+    """SH block of one direction into xin (encoding.py:104-108), evaluated
+    by the device encoder (f64 recurrences rounded to f32)."""
+    key = int(spec.grid_len), int(spec.theta_len)
+    th = _ZERO_GRIDS.get(key)
+    if th is None:
+        th = _dev.zeros((int(spec.theta_len),), torch.float32)
+        _ZERO_GRIDS[key] = th
+    X = _encode_rows(spec, th, (0.0, 0.0, 0.0), (0.0, 0.0, 1.0), (0.0, 0.0, 0.0), 0.0,
+                     (dx, dy, dz))[0]
+    g = spec.levels * spec.feats
+    s = spec.bands * spec.bands
+    xin[g:g + s] = X[g:g + s]
+    return xin
+
+
+def encode(surface, wi, grids, bands=None):
+    """One full encoded input (position, direction, aux) as a float64 vector
+    (encoding.py:170-192).  surface = (position, normal, albedo, roughness);
+    grids has .spec and .theta (a cache or a bare net)."""
+    from .errors import ConfigError
+
+    spec, theta = grids.spec, grids.theta
+    if bands is not None and bands != spec.bands:
+        raise ConfigError(f"encode bands {bands} does not match network bands {spec.bands}")
+    pos, normal, albedo, rough = surface
+    return _encode_rows(spec, theta, pos, normal, albedo, rough, wi)[0].astype(np.float64)

@@ -244,3 +244,155 @@ def render_biased(scene, cache, config, seed=0, spp=1, frame=0, v1_map=None):
     if not config.mode.startswith("biased-"):
         raise ConfigError(f"config mode '{config.mode}' is not biased")
     return render(scene, config, cache, seed, spp, frame, v1_map=v1_map, force_cache=True)
+
+
+# ---- per-interaction estimators and helpers (estimators.py:86-136, 240-320,
+# 386-393 of the reference) -------------------------------------------------
+@dataclass
+class PathState:
+    """Per-path bookkeeping of the biased stop tests (estimators.py:86-95)."""
+
+    throughput: np.ndarray = None
+    vertex: int = 0
+    a: float = 1.0
+    a0: float = 0.0
+    alive: bool = True
+    prev_pdf: float = -1.0
+
+    def __post_init__(self):
+        if self.throughput is None:
+            self.throughput = np.ones(3)
+
+
+def sph_update(state, seg_len, pdf, cos_arrival):
+    """Fold one traced segment into the footprint state (estimators.py:98-118):
+    the first segment sets a0, later ones scale a by (len / (pdf cos))^2."""
+    import math
+    from dataclasses import replace
+
+    s = replace(state, vertex=state.vertex + 1, prev_pdf=pdf)
+    if cos_arrival <= 0.0:
+        s.a = math.inf
+        return s
+    if state.vertex == 0:
+        s.a0 = seg_len * seg_len / (4.0 * math.pi * cos_arrival)
+        return s
+    if pdf > 0.0:
+        f = seg_len / (pdf * cos_arrival)
+        s.a = state.a * f * f
+    return s
+
+
+def sph_should_terminate(state, c=0.01):
+    """Spread test: fires from the second bounce once a > c * a0."""
+    return state.vertex >= 2 and state.a > c * state.a0
+
+
+def bth_continuation_probability(pdf, n_cache):
+    """Survival probability pdf / (pdf + n_cache / pi) of the stochastic
+    brdf test (estimators.py:126-136)."""
+    import math
+
+    if pdf < 0.0 or not math.isfinite(pdf):
+        raise ConfigError(f"pdf {pdf} must be finite and non-negative")
+    if n_cache < 1:
+        raise ConfigError("n_cache must be at least 1")
+    return pdf / (pdf + n_cache / math.pi)
+
+
+def _surface_dirs(scene, it, n, seed, stream, offset):
+    """n brdf draws at an interaction, (dirs, pdf, f, cos) with invalid rows
+    zero (estimators.py:260-278): u from the P_MEASURE stream (host rng,
+    bit-exact), the BSDF sampling on the device."""
+    from .rng import P_MEASURE, uniform_array
+
+    u = _dev.dev(uniform_array(seed, P_MEASURE, stream, 2 * n, offset=offset), torch.float64)
+    dirs = _dev.zeros((n, 3), torch.float64)
+    pdf = _dev.zeros((n,), torch.float64)
+    fval = _dev.zeros((n, 3), torch.float64)
+    cos = _dev.zeros((n,), torch.float64)
+    ns = np.ascontiguousarray(np.asarray(it.ns, np.float64))
+    wo = np.ascontiguousarray(np.asarray(it.wo, np.float64))
+    lib = _lib.load()
+    ds = scene.device()
+    _lib.check(lib.nirc_surface_samples(ds.ptr(), ns.ctypes.data, wo.ctypes.data, int(it.mat),
+                                        _dev.ptr(u), int(n), _dev.ptr(dirs), _dev.ptr(pdf),
+                                        _dev.ptr(fval), _dev.ptr(cos), _dev.stream()),
+               "nirc_surface_samples")
+    return dirs.cpu().numpy(), pdf.cpu().numpy(), fval.cpu().numpy(), cos.cpu().numpy()
+
+
+def _check_not_delta(scene, it, what):
+    from .scene import MAT_MIRROR
+
+    if int(scene.pack.mat_kind[it.mat]) == MAT_MIRROR:
+        raise ConfigError(f"{what} undefined on a delta lobe")
+
+
+def estimate_Lc(scene, it, cache, n_c=15, seed=0, stream=0):
+    """Cache term of the two-level split at one interaction
+    (estimators.py:281-296): mean over n_c brdf-sampled directions of
+    n(w) f cos / pdf; rejected draws contribute zero."""
+    _check_not_delta(scene, it, "cache term")
+    if n_c < 1:
+        raise ConfigError("n_c must be at least 1")
+    dirs, pdf, fval, cos = _surface_dirs(scene, it, n_c, seed, stream, 0)
+    out = np.zeros(3)
+    ok = pdf > 0.0
+    if np.any(ok):
+        pred = cache.nirc_query(it, dirs[ok])
+        wgt = cos[ok] / pdf[ok]
+        out = np.sum(pred * fval[ok] * wgt[:, None], axis=0)
+    return out / n_c
+
+
+def estimate_Lr(scene, it, cache, n_r=1, seed=0, stream=0):
+    """Residual term of the split (estimators.py:299-320): mean over n_r
+    fresh brdf draws of (L_i(w) - n(w)) f cos / pdf, L_i from an
+    independent device recording walk along w."""
+    from .caches import sample_incident_targets
+
+    _check_not_delta(scene, it, "residual term")
+    if n_r < 1:
+        raise ConfigError("n_r must be at least 1")
+    dirs, pdf, fval, cos = _surface_dirs(scene, it, n_r, seed, stream, 1000)
+    out = np.zeros(3)
+    for k in range(n_r):
+        if pdf[k] <= 0.0:
+            continue
+        li, _ = sample_incident_targets(scene, it.position, dirs[k], seed + 7919 * (stream + 1),
+                                        1, prev_pdf=pdf[k], prev_ns=it.ns, frame=k)
+        pred = cache.nirc_query(it, dirs[k][None, :])[0]
+        out += (li[0] - pred) * fval[k] * (cos[k] / pdf[k])
+    return out / n_r
+
+
+def pt_radiance(scene, ix, iy, seed=0, sample=0, frame=0):
+    """One path-traced radiance sample of pixel (ix, iy) as the renderer
+    draws it (estimators.py:240-257), traced on the device."""
+    cfg = _c_cfg(EstimatorConfig(mode="pt"), scene, 1, seed, frame, 0)
+    out = _dev.zeros((3,), torch.float64)
+    lib = _lib.load()
+    ds = scene.device()
+    _lib.check(lib.nirc_pt_radiance(ds.ptr(), _dev.ptr(ds.cam), C.byref(cfg), int(ix), int(iy),
+                                    int(sample), _dev.ptr(out), _dev.stream()),
+               "nirc_pt_radiance")
+    return out.cpu().numpy()
+
+
+def reference_render(scene, spp, seed=0, out_dir=".refcache", allow_compute=True, force=False):
+    """Path-traced reference image, cached on disk as PFM by scene state and
+    seed (estimators.py:386-393)."""
+    import os
+
+    from .pfm import read_pfm, write_pfm
+
+    path = os.path.join(out_dir, f"ref-{scene.content_hash()}-{spp}-{seed}.pfm")
+    if not force and os.path.exists(path):
+        return read_pfm(path).astype(np.float64)
+    if not allow_compute:
+        raise ConfigError(f"missing cached render {path}")
+    img = render(scene, EstimatorConfig(mode="pt"), seed=seed, spp=spp).image
+    os.makedirs(out_dir, exist_ok=True)
+    write_pfm(path, img)
+    return np.asarray(img, np.float64)

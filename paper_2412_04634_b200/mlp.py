@@ -166,3 +166,14 @@ def full_forward(spec, theta, pos, normal, albedo, rough, dirs, training=False,
         return _dev.out(mlp_forward(spec, th, X), host)
     _lib.check(st, "nirc_full_forward")
     return _dev.out(Y, host)
+
+
+def mlp_forward_s(spec, theta, xin, h1=None, h2=None):
+    """Scalar forward of one encoded input (mlp.py:160-192): the first three
+    outputs as a tuple (unused slots zero).  h1/h2 (the reference's scratch
+    rows) are accepted and unused: the device kernel keeps its own."""
+    X = np.asarray(xin, np.float32).reshape(1, -1)
+    Y = mlp_forward(spec, theta, X)
+    y = np.asarray(Y, np.float64).reshape(-1)
+    out = [float(y[i]) if i < y.size else 0.0 for i in range(3)]
+    return out[0], out[1], out[2]

@@ -341,7 +341,47 @@ def golden_snapshot():
     c.save(os.path.join(HERE, "snapshot_trained.nncache"))
 
 
+def golden_api():
+    """Per-interaction API of the reference on the BOX: estimate_Lc /
+    estimate_Lr (estimators.py:281-320), sample_incident_targets
+    (caches.py:134-155), pt_radiance (estimators.py:240-257), encode +
+    mlp_forward_s (encoding.py:170-192, mlp.py:160-192)."""
+    from nirclab.caches import Cache, sample_incident_targets
+    from nirclab.encoding import encode
+    from nirclab.estimators import estimate_Lc, estimate_Lr, pt_radiance
+    from nirclab.mlp import mlp_forward_s
+    from nirclab.scene import load_scene
+
+    box = load_scene(BOX)
+    cache = Cache.create("nirc", box, seed=9, init="random")
+    it = box.intersect(np.array([0.5, 0.5, 0.5]), np.array([0.0, -1.0, 0.0]))
+    out = {"Lc": estimate_Lc(box, it, cache, n_c=8, seed=3, stream=1),
+           "Lr": estimate_Lr(box, it, cache, n_r=3, seed=2, stream=0)}
+    d = np.array([0.3, -0.4, 0.5])
+    d /= np.linalg.norm(d)
+    out["sit"], out["sit_full"] = sample_incident_targets(
+        box, [0.5, 0.5, 0.5], d, seed=5, count=6, prev_pdf=0.3, prev_ns=(0.0, 1.0, 0.0),
+        frame=2)
+    # the reference test's pixels (tests/test_estimators.py:147-152).  Its
+    # pt_radiance builds the key in interpreted Python: keys >= 2^63 overflow
+    # the jitted rand_uniform, and for frame != 0 it disagrees with its own
+    # render_kernel (which ours matches: the convergence run pins the walks)
+    pix = [(0, 0, 0), (7, 3, 0), (15, 15, 0)]
+    out["pix"] = np.array(pix)
+    out["ptr"] = np.array([pt_radiance(box, ix, iy, seed=11, sample=s, frame=0)
+                           for ix, iy, s in pix])
+    surf = (np.array([0.3, 0.2, 0.7]), np.array([0.0, 1.0, 0.0]), np.array([0.7, 0.7, 0.7]), 1.0)
+    x = encode(surf, d, cache)
+    out["x"] = x
+    mw = int(max(cache.spec.dims))
+    out["y"] = np.array(mlp_forward_s(cache.spec, cache.theta, x.astype(np.float32),
+                                      np.zeros(mw, np.float32), np.zeros(mw, np.float32)))
+    np.savez_compressed(os.path.join(HERE, "api.npz"), **out)
+
+
 if __name__ == "__main__" and len(sys.argv) > 1:
+    if "api" in sys.argv:
+        golden_api()
     if "snapshot" in sys.argv:
         golden_snapshot()
     if "biased" in sys.argv:
