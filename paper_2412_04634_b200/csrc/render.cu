@@ -17,6 +17,7 @@
 //                     deterministic order (cache_lc_s, kernels.py:424-448).
 //   k_accumulate      per pixel: r = PT sum + cache terms; img += r,
 //                     img2 += r*r, term += vertices (render_kernel :753-759).
+#include <type_traits>
 #include "common.cuh"
 #include "pt_common.cuh"
 #include "tc_mlp.cuh"
@@ -284,9 +285,8 @@ __device__ inline bool trace_vertex_biased(const nirc_scene_t& scn, const nirc_r
 // One vertex of trace_sample (kernels.py:481-608) for MODE_PT / MODE_TL.
 // Returns true when the path ended.  A two-level cache vertex is returned in
 // `rec` (pending == 1) instead of being evaluated inline.
-__device__ inline bool trace_vertex(const nirc_scene_t& scn, const nirc_render_cfg_t& cfg,
-                                    PathState& p, CacheVertex& rec, int& pending) {
-  if (cfg.mode >= 2) return trace_vertex_biased(scn, cfg, p, rec, pending);
+__device__ inline bool trace_vertex_pt_tl(const nirc_scene_t& scn, const nirc_render_cfg_t& cfg,
+                                          PathState& p, CacheVertex& rec, int& pending) {
   pending = 0;
   const int v = p.v;
   const pt::Hit h = pt::intersect<false>(scn, p.o, p.d, pt::T_FAR);
@@ -390,6 +390,15 @@ __device__ inline bool trace_vertex(const nirc_scene_t& scn, const nirc_render_c
   p.lns = ns;
   p.v = v + 1;
   return p.v >= pt::MAXB;
+}
+
+// kBiased: the biased early-stop family, else MODE_PT / MODE_TL.  Compiled
+// as separate tracer instantiations so each carries only its own code.
+template <bool kBiased>
+__device__ inline bool trace_vertex(const nirc_scene_t& scn, const nirc_render_cfg_t& cfg,
+                                    PathState& p, CacheVertex& rec, int& pending) {
+  if constexpr (kBiased) return trace_vertex_biased(scn, cfg, p, rec, pending);
+  else return trace_vertex_pt_tl(scn, cfg, p, rec, pending);
 }
 
 // ---------------------------------------------------------------------
@@ -639,22 +648,26 @@ struct WalkJob {
 #ifndef NIRC_TRACE_MINB
 #define NIRC_TRACE_MINB 3  // measured with the fp32 pre-test: 3 CTAs/SM (168 regs) beat 4 and 2
 #endif
-__global__ void __launch_bounds__(128, NIRC_TRACE_MINB) k_trace(nirc_scene_t scn, const double* __restrict__ cam,
-                                                  nirc_render_cfg_t cfg, TraceOut out,
-                                                  WalkJob job) {
+// kWalks: the launch also traces the frame's training walks (render+collect);
+// render-only launches are compiled without the walk lanes' state.
+template <bool kBiased, bool kWalks>
+__global__ void __launch_bounds__(128, NIRC_TRACE_MINB)
+    k_trace(nirc_scene_t scn, const double* __restrict__ cam, nirc_render_cfg_t cfg, TraceOut out,
+            WalkJob job) {
   __shared__ __align__(16) unsigned char scene_sm[pt::kSceneSmemBytes];
   pt::stage_scene(scn, scene_sm);
   const int64_t nsamp = (int64_t)(cfg.row1 - cfg.row0) * cfg.width * cfg.spp;
-  const int64_t nwork = job.n + nsamp;
+  const int64_t nwalk = kWalks ? job.n : 0;
+  const int64_t nwork = nwalk + nsamp;
   PathState p;
-  WalkLane wl;
+  typename std::conditional<kWalks, WalkLane, char>::type wl;
   bool active = false, walking = false;
   auto start = [&](int64_t item) {
-    if (item < job.n) {
-      walk_start(wl, cam, job.seed, job.frame, job.st, item);
+    if (item < nwalk) {
+      if constexpr (kWalks) walk_start(wl, cam, job.seed, job.frame, job.st, item);
       walking = true;
     } else {
-      start_path(p, cam, cfg, item - job.n);
+      start_path(p, cam, cfg, item - nwalk);
       walking = false;
     }
     active = true;
@@ -667,10 +680,12 @@ __global__ void __launch_bounds__(128, NIRC_TRACE_MINB) k_trace(nirc_scene_t scn
     bool done = false;
     if (active) {
       if (walking) {
-        done = walk_vertex(scn, wl, job.st);
-        if (done) walk_finish(wl, job.st);
+        if constexpr (kWalks) {
+          done = walk_vertex(scn, wl, job.st);
+          if (done) walk_finish(wl, job.st);
+        }
       } else {
-        done = trace_vertex(scn, cfg, p, rec, pending);
+        done = trace_vertex<kBiased>(scn, cfg, p, rec, pending);
       }
     }
     // warp-aggregated append of the cache-vertex records and query counts
@@ -1273,16 +1288,22 @@ static int render_impl(const nirc_scene_t* scene, const double* cam, const nirc_
   NIRC_CUDA_TRY(cudaMemsetAsync(w.counters, 0, 64, s));
   if (tl) NIRC_CUDA_TRY(cudaMemsetAsync(w.result, 0, ns * c.max_cv * 24, s));
   TraceOut to{w.acc, w.term, w.cv, w.counters};
-  static int trace_blocks_per_sm = 0;
-  if (!trace_blocks_per_sm) {
-    NIRC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&trace_blocks_per_sm, k_trace,
-                                                                128, 0));
-    if (trace_blocks_per_sm < 1) trace_blocks_per_sm = 1;
-  }
-  const int64_t tgrid_max = (ns + job.n + 127) / 128;
-  const int64_t tgrid_pers = (int64_t)sm_count() * trace_blocks_per_sm;
-  k_trace<<<(int)(tgrid_max < tgrid_pers ? tgrid_max : tgrid_pers), 128, 0, s>>>(*scene, cam, c,
-                                                                                  to, job);
+  auto launch_trace = [&](auto kern) -> int {
+    int per_sm = 0;
+    NIRC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0));
+    if (per_sm < 1) per_sm = 1;
+    const int64_t tgrid_max = (ns + job.n + 127) / 128;
+    const int64_t tgrid_pers = (int64_t)sm_count() * per_sm;
+    kern<<<(int)(tgrid_max < tgrid_pers ? tgrid_max : tgrid_pers), 128, 0, s>>>(*scene, cam, c,
+                                                                                to, job);
+    return NIRC_OK;
+  };
+  int tst;
+  if (c.mode >= 2)
+    tst = job.n > 0 ? launch_trace(k_trace<true, true>) : launch_trace(k_trace<true, false>);
+  else
+    tst = job.n > 0 ? launch_trace(k_trace<false, true>) : launch_trace(k_trace<false, false>);
+  if (tst) return tst;
   NIRC_LAUNCH_CHECK("k_trace");
   if (tl) {
     if (!spec || !theta) return NIRC_E_CONFIG;
@@ -1603,7 +1624,7 @@ __global__ void k_pt_radiance(nirc_scene_t scn, const double* cam, nirc_render_c
   start_path(p, cam, cfg, sid);
   CacheVertex rec;
   int pending;
-  while (!trace_vertex(scn, cfg, p, rec, pending)) {
+  while (!trace_vertex<false>(scn, cfg, p, rec, pending)) {
   }
   out[0] = p.ar;
   out[1] = p.ag;
