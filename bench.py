@@ -332,14 +332,15 @@ def run_b200(args, rank, world, local_rank):
     value = world * n * args.steps / (ms * 1e-3)
 
     # ---- end-to-end through the public API with pinned host buffers ----
+    # the user's call: pinned host f64 rows in, host f32 rgb out; full_forward
+    # streams them through its chunked H2D / kernel / D2H pipeline
     host = [torch.from_numpy(np.ascontiguousarray(a.cpu().numpy())).pin_memory() for a in q_dev]
     y_host = torch.empty((n, 3), dtype=torch.float32).pin_memory()
     e2e_steps = max(3, min(args.steps, 20))
+    y_last = [None]
 
     def e2e_step():
-        dq = [h.to("cuda", non_blocking=True) for h in host]
-        y = full_forward(spec, theta, *dq, precision=PRECISION)
-        y_host.copy_(y, non_blocking=True)
+        y_last[0] = full_forward(spec, theta, *host, precision=PRECISION, out=y_host)
 
     for _ in range(2):
         e2e_step()
@@ -356,7 +357,7 @@ def run_b200(args, rank, world, local_rank):
         dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
     e2e_value = world * n * e2e_steps / (float(e_ms.item()) * 1e-3)
     h2d = int(sum(h.numel() * h.element_size() for h in host))
-    d2h = int(y_host.numel() * 4)
+    d2h = int(y_last[0].numel() * 4)
 
     fb = None
     if not args.no_frame:
@@ -418,7 +419,8 @@ def run_b200(args, rank, world, local_rank):
         "clocks": clocks.summary(),
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-                "path": "paper_2412_04634_b200.mlp.full_forward, pinned host buffers"},
+                "path": "paper_2412_04634_b200.mlp.full_forward on pinned host tensors (chunked "
+                        "H2D / fused kernel / D2H pipeline inside the call)"},
         "gpu_launches": 2 * args.steps,
     }
     if fb is not None:

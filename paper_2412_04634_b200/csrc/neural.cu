@@ -473,11 +473,18 @@ __global__ void k_adam_apply4(float* __restrict__ theta, float* __restrict__ m,
     if (blockIdx.x == 0 && threadIdx.x == 0) skipped[0] += 1;
     return;
   }
-  const int64_t tn = t[0] + 1;  // read before block 0 publishes (see k_adam_tick)
+  // bias corrections once per block (f64 pow, the reference's python float
+  // arithmetic), t read before block 0 publishes (see k_adam_tick)
+  __shared__ float s_bc[2];
+  if (threadIdx.x == 0) {
+    const int64_t tn = t[0] + 1;
+    s_bc[0] = (float)(1.0 - pow(b1, (double)tn));
+    s_bc[1] = (float)(1.0 - pow(b2, (double)tn));
+  }
+  __syncthreads();
   const float c1 = (float)(1.0 - b1);
   const float c2 = (float)(1.0 - b2);
-  const float bc1 = (float)(1.0 - pow(b1, (double)tn));
-  const float bc2 = (float)(1.0 - pow(b2, (double)tn));
+  const float bc1 = s_bc[0], bc2 = s_bc[1];
   const int64_t n4 = n >> 2;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (int64_t i = tid; i < n4; i += (int64_t)gridDim.x * blockDim.x) {

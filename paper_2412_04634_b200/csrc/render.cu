@@ -1111,42 +1111,78 @@ __global__ void k_accumulate(nirc_render_cfg_t cfg, const double* __restrict__ a
 }
 
 // Exclusive scan of per-path record counts (one CTA; count is ~5e4).
-__global__ void k_scan_counts(const int32_t* __restrict__ cnt, int64_t n, int64_t* __restrict__ off,
-                              int64_t* __restrict__ total) {
-  __shared__ int64_t part[1024];
-  const int tid = threadIdx.x;
-  const int64_t per = (n + blockDim.x - 1) / blockDim.x;
-  const int64_t b = tid * per, e = (b + per < n) ? b + per : n;
-  int64_t s = 0;
-  for (int64_t i = b; i < e; ++i) s += cnt[i];
-  part[tid] = s;
+// Exclusive scan of per-path record counts in two levels: k_scan_local
+// scans each 1024-path chunk (warp shuffles) and emits the chunk totals,
+// k_scan_top scans the totals (one warp); the compaction adds the chunk
+// prefix.  Every level is coalesced and fully parallel.
+constexpr int kScanChunk = 1024;
+
+__global__ void k_scan_local(const int32_t* __restrict__ cnt, int64_t n,
+                             int64_t* __restrict__ off, int64_t* __restrict__ chunk_sum) {
+  __shared__ int32_t wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t i = (int64_t)blockIdx.x * kScanChunk + tid;
+  const int32_t v = i < n ? cnt[i] : 0;
+  int32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
   __syncthreads();
-  if (tid == 0) {
-    int64_t run = 0;
-    for (int i = 0; i < (int)blockDim.x; ++i) {
-      const int64_t t = part[i];
-      part[i] = run;
-      run += t;
+  if (w == 0) {
+    int32_t z = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
     }
-    *total = run;
+    wsum[lane] = z;
   }
   __syncthreads();
-  int64_t run = part[tid];
-  for (int64_t i = b; i < e; ++i) {
-    off[i] = run;
-    run += cnt[i];
+  const int32_t incl = x + (w > 0 ? wsum[w - 1] : 0);
+  if (i < n) off[i] = incl - v;
+  if (tid == kScanChunk - 1) chunk_sum[blockIdx.x] = incl;
+}
+
+__global__ void k_scan_top(int64_t* __restrict__ chunk_sum, int64_t nchunks,
+                           int64_t* __restrict__ total) {
+  const int lane = threadIdx.x;
+  int64_t carry = 0;
+  for (int64_t b0 = 0; b0 < nchunks; b0 += 32) {
+    const int64_t b = b0 + lane;
+    const int64_t v = b < nchunks ? chunk_sum[b] : 0;
+    int64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (b < nchunks) chunk_sum[b] = carry + x - v;  // exclusive chunk prefix
+    carry += __shfl_sync(0xffffffffu, x, 31);
   }
+  if (lane == 0) *total = carry;
+}
+
+static inline int scan_counts(const int32_t* cnt, int64_t n, int64_t* off, int64_t* chunk,
+                              int64_t* total, cudaStream_t s) {
+  const int64_t nchunks = (n + kScanChunk - 1) / kScanChunk;
+  k_scan_local<<<(int)nchunks, kScanChunk, 0, s>>>(cnt, n, off, chunk);
+  k_scan_top<<<1, 32, 0, s>>>(chunk, nchunks, total);
+  return cudaGetLastError() == cudaSuccess ? NIRC_OK : NIRC_E_CUDA;
 }
 
 // One warp per path: lanes take the path's vertices (<= 64, two rounds),
 // ballot the kept ones and write them in vertex order at off[p] + rank --
 // the reference's (path, vertex) row order with coalesced stores.
 __global__ void k_compact_records(Stage st, const int64_t* __restrict__ off,
+                                  const int64_t* __restrict__ chunk_pre,
                                   nirc_records_out_t out) {
   const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (p >= st.count) return;
-  int64_t o = off[p];
+  int64_t o = off[p] + chunk_pre[p / kScanChunk];
   const int n = st.nvert[p];
   for (int v0 = 0; v0 < n; v0 += 32) {
     const int v = v0 + lane;
@@ -1246,6 +1282,7 @@ Stage carve_stage(int64_t count, void* base, size_t* bytes) {
   st.nrec = (int32_t*)take(count * 4);
   st.nvert = (int32_t*)take(count * 4);
   take(count * 8);  // offsets
+  take(((count + kScanChunk - 1) / kScanChunk) * 8 + 8);  // chunk prefixes
   st.count = count;
   *bytes = off;
   return st;
@@ -1422,9 +1459,10 @@ extern "C" int nirc_render_collect(const nirc_scene_t* scene, const double* cam,
   if ((st = render_impl(scene, cam, *cfg, spec, theta, img, img2, term, queries_out, w, job, s)))
     return st;
   int64_t* off = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(stg.nvert) + aup(count * 4));
-  k_scan_counts<<<1, 1024, 0, s>>>(stg.nrec, count, off, n_out);
-  NIRC_LAUNCH_CHECK("k_scan_counts");
-  k_compact_records<<<(int)((count * 32 + 255) / 256), 256, 0, s>>>(stg, off, *out);
+  int64_t* chunk = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(off) + aup(count * 8));
+  if ((st = scan_counts(stg.nrec, count, off, chunk, n_out, s))) return st;
+  NIRC_LAUNCH_CHECK("k_scan_*");
+  k_compact_records<<<(int)((count * 32 + 255) / 256), 256, 0, s>>>(stg, off, chunk, *out);
   NIRC_LAUNCH_CHECK("k_compact_records");
   return NIRC_OK;
 }
@@ -1458,11 +1496,12 @@ extern "C" int nirc_collect_range(const nirc_scene_t* scene, const double* cam, 
   st.path0 = path0;
   st.kind = kind;
   int64_t* off = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(st.nvert) + aup(count * 4));
+  int64_t* chunk = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(off) + aup(count * 8));
   k_walk_record<<<(int)((count + 63) / 64), 64, 0, s>>>(*scene, cam, seed, frame, st);
   NIRC_LAUNCH_CHECK("k_walk_record");
-  k_scan_counts<<<1, 1024, 0, s>>>(st.nrec, count, off, n_out);
-  NIRC_LAUNCH_CHECK("k_scan_counts");
-  k_compact_records<<<(int)((count * 32 + 255) / 256), 256, 0, s>>>(st, off, *out);
+  if (scan_counts(st.nrec, count, off, chunk, n_out, s)) return NIRC_E_CUDA;
+  NIRC_LAUNCH_CHECK("k_scan_*");
+  k_compact_records<<<(int)((count * 32 + 255) / 256), 256, 0, s>>>(st, off, chunk, *out);
   NIRC_LAUNCH_CHECK("k_compact_records");
   return NIRC_OK;
 }

@@ -403,8 +403,10 @@ __global__ void k_reduce_grad(nirc_spec_t sp, const float* __restrict__ partials
   for (int pb = blockIdx.x * 32; pb < np; pb += gridDim.x * 32) {
     const int p = pb + lane;
     float s = 0.0f;
-    if (p < np)
+    if (p < np) {
+#pragma unroll 8
       for (int t = t0; t < t1; ++t) s += partials[(int64_t)t * np + p];
+    }
     part[wid][lane] = s;
     __syncthreads();
     if (wid == 0 && p < np) {

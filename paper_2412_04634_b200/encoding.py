@@ -28,6 +28,12 @@ def level_resolutions(levels, base_res, max_res):
     return np.floor(base_res * growth ** np.arange(levels) + 0.5).astype(np.int64)
 
 
+def is_default_layout(spec):
+    """The 12 x 2 hash + 4-band SH input the fused kernels are built for."""
+    return (int(spec.levels) == 12 and int(spec.feats) == 2 and int(spec.bands) == 4
+            and int(spec.in_dim) == 47)
+
+
 def _c_spec(spec):
     return _lib.make_c_spec(spec)
 
