@@ -118,6 +118,10 @@ constexpr int kLinearMaxPrims = 64;
 // 1/det and the products.  Rows of T (48 B per triangle, 16 B aligned):
 //   (v0.xyz, |e1|_1), (e1.xyz, |e2|_1), (e2.xyz, |v0|_1).
 constexpr float kFilterK = 16.0f * 5.9604645e-8f * 1.0001f;  // 16 unit roundoffs
+#ifndef NIRC_FILTER_UNROLL
+#define NIRC_FILTER_UNROLL 1  // measured: 1 < 2 < 4 < 8 (instruction-cache pressure)
+#endif
+constexpr int kFilterUnroll = NIRC_FILTER_UNROLL;
 struct RayF32 {
   float ox, oy, oz, dx, dy, dz, kd, no;  // kd = K * |d|_1, no = |o|_1
 };
@@ -177,7 +181,7 @@ __device__ inline Hit intersect(const nirc_scene_t& s, V3 o, V3 d, double t_max)
     const float f_lo = (float)eps;
     const float f_hi = t_max < 1e29 ? (float)t_max : __int_as_float(0x7f800000);
     uint64_t cand = 0;
-#pragma unroll 4
+#pragma unroll(kFilterUnroll)
     for (int k = 0; k < np; ++k)
       cand |= (uint64_t)tri_candidate(r, T + 3 * k, f_lo, f_hi) << k;
     while (cand) {

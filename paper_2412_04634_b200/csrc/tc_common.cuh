@@ -73,11 +73,15 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes)
                : "memory");
 }
+#ifndef NIRC_MBAR_MODE
+#define NIRC_MBAR_MODE 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
   // try_wait with a suspend-time hint: the warp sleeps in hardware until the
   // phase completes (or ~20 us pass) instead of spinning on issue slots that
   // the other groups of the CTA need.
   uint32_t done = 0;
+#if NIRC_MBAR_MODE == 0
   while (!done) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -87,6 +91,29 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
         : "r"(mbar), "r"(parity), "r"(20000u)
         : "memory");
   }
+#elif NIRC_MBAR_MODE == 1
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(mbar), "r"(parity)
+        : "memory");
+  }
+#else
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(mbar), "r"(parity)
+        : "memory");
+    if (done) break;
+    __nanosleep(NIRC_MBAR_MODE);
+  }
+#endif
 }
 
 // 1-D TMA bulk copy global -> shared, completion counted on an mbarrier.
