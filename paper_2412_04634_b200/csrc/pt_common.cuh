@@ -166,37 +166,13 @@ __device__ inline bool tri_candidate(const RayF32& r, const float4* T, float t_l
   return !(ad > Ed) | !out;  // sign of det uncertain: the exact test decides
 }
 
+// Linear f64 scan (no staged fp32 table) or BVH traversal (spheres, larger
+// scenes) -- the reference's intersect_bvh order; kept out of line.
 template <bool AnyHit>
-__device__ inline Hit intersect(const nirc_scene_t& s, V3 o, V3 d, double t_max) {
+__device__ __noinline__ void bvh_scan(const nirc_scene_t& s, V3 o, V3 d, double& best, int& kind,
+                                      int& prim) {
   const double eps = s.eps;
-  double best = t_max;
-  int kind = -1, prim = -1;
-  if (s.tri_f32 && s.n_sph == 0 && s.n_tri <= kLinearMaxPrims) {
-    // warp-uniform fp32 pre-test over the scan order, then ray_tri (f64,
-    // the reference's arithmetic) on each lane's own candidates in scan
-    // order: the accepted hit (and any-hit boolean) equal the full scan's
-    const int np = s.n_tri;
-    const RayF32 r = ray_f32(o, d);
-    const float4* T = reinterpret_cast<const float4*>(s.tri_f32);
-    const float f_lo = (float)eps;
-    const float f_hi = t_max < 1e29 ? (float)t_max : __int_as_float(0x7f800000);
-    uint64_t cand = 0;
-#pragma unroll(kFilterUnroll)
-    for (int k = 0; k < np; ++k)
-      cand |= (uint64_t)tri_candidate(r, T + 3 * k, f_lo, f_hi) << k;
-    while (cand) {
-      const int k = __ffsll((long long)cand) - 1;
-      cand &= cand - 1;
-      const int pid = s.bvh_prim[k];
-      const double t = ray_tri(o, d, ld3(s.tri_v0, pid), ld3(s.tri_e1, pid), ld3(s.tri_e2, pid));
-      if (t > eps && t < best) {
-        best = t;
-        kind = 0;
-        prim = pid;
-        if (AnyHit) break;
-      }
-    }
-  } else if (s.n_tri + s.n_sph <= kLinearMaxPrims && s.n_sph == 0) {
+  if (s.n_tri + s.n_sph <= kLinearMaxPrims && s.n_sph == 0) {
     const int np = s.n_tri;
     for (int k = 0; k < np; ++k) {
       const int pid = s.bvh_prim[k];
@@ -238,17 +214,49 @@ __device__ inline Hit intersect(const nirc_scene_t& s, V3 o, V3 d, double t_max)
             prim = j;
           }
         }
-        if (AnyHit && kind >= 0) {
-          Hit h;
-          h.kind = kind;
-          return h;
-        }
+        if (AnyHit && kind >= 0) return;
       }
     } else if (count == 0 && s.bvh_a[node] != node) {
       stack[top++] = s.bvh_a[node];
       stack[top++] = node + 1;
     }
   }
+  }
+}
+
+template <bool AnyHit>
+__device__ inline Hit intersect(const nirc_scene_t& s, V3 o, V3 d, double t_max) {
+  const double eps = s.eps;
+  double best = t_max;
+  int kind = -1, prim = -1;
+  if (s.tri_f32 && s.n_sph == 0 && s.n_tri <= kLinearMaxPrims) {
+    // warp-uniform fp32 pre-test over the scan order, then ray_tri (f64,
+    // the reference's arithmetic) on each lane's own candidates in scan
+    // order: the accepted hit (and any-hit boolean) equal the full scan's
+    const int np = s.n_tri;
+    const RayF32 r = ray_f32(o, d);
+    const float4* T = reinterpret_cast<const float4*>(s.tri_f32);
+    const float f_lo = (float)eps;
+    const float f_hi = t_max < 1e29 ? (float)t_max : __int_as_float(0x7f800000);
+    uint64_t cand = 0;
+#pragma unroll(kFilterUnroll)
+    for (int k = 0; k < np; ++k)
+      cand |= (uint64_t)tri_candidate(r, T + 3 * k, f_lo, f_hi) << k;
+    while (cand) {
+      const int k = __ffsll((long long)cand) - 1;
+      cand &= cand - 1;
+      const int pid = s.bvh_prim[k];
+      const double t = ray_tri(o, d, ld3(s.tri_v0, pid), ld3(s.tri_e1, pid), ld3(s.tri_e2, pid));
+      if (t > eps && t < best) {
+        best = t;
+        kind = 0;
+        prim = pid;
+        if (AnyHit) break;
+      }
+    }
+  } else {
+    // general scenes (spheres, > 64 primitives): out of line, see below
+    bvh_scan<AnyHit>(s, o, d, best, kind, prim);
   }
   Hit h;
   h.kind = kind;
@@ -302,12 +310,24 @@ __device__ inline double ggx_g1(double alpha, double cv) {
   return 2.0 * cv / (cv + sqrt(a2 + (1.0 - a2) * cv * cv));
 }
 
+// The conductor (GGX) lobe is kept out of line (__noinline__): scenes of
+// Lambert walls never execute it, and the tracer is instruction-cache bound.
+__device__ __noinline__ V3 ggx_eval(V3 a, double rough, V3 n, V3 wo, V3 wi, double ci,
+                                    double co);
+__device__ __noinline__ double ggx_pdf(double rough, V3 n, V3 wo, V3 wi);
+struct BsdfSample;
+
 // bsdf_eval_s (bsdf.py:38-72)
 __device__ inline V3 bsdf_eval(int kind, V3 a, double rough, V3 n, V3 wo, V3 wi) {
   const double ci = n.x * wi.x + n.y * wi.y + n.z * wi.z;
   const double co = n.x * wo.x + n.y * wo.y + n.z * wo.z;
   if (ci <= 0.0 || co <= 0.0 || kind == MAT_MIRROR) return {0.0, 0.0, 0.0};
   if (kind == MAT_LAMBERT) return {a.x * INV_PI, a.y * INV_PI, a.z * INV_PI};
+  return ggx_eval(a, rough, n, wo, wi, ci, co);
+}
+
+__device__ __noinline__ V3 ggx_eval(V3 a, double rough, V3 n, V3 wo, V3 wi, double ci,
+                                    double co) {
   const double alpha = rough > ALPHA_MIN ? rough : ALPHA_MIN;
   double hx = wi.x + wo.x, hy = wi.y + wo.y, hz = wi.z + wo.z;
   const double hl = sqrt(hx * hx + hy * hy + hz * hz);
@@ -334,6 +354,10 @@ __device__ inline double bsdf_pdf(int kind, double rough, V3 n, V3 wo, V3 wi) {
   const double co = n.x * wo.x + n.y * wo.y + n.z * wo.z;
   if (ci <= 0.0 || co <= 0.0 || kind == MAT_MIRROR) return 0.0;
   if (kind == MAT_LAMBERT) return ci * INV_PI;
+  return ggx_pdf(rough, n, wo, wi);
+}
+
+__device__ __noinline__ double ggx_pdf(double rough, V3 n, V3 wo, V3 wi) {
   const double alpha = rough > ALPHA_MIN ? rough : ALPHA_MIN;
   double hx = wi.x + wo.x, hy = wi.y + wo.y, hz = wi.z + wo.z;
   const double hl = sqrt(hx * hx + hy * hy + hz * hz);
@@ -354,6 +378,9 @@ struct BsdfSample {
   V3 f;
   int delta;
 };
+
+__device__ __noinline__ BsdfSample ggx_sample(int kind, V3 a, double rough, V3 n, V3 wo,
+                                              double u1, double u2);
 
 // bsdf_sample_s (bsdf.py:103-154)
 __device__ inline BsdfSample bsdf_sample(int kind, V3 a, double rough, V3 n, V3 wo, double u1,
@@ -387,6 +414,16 @@ __device__ inline BsdfSample bsdf_sample(int kind, V3 a, double rough, V3 n, V3 
     r.f = {a.x * INV_PI, a.y * INV_PI, a.z * INV_PI};
     return r;
   }
+  return ggx_sample(kind, a, rough, n, wo, u1, u2);
+}
+
+__device__ __noinline__ BsdfSample ggx_sample(int kind, V3 a, double rough, V3 n, V3 wo,
+                                              double u1, double u2) {
+  BsdfSample r;
+  r.wi = {0.0, 0.0, 1.0};
+  r.pdf = 0.0;
+  r.f = {0.0, 0.0, 0.0};
+  r.delta = 0;
   const double alpha = rough > ALPHA_MIN ? rough : ALPHA_MIN;
   const double ch = sqrt((1.0 - u1) / (1.0 + (alpha * alpha - 1.0) * u1));
   const double sh = sqrt(ch < 1.0 ? 1.0 - ch * ch : 0.0);
@@ -409,8 +446,8 @@ __device__ inline BsdfSample bsdf_sample(int kind, V3 a, double rough, V3 n, V3 
 }
 
 // -------------------------------------------------------------- lights --
-// env_eval_s (lights.py:20-58)
-__device__ inline V3 env_eval(const nirc_scene_t& s, V3 d) {
+// env_eval_s (lights.py:20-58); out of line (cold for closed scenes)
+__device__ __noinline__ V3 env_eval(const nirc_scene_t& s, V3 d) {
   if (s.env_kind == ENV_NONE) return {0.0, 0.0, 0.0};
   if (s.env_kind == ENV_CONSTANT) return {s.env_c0[0], s.env_c0[1], s.env_c0[2]};
   if (s.env_kind == ENV_SKY) {
