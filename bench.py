@@ -391,11 +391,26 @@ def run_b200(args, rank, world, local_rank):
     tflops = n * FLOPS_PER_QUERY / (avg_launch_ms * 1e-3) / 1e12
     l2_gbs = n * L2_GATHER_BYTES_PER_QUERY / (avg_launch_ms * 1e-3) / 1e9
     traffic = None
+    prof = {}
     try:
         prof = _json.load(open(os.path.join(ROOT, "profiles", "full_forward_traffic.json")))
         traffic = prof.get("dram_bytes_per_launch")
     except Exception:
         pass
+    csum = clocks.summary()
+    # the binding resource (ncu): the L1TEX data pipe, 1 wavefront / SM / cycle;
+    # wavefronts per query from the committed capture, clock sampled live
+    binding = None
+    if prof.get("lsu_wavefronts_per_query") and csum.get("sm_mhz"):
+        wpq = float(prof["lsu_wavefronts_per_query"])
+        nsm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        ach = (n / (avg_launch_ms * 1e-3)) * wpq / (nsm * csum["sm_mhz"] * 1e6)
+        pk = float(prof.get("lsu_wavefront_peak_per_sm_cycle", 1.0))
+        binding = {"resource": "L1TEX data-pipe wavefronts (scattered hash-table gathers)",
+                   "wavefronts_per_query": wpq, "achieved_per_sm_cycle": ach,
+                   "peak_per_sm_cycle": pk, "frac": ach / pk,
+                   "source": "profiles/full_forward_traffic.json (ncu) + live launch time "
+                             "and SM clock"}
     line = {
         "metric": "nirc_queries_per_sec", "value": value, "unit": "queries/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -415,8 +430,9 @@ def run_b200(args, rank, world, local_rank):
                      "tensor_tflops": tflops,
                      "tensor_frac": tflops / float(peaks.get("bf16_tflops", 1590.0)),
                      "l2_gather_gbs": l2_gbs,
-                     "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback"},
-        "clocks": clocks.summary(),
+                     "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
+                     "binding_resource": binding},
+        "clocks": csum,
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                 "path": "paper_2412_04634_b200.mlp.full_forward on pinned host tensors (chunked "
