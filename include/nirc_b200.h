@@ -215,7 +215,7 @@ int64_t nirc_train_frame_workspace_bytes(const nirc_spec_t* spec,
 /* Multi-GPU split of nirc_train_step (the reference step is
  * caches.py:327-350).  Every rank holds the same records and selects the
  * same batch; rank r runs the fused encode/forward/loss/backward over the
- * 64-row batch tiles [tile_begin, tile_end) of nirc_train_tiles() and writes
+ * 128-row batch tiles [tile_begin, tile_end) of nirc_train_tiles() and writes
  *   grad (theta_len f32, overwritten): its shard's gradient, the loss still
  *        normalised by the GLOBAL batch (losses.py:33-42 divides by B*3);
  *   aux (2 f64): [0] its shard's raw loss sum, [1] 1.0 if a row had pdf <= 0.

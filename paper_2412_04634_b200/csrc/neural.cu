@@ -733,7 +733,7 @@ int launch_fused_train(const nirc_spec_t& sp, const float* theta, const nirc_rec
                        float* grad, float* partials, double* loss_part, double* loss_out,
                        int32_t* flags, int32_t* adam_bad, cudaStream_t s, int64_t tile0,
                        int64_t tile1, int mode);
-constexpr int kFusedTileRows = 64;  // rows per k_train_tile CTA (train_fused.cu kTR)
+constexpr int kFusedTileRows = 128;  // rows per k_train_tile CTA (train_fused.cu kTR)
 }  // namespace nirc
 
 using namespace nirc;
@@ -927,7 +927,7 @@ TrainWs carve_train(const nirc_spec_t& sp, int64_t n, int64_t B, int steps, void
   w.grad = (float*)take(sp.theta_len * 4);
   w.partial = (double*)take((B / kLossThreads + 2) * 3 * 8);
   w.adam_bad = (int32_t*)take(16);
-  const int64_t ntiles = (B + 63) / 64;
+  const int64_t ntiles = (B + kFusedTileRows - 1) / kFusedTileRows;
   w.fpart = (float*)take(ntiles * (sp.theta_len - sp.grid_len) * 4);
   w.floss = (double*)take(ntiles * 8);
   w.bytes = off;

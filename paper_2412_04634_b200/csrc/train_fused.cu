@@ -1,33 +1,42 @@
 // Fused online-training step (train_frame body, pkg/src/nirclab/caches.py:
-// 330-350) for the l2 / relative-L2 losses: ONE kernel per optimizer step
-// runs, per 64-row tile of the batch,
-//   encode (bit-exact, encoding.py:111-157) -> forward with pre-activation
-//   stash (mlp.py:102-122) -> loss gradient (losses.py:23-42, f64) ->
-//   backward (mlp.py:125-154, ReLU' = z >= 0) -> hash-grid scatter
-//   (encoding.py:160-167) straight from registers,
-// keeping every activation in shared memory.  Weight/bias gradients are
-// written as per-CTA partials and summed in a fixed order by k_reduce_grad
-// (deterministic), which also folds the loss, flags a non-finite loss
-// (DivergenceError) or gradient (Adam skip) and feeds the dense Adam kernels.
+// 330-350) for the l2 / relative-L2 losses: ONE kernel per optimizer step,
+// one CTA of 128 threads per 128-row tile of the batch, one thread per row:
+//   encode (bit-exact, encoding.py:111-157) -> forward (mlp.py:102-122) ->
+//   loss gradient (losses.py:23-42, f64) -> backward (mlp.py:125-154,
+//   ReLU' = z >= 0) -> hash-grid scatter (encoding.py:160-167).
+// Each thread keeps its row's layer outputs / input gradients in registers
+// (64 accumulators: long independent FMA chains) and reads the weights as
+// broadcast 16-byte shared-memory rows (W^T for the forward, W for the
+// backward); every layer's pre-activations and the encoded input are stashed
+// in TENSOR memory (the thread's own TMEM lane, 4 x 64 + 48 columns) instead
+// of shared memory, which leaves room for both weight images and keeps the
+// whole batch in one wave (B / 128 = 128 CTAs on 148 SMs).  Weight/bias
+// gradients are per-CTA partials from a shared-memory block GEMM over the
+// tile's rows, summed in a fixed order by k_reduce_grad (deterministic); the
+// hash-grid scatter is the one atomic (non-deterministic) sum.
 //
-// fp32 SIMT, register-blocked 4x4 micro-tiles: all GEMMs here are 64 wide
-// and the batch is 16384 rows, so the step is latency- not FLOP-bound.
+// fp32 SIMT: the reference's accuracy class.
 #include <cmath>
 #include "common.cuh"
+#include "tc_common.cuh"
 
 namespace nirc {
 
-constexpr int kTR = 64;          // rows per tile
-constexpr int kTT = 256;         // threads per CTA
-constexpr int kLDR = 68;         // row stride of [feature][row] arrays (68/4 odd)
+constexpr int kTR = 128;         // rows per tile
+constexpr int kTT = 256;         // threads per CTA: two per row (output halves)
+constexpr int kLD2 = 132;        // row stride of the [feature][row] staging arrays
 constexpr int kMaxW = 64;        // widest layer supported by the fused path
+constexpr int kMaxNL = 8;
 
 struct FusedLayout {
-  int nl, din[8], dout[8], ldw[8];
-  int woff[8], boff[8];          // float offsets in the smem weight block
-  int wfloats;                   // weight block size (floats)
-  int x_off, z_off[8], dz_off[2], dy_off, red_off, total_floats;
+  int nl, din[kMaxNL], dout[kMaxNL];
+  int ldw[kMaxNL], ldt[kMaxNL];    // row strides of W (dout x ldw) and W^T (din x ldt)
+  int w_off[kMaxNL], t_off[kMaxNL], b_off[kMaxNL];  // float offsets in smem
+  int dz_off, a_off, red_off, total_floats;
+  int x_col, tmem_cols;            // TMEM: z of layer l at cols 64*l, X at x_col
 };
+
+__host__ __device__ inline int up4(int x) { return (x + 3) & ~3; }
 
 __host__ __device__ inline FusedLayout fused_layout(const nirc_spec_t& sp) {
   FusedLayout L{};
@@ -36,166 +45,133 @@ __host__ __device__ inline FusedLayout fused_layout(const nirc_spec_t& sp) {
   for (int l = 0; l < sp.n_layers; ++l) {
     L.din[l] = sp.dims[l];
     L.dout[l] = sp.dims[l + 1];
-    L.ldw[l] = sp.dims[l] | 1;  // odd stride: strided-column loads hit distinct banks
-    L.woff[l] = off;
-    off += L.dout[l] * L.ldw[l];
-    L.boff[l] = off;
-    off += (L.dout[l] + 3) & ~3;
+    L.ldw[l] = up4(L.din[l]);
+    L.ldt[l] = up4(L.dout[l]);
+    L.w_off[l] = off;
+    off += up4(L.dout[l]) * L.ldw[l];
+    L.t_off[l] = off;
+    off += up4(L.din[l]) * L.ldt[l];
+    L.b_off[l] = off;
+    off += kMaxW;
   }
-  L.wfloats = (off + 3) & ~3;
-  int f = L.wfloats;
-  L.x_off = f;
-  f += sp.in_dim * kLDR;
-  for (int l = 0; l < sp.n_layers; ++l) {
-    L.z_off[l] = f;
-    f += L.dout[l] * kLDR;
-  }
-  L.dz_off[0] = f;
-  f += kMaxW * kLDR;
-  L.dz_off[1] = f;
-  f += kMaxW * kLDR;
-  L.dy_off = f;
-  f += 4 * kLDR;
-  L.red_off = f;
-  f += kTT * 2;  // f64 reduction scratch (as 2 floats each)
-  L.total_floats = f;
+  L.dz_off = off;
+  off += kMaxW * kLD2;
+  L.a_off = off;
+  off += kMaxW * kLD2;
+  L.red_off = off;
+  off += 2 * kTT;  // f64 reduction scratch
+  L.total_floats = off;
+  L.x_col = (sp.n_layers - 1) * 64;
+  int need = L.x_col + 64;
+  int c = 32;
+  while (c < need) c <<= 1;
+  L.tmem_cols = c;
   return L;
 }
 
 bool fused_supported(const nirc_spec_t& sp) {
-  if (sp.n_layers > 8 || sp.in_dim > kMaxW || sp.feats != 2) return false;
-  for (int l = 1; l <= sp.n_layers; ++l)
+  if (sp.n_layers < 2 || sp.n_layers > kMaxNL || sp.in_dim > kMaxW || sp.feats != 2 ||
+      sp.levels > 12)
+    return false;
+  for (int l = 1; l < sp.n_layers; ++l)
     if (sp.dims[l] > kMaxW) return false;
-  return sp.dims[sp.n_layers] <= 4;
+  if (sp.dims[sp.n_layers] > 4) return false;
+  return fused_layout(sp).tmem_cols <= 512;
 }
 
-__device__ inline float act_hidden(float z) { return z > 0.0f ? z : 0.0f; }
+size_t fused_smem_bytes(const nirc_spec_t& sp) {
+  return (size_t)fused_layout(sp).total_floats * 4 + 16;
+}
 
-// out[j][r] (+)= sum_i in[i][r] * W[j][i] (+ b[j]) over a 64-row tile.
-// Thread (rg, cg): rows 4rg..4rg+3, outputs cg + 16q.  `relu_in` applies
-// max(.,0) to the stashed pre-activations on the fly.
-__device__ inline void tile_gemm_fwd(const float* __restrict__ in, int din, bool relu_in,
-                                     const float* __restrict__ W, int ldw,
-                                     const float* __restrict__ b, int dout,
-                                     float* __restrict__ out) {
-  const int tid = threadIdx.x, rg = tid >> 4, cg = tid & 15;
-  float acc[4][4];
+__device__ __forceinline__ float relu(float z) { return z > 0.0f ? z : 0.0f; }
+
+// Thread (r, h): row r of the tile, output half h (columns 32h .. 32h+31).
+constexpr int kHalf = 32;
+
+// out[j] = b[c0 + j] + sum_i in[i][r] * W[c0 + j][i], j < NOUT, c0 = column
+// offset; the input column read from the staging array, W^T row segments as
+// broadcast float4.
+template <int NOUT>
+__device__ __forceinline__ void row_forward(const float* __restrict__ in, int din,
+                                            const float* __restrict__ WT, int ldt, int c0,
+                                            const float* __restrict__ b, int r, float* out) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
-#pragma unroll
-    for (int r = 0; r < 4; ++r) acc[q][r] = 0.0f;
+  for (int j = 0; j < NOUT; ++j) out[j] = b[c0 + j];
+#pragma unroll 2
   for (int i = 0; i < din; ++i) {
-    float4 a = *reinterpret_cast<const float4*>(in + i * kLDR + 4 * rg);
-    if (relu_in) {
-      a.x = act_hidden(a.x);
-      a.y = act_hidden(a.y);
-      a.z = act_hidden(a.z);
-      a.w = act_hidden(a.w);
-    }
+    const float ai = in[i * kLD2 + r];
+    const float4* w = reinterpret_cast<const float4*>(WT + i * ldt + c0);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int j = cg + 16 * q;
-      const float w = j < dout ? W[j * ldw + i] : 0.0f;
-      acc[q][0] = fmaf(a.x, w, acc[q][0]);
-      acc[q][1] = fmaf(a.y, w, acc[q][1]);
-      acc[q][2] = fmaf(a.z, w, acc[q][2]);
-      acc[q][3] = fmaf(a.w, w, acc[q][3]);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int j = cg + 16 * q;
-    if (j < dout) {
-      const float bj = b[j];
-      float4 o;
-      o.x = acc[q][0] + bj;
-      o.y = acc[q][1] + bj;
-      o.z = acc[q][2] + bj;
-      o.w = acc[q][3] + bj;
-      *reinterpret_cast<float4*>(out + j * kLDR + 4 * rg) = o;
+    for (int q = 0; q < NOUT / 4; ++q) {
+      const float4 v = w[q];
+      out[4 * q] = fmaf(ai, v.x, out[4 * q]);
+      out[4 * q + 1] = fmaf(ai, v.y, out[4 * q + 1]);
+      out[4 * q + 2] = fmaf(ai, v.z, out[4 * q + 2]);
+      out[4 * q + 3] = fmaf(ai, v.w, out[4 * q + 3]);
     }
   }
 }
 
-// da[i][r] = sum_j dz[j][r] W[j][i]; optionally masked by (z_prev[i][r] >= 0).
-__device__ inline void tile_gemm_bwd(const float* __restrict__ dz, int dout,
-                                     const float* __restrict__ W, int ldw, int din,
-                                     const float* __restrict__ zprev, float* __restrict__ out) {
-  const int tid = threadIdx.x, rg = tid >> 4, ig = tid & 15;
-  float acc[4][4];
+// da[i] = sum_j dz[j][r] * W[j][c0 + i], i < NIN.
+template <int NIN>
+__device__ __forceinline__ void row_backward(const float* __restrict__ dz, int dout,
+                                             const float* __restrict__ W, int ldw, int c0, int r,
+                                             float* da) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
-#pragma unroll
-    for (int r = 0; r < 4; ++r) acc[q][r] = 0.0f;
+  for (int i = 0; i < NIN; ++i) da[i] = 0.0f;
+#pragma unroll 2
   for (int j = 0; j < dout; ++j) {
-    const float4 g = *reinterpret_cast<const float4*>(dz + j * kLDR + 4 * rg);
+    const float g = dz[j * kLD2 + r];
+    const float4* w = reinterpret_cast<const float4*>(W + j * ldw + c0);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int i = ig + 16 * q;
-      const float w = i < din ? W[j * ldw + i] : 0.0f;
-      acc[q][0] = fmaf(g.x, w, acc[q][0]);
-      acc[q][1] = fmaf(g.y, w, acc[q][1]);
-      acc[q][2] = fmaf(g.z, w, acc[q][2]);
-      acc[q][3] = fmaf(g.w, w, acc[q][3]);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int i = ig + 16 * q;
-    if (i < din) {
-      float4 o = make_float4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
-      if (zprev) {
-        const float4 z = *reinterpret_cast<const float4*>(zprev + i * kLDR + 4 * rg);
-        o.x = z.x >= 0.0f ? o.x : 0.0f;
-        o.y = z.y >= 0.0f ? o.y : 0.0f;
-        o.z = z.z >= 0.0f ? o.z : 0.0f;
-        o.w = z.w >= 0.0f ? o.w : 0.0f;
-      }
-      *reinterpret_cast<float4*>(out + i * kLDR + 4 * rg) = o;
+    for (int q = 0; q < NIN / 4; ++q) {
+      const float4 v = w[q];
+      da[4 * q] = fmaf(g, v.x, da[4 * q]);
+      da[4 * q + 1] = fmaf(g, v.y, da[4 * q + 1]);
+      da[4 * q + 2] = fmaf(g, v.z, da[4 * q + 2]);
+      da[4 * q + 3] = fmaf(g, v.w, da[4 * q + 3]);
     }
   }
 }
 
-// Per-CTA partial dW[j][i] = sum_r dz[j][r] a[i][r] and db[j] = sum_r dz[j][r].
-__device__ inline void tile_wgrad(const float* __restrict__ dz, int dout,
-                                  const float* __restrict__ a, bool relu_a, int din, int nrows,
-                                  float* __restrict__ part_w, float* __restrict__ part_b) {
+// Per-CTA partial dW[j][i] = sum_r dz[j][r] a[i][r], db[j] = sum_r dz[j][r]:
+// 256 threads as a 16 x 16 grid over the 64 x 64 outputs, 4 x 4 each, rows
+// in float4 steps.
+__device__ __forceinline__ void tile_wgrad(const float* __restrict__ dz, int dout,
+                                           const float* __restrict__ a, int din,
+                                           float* __restrict__ part_w,
+                                           float* __restrict__ part_b) {
   const int tid = threadIdx.x, jg = tid >> 4, ig = tid & 15;
   float acc[4][4];
 #pragma unroll
   for (int p = 0; p < 4; ++p)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[p][q] = 0.0f;
-  for (int r = 0; r < nrows; r += 4) {
-    float4 g[4], x[4];
+  if (jg < dout) {
+    for (int r = 0; r < kTR; r += 4) {
+      float4 g[4], x[4];
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const int j = jg + 16 * p;
-      g[p] = j < dout ? *reinterpret_cast<const float4*>(dz + j * kLDR + r)
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int i = ig + 16 * q;
-      float4 v = i < din ? *reinterpret_cast<const float4*>(a + i * kLDR + r)
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
-      if (relu_a) {
-        v.x = act_hidden(v.x);
-        v.y = act_hidden(v.y);
-        v.z = act_hidden(v.z);
-        v.w = act_hidden(v.w);
+      for (int p = 0; p < 4; ++p) {
+        const int j = jg + 16 * p;
+        g[p] = j < dout ? *reinterpret_cast<const float4*>(dz + j * kLD2 + r)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      x[q] = v;
-    }
-#pragma unroll
-    for (int p = 0; p < 4; ++p)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        acc[p][q] = fmaf(g[p].x, x[q].x, acc[p][q]);
-        acc[p][q] = fmaf(g[p].y, x[q].y, acc[p][q]);
-        acc[p][q] = fmaf(g[p].z, x[q].z, acc[p][q]);
-        acc[p][q] = fmaf(g[p].w, x[q].w, acc[p][q]);
+        const int i = ig + 16 * q;
+        x[q] = i < din ? *reinterpret_cast<const float4*>(a + i * kLD2 + r)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
       }
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          acc[p][q] = fmaf(g[p].x, x[q].x, acc[p][q]);
+          acc[p][q] = fmaf(g[p].y, x[q].y, acc[p][q]);
+          acc[p][q] = fmaf(g[p].z, x[q].z, acc[p][q]);
+          acc[p][q] = fmaf(g[p].w, x[q].w, acc[p][q]);
+        }
+    }
   }
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
@@ -209,97 +185,136 @@ __device__ inline void tile_wgrad(const float* __restrict__ dz, int dout,
   }
   if (tid < dout) {
     float s = 0.0f;
-    for (int r = 0; r < nrows; ++r) s += dz[tid * kLDR + r];
+    for (int r = 0; r < kTR; ++r) s += dz[tid * kLD2 + r];
     part_b[tid] = s;
   }
 }
 
-// One 64-row tile of the batch per CTA.  rec rows idx[tile*64 + r].
+// 32 TMEM columns of this thread's lane <-> v[32]
+__device__ __forceinline__ void tmem_put32(uint32_t taddr, const float* v) {
+  tc::tmem_st16(taddr, v);
+  tc::tmem_st16(taddr + 16, v + 16);
+}
+__device__ __forceinline__ void tmem_get32(uint32_t taddr, float* v) {
+  tc::tmem_ld32(taddr, v);
+  tc::tmem_wait_ld();
+}
+
+// One 128-row tile of the batch per CTA (tiles tile0 + blockIdx.x); rows
+// idx[tile*128 + r]; thread (r, h) = (tid & 127, tid >> 7).
 __global__ void __launch_bounds__(kTT, 1)
     k_train_tile(nirc_spec_t sp, FusedLayout L, const float* __restrict__ theta,
                  nirc_records_t rec, const int64_t* __restrict__ idx, int64_t B, int loss_kind,
                  double loss_eps, float* __restrict__ grad, float* __restrict__ partials,
                  double* __restrict__ loss_part, int32_t* __restrict__ flags, int64_t tile0) {
   extern __shared__ __align__(16) float fsm[];
+  __shared__ uint32_t tmem_holder;
   if (flags[0] & 3) return;
   const int tid = threadIdx.x;
-  const int64_t row0 = (tile0 + blockIdx.x) * kTR;
-  const int nrows = (int)((B - row0) < kTR ? (B - row0) : kTR);
-  // ---- stage the network (odd-stride rows) ---------------------------------
+  const int r = tid & (kTR - 1), h = tid >> 7;
+  const int c0 = kHalf * h;
+  const int lane_base = ((tid >> 5) & 3) * 32;
+  const int64_t row = (tile0 + blockIdx.x) * kTR + r;
+  const bool live = row < B;
+  // ---- weights: W (dout x ldw) and W^T (din x ldt), zero padded ----------
   for (int l = 0; l < L.nl; ++l) {
     const float* Wg = theta + sp.w_off[l];
-    for (int e = tid; e < L.dout[l] * L.din[l]; e += kTT) {
-      const int j = e / L.din[l], i = e % L.din[l];
-      fsm[L.woff[l] + j * L.ldw[l] + i] = Wg[e];
+    const int din = L.din[l], dout = L.dout[l];
+    for (int e = tid; e < up4(dout) * L.ldw[l]; e += kTT) {
+      const int j = e / L.ldw[l], i = e - j * L.ldw[l];
+      fsm[L.w_off[l] + e] = (j < dout && i < din) ? Wg[j * din + i] : 0.0f;
     }
-    for (int j = tid; j < L.dout[l]; j += kTT) fsm[L.boff[l] + j] = theta[sp.b_off[l] + j];
+    for (int e = tid; e < up4(din) * L.ldt[l]; e += kTT) {
+      const int i = e / L.ldt[l], j = e - i * L.ldt[l];
+      fsm[L.t_off[l] + e] = (j < dout && i < din) ? Wg[j * din + i] : 0.0f;
+    }
+    for (int j = tid; j < kMaxW; j += kTT)
+      fsm[L.b_off[l] + j] = j < dout ? theta[sp.b_off[l] + j] : 0.0f;
   }
-  // ---- encode: thread (row r, part p) does levels 3p..3p+2; p == 0 also SH+aux
-  const int r = tid & 63, part = tid >> 6;
-  float* X = fsm + L.x_off;
-  LevelCell cells[3];
-  const bool live = r < nrows;
-  int64_t ri = 0;
+  if (tid < 32) tc::tmem_alloc(tc::smem_u32(&tmem_holder), (uint32_t)L.tmem_cols);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = tmem_holder + ((uint32_t)lane_base << 16);
+  float* A = fsm + L.a_off;   // [feature][row]: the current layer's input
+  float* DZ = fsm + L.dz_off;
+  // ---- encode (bit-exact): levels 6h .. 6h+5; h == 0 also SH + aux --------
   const uint32_t T = 1u << sp.table_log2;
+  int64_t ri = 0;
+  float ux = 0.0f, uy = 0.0f, uz = 0.0f;
   if (live) {
-    ri = idx[row0 + r];
+    ri = idx[row];
     const double* p = rec.pos + 3 * ri;
-    const float ux = norm_coord(p[0], sp.bb_min[0], sp.bb_inv[0]);
-    const float uy = norm_coord(p[1], sp.bb_min[1], sp.bb_inv[1]);
-    const float uz = norm_coord(p[2], sp.bb_min[2], sp.bb_inv[2]);
+    ux = norm_coord(p[0], sp.bb_min[0], sp.bb_inv[0]);
+    uy = norm_coord(p[1], sp.bb_min[1], sp.bb_inv[1]);
+    uz = norm_coord(p[2], sp.bb_min[2], sp.bb_inv[2]);
+  }
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const int lvl = 3 * part + q;
-      if (lvl < sp.levels) {
-        cells[q] = level_cell(ux, uy, uz, sp.res[lvl]);
-        const float2 f = level_features2(theta + (size_t)lvl * T * 2, cells[q], T - 1u);
-        X[(2 * lvl) * kLDR + r] = f.x;
-        X[(2 * lvl + 1) * kLDR + r] = f.y;
+  for (int q = 0; q < 6; ++q) {
+    const int lvl = 6 * h + q;
+    if (lvl < sp.levels) {
+      float2 f = make_float2(0.0f, 0.0f);
+      if (live) {
+        const LevelCell c = level_cell(ux, uy, uz, sp.res[lvl]);
+        f = level_features2(theta + (size_t)lvl * T * 2, c, T - 1u);
       }
+      A[(2 * lvl) * kLD2 + r] = f.x;
+      A[(2 * lvl + 1) * kLD2 + r] = f.y;
     }
-    if (part == 0) {
-      const int g = sp.levels * 2;
+  }
+  if (h == 0) {
+    const int g = sp.levels * 2;
+    if (live) {
       const double* d = rec.dirs + 3 * ri;
       sh_eval<true>(d[0], d[1], d[2], sp.bands, sp.sh_k,
-                    [&](int i, double v) { X[(g + i) * kLDR + r] = __double2float_rn(v); });
+                    [&](int i, double v) { A[(g + i) * kLD2 + r] = __double2float_rn(v); });
       const int a0 = g + sp.bands * sp.bands;
       const double* nn = rec.ns + 3 * ri;
       const double* al = rec.alb + 3 * ri;
       for (int c = 0; c < 3; ++c) {
-        X[(a0 + c) * kLDR + r] = __double2float_rn(dmul(dadd(nn[c], 1.0), 0.5));
-        X[(a0 + 3 + c) * kLDR + r] = __double2float_rn(al[c]);
+        A[(a0 + c) * kLD2 + r] = __double2float_rn(dmul(dadd(nn[c], 1.0), 0.5));
+        A[(a0 + 3 + c) * kLD2 + r] = __double2float_rn(al[c]);
       }
-      X[(a0 + 6) * kLDR + r] = __double2float_rn(rec.rough[ri]);
+      A[(a0 + 6) * kLD2 + r] = __double2float_rn(rec.rough[ri]);
+    } else {
+      for (int i = g; i < sp.in_dim; ++i) A[i * kLD2 + r] = 0.0f;
     }
-  } else if (part == 0) {
-    for (int i = 0; i < sp.in_dim; ++i) X[i * kLDR + r] = 0.0f;
   }
   __syncthreads();
-  // ---- forward, stashing every pre-activation -----------------------------
+  {  // the encoded row -> TMEM (layer 0's a_prev for its weight gradient)
+    float x[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x[i] = (c0 + i) < sp.in_dim ? A[(c0 + i) * kLD2 + r] : 0.0f;
+    tmem_put32(tbase + L.x_col + c0, x);
+  }
+  // ---- forward: hidden layers stash z in TMEM, write relu(z) as next input
   const int NL = L.nl;
-  for (int l = 0; l < NL; ++l) {
-    const float* in = l == 0 ? X : fsm + L.z_off[l - 1];
-    tile_gemm_fwd(in, L.din[l], l > 0, fsm + L.woff[l], L.ldw[l], fsm + L.boff[l], L.dout[l],
-                  fsm + L.z_off[l]);
+  for (int l = 0; l < NL - 1; ++l) {
+    float z[kHalf];
+    row_forward<kHalf>(A, L.din[l], fsm + L.t_off[l], L.ldt[l], c0, fsm + L.b_off[l], r, z);
+    tmem_put32(tbase + 64 * l + c0, z);
+    __syncthreads();  // both halves finished reading this layer's input
+#pragma unroll
+    for (int j = 0; j < kHalf; ++j) A[(c0 + j) * kLD2 + r] = relu(z[j]);
     __syncthreads();
   }
-  // ---- loss gradient (f64, the reference's promotions) --------------------
+  float y[4];
+  row_forward<4>(A, L.din[NL - 1], fsm + L.t_off[NL - 1], L.ldt[NL - 1], 0, fsm + L.b_off[NL - 1],
+                 r, y);
+  tc::tmem_wait_st();
+  // ---- loss gradient (f64, the reference's promotions), half 0 ------------
   const int dout = L.dout[NL - 1];
-  const float* zo = fsm + L.z_off[NL - 1];
-  float* dz = fsm + L.dz_off[0];
   double lsum = 0.0;
-  if (tid < kTR) {
-    const int rr = tid;
-    if (rr < nrows) {
-      const int64_t rj = idx[row0 + rr];
-      const double pdf = rec.pdf[rj];
+  if (h == 0) {
+    if (live) {
+      const double pdf = rec.pdf[ri];
       if (!(pdf > 0.0)) atomicOr(flags, 1);
       const double n_total = (double)(B * 3);
       for (int j = 0; j < dout; ++j) {
-        const float z = zo[j * kLDR + rr];
+        const float z = y[j];
         const float yf = sp.out_act == 0 ? (z > 0.0f ? z : 0.0f) : 1.0f / (1.0f + expf(-z));
-        const double y = (double)yf, t = rec.target[3 * rj + j];
-        const double diff = dsub(y, t);
+        const double yd = (double)yf, t = rec.target[3 * ri + j];
+        const double diff = dsub(yd, t);
         double g, v;
         if (loss_kind == 0) {
           v = ddiv(dmul(diff, diff), pdf);
@@ -312,71 +327,70 @@ __global__ void __launch_bounds__(kTT, 1)
         }
         lsum += v;
         const float gf = __double2float_rn(g);
-        float gz;
-        if (sp.out_act == 0) gz = z >= 0.0f ? gf : 0.0f;
-        else gz = gf * yf * (1.0f - yf);
-        dz[j * kLDR + rr] = gz;
+        DZ[j * kLD2 + r] = sp.out_act == 0 ? (z >= 0.0f ? gf : 0.0f) : gf * yf * (1.0f - yf);
       }
     } else {
-      for (int j = 0; j < dout; ++j) dz[j * kLDR + rr] = 0.0f;
+      for (int j = 0; j < dout; ++j) DZ[j * kLD2 + r] = 0.0f;
     }
   }
-  // deterministic per-tile loss partial (tree over the 64 row threads)
+  // deterministic per-tile loss partial (tree over the threads)
   double* red = reinterpret_cast<double*>(fsm + L.red_off);
   red[tid] = lsum;
   __syncthreads();
-  for (int s = kTT / 2; s > 0; s >>= 1) {
-    if (tid < s) red[tid] += red[tid + s];
+  for (int st = kTT / 2; st > 0; st >>= 1) {
+    if (tid < st) red[tid] += red[tid + st];
     __syncthreads();
   }
   if (tid == 0) loss_part[blockIdx.x] = red[0];
   // ---- backward ----------------------------------------------------------
   float* wpart = partials + (int64_t)blockIdx.x * (sp.theta_len - sp.grid_len);
-  int cur = 0;
-  float dX[3][2];
+  float dX[12];
   for (int l = NL - 1; l >= 0; --l) {
-    float* dzc = fsm + L.dz_off[cur];
-    const float* a_prev = l == 0 ? X : fsm + L.z_off[l - 1];
-    tile_wgrad(dzc, L.dout[l], a_prev, l > 0, L.din[l], kTR,
-               wpart + (sp.w_off[l] - sp.grid_len), wpart + (sp.b_off[l] - sp.grid_len));
-    if (l > 0) {
-      tile_gemm_bwd(dzc, L.dout[l], fsm + L.woff[l], L.ldw[l], L.din[l], fsm + L.z_off[l - 1],
-                    fsm + L.dz_off[1 - cur]);
-      __syncthreads();
-      cur = 1 - cur;
-    } else {
-      // dX for the hash-grid block only: thread (r, part) needs its 3 levels
-      const float* W0 = fsm + L.woff[0];
+    {  // a_prev of layer l -> staging (relu(z_{l-1}) or the encoded input)
+      float v[32];
+      tmem_get32(tbase + (l == 0 ? L.x_col : 64 * (l - 1)) + c0, v);
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        const int lvl = 3 * part + q;
-        float s0 = 0.0f, s1 = 0.0f;
-        if (lvl < sp.levels)
-          for (int j = 0; j < L.dout[0]; ++j) {
-            const float g = dzc[j * kLDR + r];
-            s0 = fmaf(g, W0[j * L.ldw[0] + 2 * lvl], s0);
-            s1 = fmaf(g, W0[j * L.ldw[0] + 2 * lvl + 1], s1);
-          }
-        dX[q][0] = s0;
-        dX[q][1] = s1;
+      for (int i = 0; i < 32; ++i)
+        if (c0 + i < L.din[l]) A[(c0 + i) * kLD2 + r] = l == 0 ? v[i] : relu(v[i]);
+    }
+    __syncthreads();  // DZ (layer l's dz) and A complete for the block GEMM
+    tile_wgrad(DZ, L.dout[l], A, L.din[l], wpart + (sp.w_off[l] - sp.grid_len),
+               wpart + (sp.b_off[l] - sp.grid_len));
+    if (l > 0) {
+      float da[kHalf];
+      row_backward<kHalf>(DZ, L.dout[l], fsm + L.w_off[l], L.ldw[l], c0, r, da);
+      float zp[32];
+      tmem_get32(tbase + 64 * (l - 1) + c0, zp);
+      __syncthreads();  // everyone finished reading DZ / A of layer l
+#pragma unroll
+      for (int i = 0; i < kHalf; ++i) DZ[(c0 + i) * kLD2 + r] = zp[i] >= 0.0f ? da[i] : 0.0f;
+    } else {
+      row_backward<12>(DZ, L.dout[0], fsm + L.w_off[0], L.ldw[0], 12 * h, r, dX);
+    }
+  }
+  // ---- hash-grid scatter (encoding.py:160-167), levels 6h .. 6h+5 ---------
+  if (live) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const int lvl = 6 * h + q;
+      if (lvl >= sp.levels) continue;
+      const LevelCell c = level_cell(ux, uy, uz, sp.res[lvl]);
+      float* gl = grad + (size_t)lvl * T * 2;
+      const float d0 = dX[2 * q], d1 = dX[2 * q + 1];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float w = corner_weight(c, k);
+        const uint32_t hh = corner_hash(c, k, T - 1u);
+        if (d0 != 0.0f) atomicAdd(gl + 2 * hh, __fmul_rn(w, d0));
+        if (d1 != 0.0f) atomicAdd(gl + 2 * hh + 1, __fmul_rn(w, d1));
       }
     }
   }
-  // ---- hash-grid scatter (encoding.py:160-167) from registers -------------
-  if (live) {
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const int lvl = 3 * part + q;
-      if (lvl >= sp.levels) continue;
-      float* gl = grad + (size_t)lvl * T * 2;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float w = corner_weight(cells[q], k);
-        const uint32_t h = corner_hash(cells[q], k, T - 1u);
-        if (dX[q][0] != 0.0f) atomicAdd(gl + 2 * h, __fmul_rn(w, dX[q][0]));
-        if (dX[q][1] != 0.0f) atomicAdd(gl + 2 * h + 1, __fmul_rn(w, dX[q][1]));
-      }
-    }
+  tc::fence_before();
+  __syncthreads();
+  if (tid < 32) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem_holder, (uint32_t)L.tmem_cols);
   }
 }
 
@@ -439,9 +453,6 @@ __global__ void k_reduce_grad(nirc_spec_t sp, const float* __restrict__ partials
   }
 }
 
-size_t fused_smem_bytes(const nirc_spec_t& sp) {
-  return (size_t)fused_layout(sp).total_floats * 4;
-}
 
 // Tiles [tile0, tile1) of the batch (all of it on one GPU; one shard of it
 // per GPU in the multi-GPU frame, mode 1).

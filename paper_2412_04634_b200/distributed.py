@@ -14,7 +14,7 @@ sample, dim) (pkg/src/nirclab/rng.py:59-106), so a frame partitions exactly:
   P_TRAIN, frame, p, 0)); the records are all-gathered in rank order, which
   reproduces the reference's path-major row order exactly.
 * train   -- every rank selects the same batch (caches.py:327-329) and runs
-  the fused encode/forward/loss/backward over its share of the 64-row batch
+  the fused encode/forward/loss/backward over its share of the 128-row batch
   tiles; the flat gradient (theta_len f32) and [loss sum, bad-pdf] are
   summed with one all-reduce each; every rank then runs the identical dense
   Adam, so the cache replicas stay bit-identical (all-reduce results are

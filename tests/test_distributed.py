@@ -23,7 +23,7 @@ import torch.multiprocessing as mp
 import nirc_oracle as O
 from paper_2412_04634_b200 import distributed as D
 
-TILE = 64
+TILE = 128  # rows per fused training tile (train_fused.cu kTR)
 
 
 def test_split_range_partitions():

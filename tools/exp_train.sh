@@ -1,8 +1,8 @@
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" || exit 1
-timeout 1200 python -m pytest tests/test_gpu_neural.py tests/test_gpu_distributed.py -q -x 2>&1 | tail -2
+timeout 1200 python -m pytest tests -q -x -m gpu 2>&1 | tail -3
 for rep in 1 2; do
 timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --frame-steps 10 --no-extra-frames | python -c "
 import json,sys; d=json.load(sys.stdin); f=d['frame_1080p']
-print({k:round(f[k],3) for k in ('value','render_collect_ms','train_ms')})"
+print({k:round(f[k],3) for k in ('value','render_collect_ms','train_ms','train_samples_per_sec')})"
 done
