@@ -1,19 +1,20 @@
 // Fused online-training step (train_frame body, pkg/src/nirclab/caches.py:
 // 330-350) for the l2 / relative-L2 losses: ONE kernel per optimizer step,
-// one CTA of 128 threads per 128-row tile of the batch, one thread per row:
+// one CTA of 512 threads per 128-row tile of the batch, four threads per row
+// (each owns 16 of a hidden layer's 64 columns and 3 of the 12 hash levels):
 //   encode (bit-exact, encoding.py:111-157) -> forward (mlp.py:102-122) ->
 //   loss gradient (losses.py:23-42, f64) -> backward (mlp.py:125-154,
 //   ReLU' = z >= 0) -> hash-grid scatter (encoding.py:160-167).
-// Each thread keeps its row's layer outputs / input gradients in registers
-// (64 accumulators: long independent FMA chains) and reads the weights as
-// broadcast 16-byte shared-memory rows (W^T for the forward, W for the
-// backward); every layer's pre-activations and the encoded input are stashed
-// in TENSOR memory (the thread's own TMEM lane, 4 x 64 + 48 columns) instead
-// of shared memory, which leaves room for both weight images and keeps the
-// whole batch in one wave (B / 128 = 128 CTAs on 148 SMs).  Weight/bias
-// gradients are per-CTA partials from a shared-memory block GEMM over the
-// tile's rows, summed in a fixed order by k_reduce_grad (deterministic); the
-// hash-grid scatter is the one atomic (non-deterministic) sum.
+// Each thread keeps its column slice of the row's layer outputs / input
+// gradients in registers and reads the weights as broadcast 16-byte
+// shared-memory rows (W^T for the forward, W for the backward); every layer's
+// pre-activations and the encoded input are stashed in TENSOR memory (the
+// row's TMEM lane, 4 x 64 + 64 columns) instead of shared memory, which
+// leaves room for both weight images and keeps the whole batch in one wave
+// (B / 128 = 128 CTAs on 148 SMs, 16 warps each).  Weight/bias gradients are
+// per-CTA partials from a shared-memory block GEMM over the tile's rows,
+// summed in a fixed order by k_reduce_grad (deterministic); the hash-grid
+// scatter is the one atomic (non-deterministic) sum.
 //
 // fp32 SIMT: the reference's accuracy class.
 #include <cmath>
@@ -23,7 +24,11 @@
 namespace nirc {
 
 constexpr int kTR = 128;         // rows per tile
-constexpr int kTT = 256;         // threads per CTA: two per row (output halves)
+#ifndef NIRC_TRAIN_SPLIT
+#define NIRC_TRAIN_SPLIT 4
+#endif
+constexpr int kSplit = NIRC_TRAIN_SPLIT;  // threads per row (output column slices)
+constexpr int kTT = kTR * kSplit;         // threads per CTA
 constexpr int kLD2 = 132;        // row stride of the [feature][row] staging arrays
 constexpr int kMaxW = 64;        // widest layer supported by the fused path
 constexpr int kMaxNL = 8;
@@ -85,8 +90,10 @@ size_t fused_smem_bytes(const nirc_spec_t& sp) {
 
 __device__ __forceinline__ float relu(float z) { return z > 0.0f ? z : 0.0f; }
 
-// Thread (r, h): row r of the tile, output half h (columns 32h .. 32h+31).
-constexpr int kHalf = 32;
+// Thread (r, h): row r of the tile, column slice h (columns kCols*h ..).
+constexpr int kCols = kMaxW / kSplit;   // hidden columns per thread
+constexpr int kLvl = 12 / kSplit;       // hash levels per thread
+constexpr int kDX = 2 * kLvl;           // encoded-grid gradient columns per thread
 
 // out[j] = b[c0 + j] + sum_i in[i][r] * W[c0 + j][i], j < NOUT, c0 = column
 // offset; the input column read from the staging array, W^T row segments as
@@ -122,37 +129,48 @@ __device__ __forceinline__ void row_backward(const float* __restrict__ dz, int d
 #pragma unroll 2
   for (int j = 0; j < dout; ++j) {
     const float g = dz[j * kLD2 + r];
-    const float4* w = reinterpret_cast<const float4*>(W + j * ldw + c0);
+    if constexpr (NIN % 4 == 0) {
+      const float4* w = reinterpret_cast<const float4*>(W + j * ldw + c0);
 #pragma unroll
-    for (int q = 0; q < NIN / 4; ++q) {
-      const float4 v = w[q];
-      da[4 * q] = fmaf(g, v.x, da[4 * q]);
-      da[4 * q + 1] = fmaf(g, v.y, da[4 * q + 1]);
-      da[4 * q + 2] = fmaf(g, v.z, da[4 * q + 2]);
-      da[4 * q + 3] = fmaf(g, v.w, da[4 * q + 3]);
+      for (int q = 0; q < NIN / 4; ++q) {
+        const float4 v = w[q];
+        da[4 * q] = fmaf(g, v.x, da[4 * q]);
+        da[4 * q + 1] = fmaf(g, v.y, da[4 * q + 1]);
+        da[4 * q + 2] = fmaf(g, v.z, da[4 * q + 2]);
+        da[4 * q + 3] = fmaf(g, v.w, da[4 * q + 3]);
+      }
+    } else {
+      const float2* w = reinterpret_cast<const float2*>(W + j * ldw + c0);
+#pragma unroll
+      for (int q = 0; q < NIN / 2; ++q) {
+        const float2 v = w[q];
+        da[2 * q] = fmaf(g, v.x, da[2 * q]);
+        da[2 * q + 1] = fmaf(g, v.y, da[2 * q + 1]);
+      }
     }
   }
 }
 
 // Per-CTA partial dW[j][i] = sum_r dz[j][r] a[i][r], db[j] = sum_r dz[j][r]:
-// 256 threads as a 16 x 16 grid over the 64 x 64 outputs, 4 x 4 each, rows
+// the threads as a kJG x 16 grid over the 64 x 64 outputs, kP x 4 each, rows
 // in float4 steps.
+constexpr int kJG = kTT / 16, kP = kMaxW / kJG;
 __device__ __forceinline__ void tile_wgrad(const float* __restrict__ dz, int dout,
                                            const float* __restrict__ a, int din,
                                            float* __restrict__ part_w,
                                            float* __restrict__ part_b) {
   const int tid = threadIdx.x, jg = tid >> 4, ig = tid & 15;
-  float acc[4][4];
+  float acc[kP][4];
 #pragma unroll
-  for (int p = 0; p < 4; ++p)
+  for (int p = 0; p < kP; ++p)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[p][q] = 0.0f;
   if (jg < dout) {
     for (int r = 0; r < kTR; r += 4) {
-      float4 g[4], x[4];
+      float4 g[kP], x[4];
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        const int j = jg + 16 * p;
+      for (int p = 0; p < kP; ++p) {
+        const int j = jg + kJG * p;
         g[p] = j < dout ? *reinterpret_cast<const float4*>(dz + j * kLD2 + r)
                         : make_float4(0.f, 0.f, 0.f, 0.f);
       }
@@ -163,7 +181,7 @@ __device__ __forceinline__ void tile_wgrad(const float* __restrict__ dz, int dou
                        : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
-      for (int p = 0; p < 4; ++p)
+      for (int p = 0; p < kP; ++p)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           acc[p][q] = fmaf(g[p].x, x[q].x, acc[p][q]);
@@ -174,8 +192,8 @@ __device__ __forceinline__ void tile_wgrad(const float* __restrict__ dz, int dou
     }
   }
 #pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const int j = jg + 16 * p;
+  for (int p = 0; p < kP; ++p) {
+    const int j = jg + kJG * p;
     if (j >= dout) continue;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -190,13 +208,18 @@ __device__ __forceinline__ void tile_wgrad(const float* __restrict__ dz, int dou
   }
 }
 
-// 32 TMEM columns of this thread's lane <-> v[32]
-__device__ __forceinline__ void tmem_put32(uint32_t taddr, const float* v) {
-  tc::tmem_st16(taddr, v);
-  tc::tmem_st16(taddr + 16, v + 16);
+// kCols TMEM columns of this thread's lane <-> v[kCols]
+__device__ __forceinline__ void tmem_put(uint32_t taddr, const float* v) {
+#pragma unroll
+  for (int c = 0; c < kCols; c += 16) tc::tmem_st16(taddr + c, v + c);
 }
-__device__ __forceinline__ void tmem_get32(uint32_t taddr, float* v) {
-  tc::tmem_ld32(taddr, v);
+__device__ __forceinline__ void tmem_get(uint32_t taddr, float* v) {
+  if constexpr (kCols == 32) {
+    tc::tmem_ld32(taddr, v);
+  } else {
+#pragma unroll
+    for (int c = 0; c < kCols; c += 16) tc::tmem_ld16(taddr + c, v + c);
+  }
   tc::tmem_wait_ld();
 }
 
@@ -211,8 +234,8 @@ __global__ void __launch_bounds__(kTT, 1)
   __shared__ uint32_t tmem_holder;
   if (flags[0] & 3) return;
   const int tid = threadIdx.x;
-  const int r = tid & (kTR - 1), h = tid >> 7;
-  const int c0 = kHalf * h;
+  const int r = tid & (kTR - 1), h = tid / kTR;
+  const int c0 = kCols * h;
   const int lane_base = ((tid >> 5) & 3) * 32;
   const int64_t row = (tile0 + blockIdx.x) * kTR + r;
   const bool live = row < B;
@@ -238,7 +261,7 @@ __global__ void __launch_bounds__(kTT, 1)
   const uint32_t tbase = tmem_holder + ((uint32_t)lane_base << 16);
   float* A = fsm + L.a_off;   // [feature][row]: the current layer's input
   float* DZ = fsm + L.dz_off;
-  // ---- encode (bit-exact): levels 6h .. 6h+5; h == 0 also SH + aux --------
+  // ---- encode (bit-exact): levels kLvl*h ..; h == 0 also SH + aux ---------
   const uint32_t T = 1u << sp.table_log2;
   int64_t ri = 0;
   float ux = 0.0f, uy = 0.0f, uz = 0.0f;
@@ -250,8 +273,8 @@ __global__ void __launch_bounds__(kTT, 1)
     uz = norm_coord(p[2], sp.bb_min[2], sp.bb_inv[2]);
   }
 #pragma unroll
-  for (int q = 0; q < 6; ++q) {
-    const int lvl = 6 * h + q;
+  for (int q = 0; q < kLvl; ++q) {
+    const int lvl = kLvl * h + q;
     if (lvl < sp.levels) {
       float2 f = make_float2(0.0f, 0.0f);
       if (live) {
@@ -282,20 +305,20 @@ __global__ void __launch_bounds__(kTT, 1)
   }
   __syncthreads();
   {  // the encoded row -> TMEM (layer 0's a_prev for its weight gradient)
-    float x[32];
+    float x[kCols];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) x[i] = (c0 + i) < sp.in_dim ? A[(c0 + i) * kLD2 + r] : 0.0f;
-    tmem_put32(tbase + L.x_col + c0, x);
+    for (int i = 0; i < kCols; ++i) x[i] = (c0 + i) < sp.in_dim ? A[(c0 + i) * kLD2 + r] : 0.0f;
+    tmem_put(tbase + L.x_col + c0, x);
   }
   // ---- forward: hidden layers stash z in TMEM, write relu(z) as next input
   const int NL = L.nl;
   for (int l = 0; l < NL - 1; ++l) {
-    float z[kHalf];
-    row_forward<kHalf>(A, L.din[l], fsm + L.t_off[l], L.ldt[l], c0, fsm + L.b_off[l], r, z);
-    tmem_put32(tbase + 64 * l + c0, z);
+    float z[kCols];
+    row_forward<kCols>(A, L.din[l], fsm + L.t_off[l], L.ldt[l], c0, fsm + L.b_off[l], r, z);
+    tmem_put(tbase + 64 * l + c0, z);
     __syncthreads();  // both halves finished reading this layer's input
 #pragma unroll
-    for (int j = 0; j < kHalf; ++j) A[(c0 + j) * kLD2 + r] = relu(z[j]);
+    for (int j = 0; j < kCols; ++j) A[(c0 + j) * kLD2 + r] = relu(z[j]);
     __syncthreads();
   }
   float y[4];
@@ -344,35 +367,35 @@ __global__ void __launch_bounds__(kTT, 1)
   if (tid == 0) loss_part[blockIdx.x] = red[0];
   // ---- backward ----------------------------------------------------------
   float* wpart = partials + (int64_t)blockIdx.x * (sp.theta_len - sp.grid_len);
-  float dX[12];
+  float dX[kDX];
   for (int l = NL - 1; l >= 0; --l) {
     {  // a_prev of layer l -> staging (relu(z_{l-1}) or the encoded input)
-      float v[32];
-      tmem_get32(tbase + (l == 0 ? L.x_col : 64 * (l - 1)) + c0, v);
+      float v[kCols];
+      tmem_get(tbase + (l == 0 ? L.x_col : 64 * (l - 1)) + c0, v);
 #pragma unroll
-      for (int i = 0; i < 32; ++i)
+      for (int i = 0; i < kCols; ++i)
         if (c0 + i < L.din[l]) A[(c0 + i) * kLD2 + r] = l == 0 ? v[i] : relu(v[i]);
     }
     __syncthreads();  // DZ (layer l's dz) and A complete for the block GEMM
     tile_wgrad(DZ, L.dout[l], A, L.din[l], wpart + (sp.w_off[l] - sp.grid_len),
                wpart + (sp.b_off[l] - sp.grid_len));
     if (l > 0) {
-      float da[kHalf];
-      row_backward<kHalf>(DZ, L.dout[l], fsm + L.w_off[l], L.ldw[l], c0, r, da);
-      float zp[32];
-      tmem_get32(tbase + 64 * (l - 1) + c0, zp);
+      float da[kCols];
+      row_backward<kCols>(DZ, L.dout[l], fsm + L.w_off[l], L.ldw[l], c0, r, da);
+      float zp[kCols];
+      tmem_get(tbase + 64 * (l - 1) + c0, zp);
       __syncthreads();  // everyone finished reading DZ / A of layer l
 #pragma unroll
-      for (int i = 0; i < kHalf; ++i) DZ[(c0 + i) * kLD2 + r] = zp[i] >= 0.0f ? da[i] : 0.0f;
+      for (int i = 0; i < kCols; ++i) DZ[(c0 + i) * kLD2 + r] = zp[i] >= 0.0f ? da[i] : 0.0f;
     } else {
-      row_backward<12>(DZ, L.dout[0], fsm + L.w_off[0], L.ldw[0], 12 * h, r, dX);
+      row_backward<kDX>(DZ, L.dout[0], fsm + L.w_off[0], L.ldw[0], kDX * h, r, dX);
     }
   }
-  // ---- hash-grid scatter (encoding.py:160-167), levels 6h .. 6h+5 ---------
+  // ---- hash-grid scatter (encoding.py:160-167), levels kLvl*h .. ----------
   if (live) {
 #pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      const int lvl = 6 * h + q;
+    for (int q = 0; q < kLvl; ++q) {
+      const int lvl = kLvl * h + q;
       if (lvl >= sp.levels) continue;
       const LevelCell c = level_cell(ux, uy, uz, sp.res[lvl]);
       float* gl = grad + (size_t)lvl * T * 2;
