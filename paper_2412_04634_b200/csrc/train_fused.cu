@@ -239,17 +239,32 @@ __global__ void __launch_bounds__(kTT, 1)
   const int lane_base = ((tid >> 5) & 3) * 32;
   const int64_t row = (tile0 + blockIdx.x) * kTR + r;
   const bool live = row < B;
-  // ---- weights: W (dout x ldw) and W^T (din x ldt), zero padded ----------
+  // ---- weights: W (dout x ldw) and W^T (din x ldt), zero padded; 8 loads
+  // in flight per thread before the shared-memory stores ------------------
   for (int l = 0; l < L.nl; ++l) {
     const float* Wg = theta + sp.w_off[l];
-    const int din = L.din[l], dout = L.dout[l];
-    for (int e = tid; e < up4(dout) * L.ldw[l]; e += kTT) {
-      const int j = e / L.ldw[l], i = e - j * L.ldw[l];
-      fsm[L.w_off[l] + e] = (j < dout && i < din) ? Wg[j * din + i] : 0.0f;
-    }
-    for (int e = tid; e < up4(din) * L.ldt[l]; e += kTT) {
-      const int i = e / L.ldt[l], j = e - i * L.ldt[l];
-      fsm[L.t_off[l] + e] = (j < dout && i < din) ? Wg[j * din + i] : 0.0f;
+    const int din = L.din[l], dout = L.dout[l], ldw = L.ldw[l], ldt = L.ldt[l];
+    const int nw = up4(dout) * ldw, nt = up4(din) * ldt;
+    for (int e0 = tid; e0 < nw + nt; e0 += 8 * kTT) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * kTT;
+        int j, i;
+        if (e < nw) {
+          j = e / ldw;
+          i = e - j * ldw;
+        } else {
+          i = (e - nw) / ldt;
+          j = (e - nw) - i * ldt;
+        }
+        v[u] = (e < nw + nt && j < dout && i < din) ? __ldg(Wg + j * din + i) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * kTT;
+        if (e < nw + nt) fsm[(e < nw ? L.w_off[l] : L.t_off[l] - nw) + e] = v[u];
+      }
     }
     for (int j = tid; j < kMaxW; j += kTT)
       fsm[L.b_off[l] + j] = j < dout ? theta[sp.b_off[l] + j] : 0.0f;
@@ -356,15 +371,18 @@ __global__ void __launch_bounds__(kTT, 1)
       for (int j = 0; j < dout; ++j) DZ[j * kLD2 + r] = 0.0f;
     }
   }
-  // deterministic per-tile loss partial (tree over the threads)
+  // deterministic per-tile loss partial (fixed shuffle tree per warp, then
+  // the warp sums in order)
   double* red = reinterpret_cast<double*>(fsm + L.red_off);
-  red[tid] = lsum;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lsum += __shfl_down_sync(0xffffffffu, lsum, o);
+  if ((tid & 31) == 0) red[tid >> 5] = lsum;
   __syncthreads();
-  for (int st = kTT / 2; st > 0; st >>= 1) {
-    if (tid < st) red[tid] += red[tid + st];
-    __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kTT / 32; ++w) t += red[w];
+    loss_part[blockIdx.x] = t;
   }
-  if (tid == 0) loss_part[blockIdx.x] = red[0];
   // ---- backward ----------------------------------------------------------
   float* wpart = partials + (int64_t)blockIdx.x * (sp.theta_len - sp.grid_len);
   float dX[kDX];
@@ -404,8 +422,9 @@ __global__ void __launch_bounds__(kTT, 1)
       for (int k = 0; k < 8; ++k) {
         const float w = corner_weight(c, k);
         const uint32_t hh = corner_hash(c, k, T - 1u);
-        if (d0 != 0.0f) atomicAdd(gl + 2 * hh, __fmul_rn(w, d0));
-        if (d1 != 0.0f) atomicAdd(gl + 2 * hh + 1, __fmul_rn(w, d1));
+        if (d0 != 0.0f || d1 != 0.0f)  // one 8-byte vector RED per corner
+          atomicAdd(reinterpret_cast<float2*>(gl + 2 * hh),
+                    make_float2(__fmul_rn(w, d0), __fmul_rn(w, d1)));
       }
     }
   }
