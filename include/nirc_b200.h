@@ -301,6 +301,27 @@ int nirc_incident_targets(const nirc_scene_t* scene, uint64_t seed, uint64_t fra
                           int32_t count, double* out, double* out_full,
                           void* stream);
 
+/* integrand_samples_kernel (kernels.py:342-421), the control-variate
+ * baselines' sampler (baselines.py:426-431): per pixel of the camera
+ * (width x height from cam[14..15], device f64), the centre ray's primary hit
+ * and per_round BSDF draws keyed stream_key(seed, P_BASELINE, frame, p, k),
+ * each with one incident-radiance walk.  Output shapes (device):
+ * o_dir / o_f / o_frc (P, K, 3) f64, o_pdf (P, K) f64, o_valid (P,) u8,
+ * o_spos / o_sns / o_salb (P, 3) f64, o_srough (P,) f64.  Entries the
+ * reference leaves untouched (missed / mirror pixels, dead draws' dir / f /
+ * frc) are not written. */
+int nirc_integrand_samples(const nirc_scene_t* scene, const double* cam, uint64_t seed,
+                           uint64_t frame, int32_t per_round, double* o_dir, double* o_f,
+                           double* o_frc, double* o_pdf, uint8_t* o_valid, double* o_spos,
+                           double* o_sns, double* o_salb, double* o_srough, void* stream);
+
+/* occluded (geometry.py:206-210) for n shadow rays: out[i] = 1 when any
+ * primitive is hit with t in (eps, t_max).  origins / dirs (n, 3) device
+ * f64, out (n,) device u8.  Used by estimate_env_direct's residual
+ * (estimators.py:323-370). */
+int nirc_occluded(const nirc_scene_t* scene, const double* origins, const double* dirs,
+                  int64_t n, double t_max, uint8_t* out, void* stream);
+
 /* pt_radiance (estimators.py:240-257): sample `sample` of pixel (ix, iy),
  * MODE_PT, seed / frame / width / height from cfg; out (3,) device f64. */
 int nirc_pt_radiance(const nirc_scene_t* scene, const double* cam,

@@ -42,7 +42,8 @@ def dev(x, dtype, shape=None):
 
 def _np_dtype(dtype):
     return {torch.float32: np.float32, torch.float64: np.float64,
-            torch.int64: np.int64, torch.int32: np.int32}[dtype]
+            torch.int64: np.int64, torch.int32: np.int32, torch.uint8: np.uint8,
+            torch.bool: np.bool_}[dtype]
 
 
 def ptr(t):

@@ -138,6 +138,9 @@ SIGNATURES = {
     "nirc_surface_samples": (I32, [C.POINTER(NircScene), P, P, I32, P, I32, P, P, P, P, P]),
     "nirc_incident_targets": (I32, [C.POINTER(NircScene), U64, U64, P, P, F64, P, I32, P, P,
                                     P]),
+    "nirc_integrand_samples": (I32, [C.POINTER(NircScene), P, U64, U64, I32, P, P, P, P, P, P,
+                                     P, P, P, P]),
+    "nirc_occluded": (I32, [C.POINTER(NircScene), P, P, I64, F64, P, P]),
     "nirc_pt_radiance": (I32, [C.POINTER(NircScene), P, C.POINTER(NircRenderCfg), I32, I32, I32,
                                P, P]),
     "nirc_collect_range": (I32, [C.POINTER(NircScene), P, U64, U64, I64, I64, I32,

@@ -1605,6 +1605,39 @@ __global__ void k_surface_samples(nirc_scene_t scn, V3 ns, V3 wo, int mat, const
   cosv[k] = ok ? c : 0.0;
 }
 
+// walk_record's return value (kernels.py:249-286): runs the walk w (key,
+// ray, prev_pdf / prev_ns already set) to its end and sweeps it backwards;
+// res[1:4] -> out, res[4:7] -> out_full.
+__device__ inline void walk_incident(const nirc_scene_t& scn, WalkLane& w, const Stage& st,
+                                     double* out, double* out_full) {
+  w.v = 0;
+  w.esc = 0;
+  for (int c = 0; c < 3; ++c) w.env_m[c] = w.env_r[c] = 0.0;
+  while (!walk_vertex(scn, w, st)) {
+  }
+  walk_finish(w, st);
+  const int n = w.v;
+  if (n == 0) {
+    for (int c = 0; c < 3; ++c) {
+      out[c] = w.env_m[c];
+      out_full[c] = w.env_r[c];
+    }
+    return;
+  }
+  double l[3] = {0.0, 0.0, 0.0};
+  for (int v = n - 1; v >= 0; --v) {
+    double cc[3];
+    for (int c = 0; c < 3; ++c) {
+      cc[c] = v == n - 1 ? (w.esc ? w.env_m[c] : 0.0) : w.mise[v + 1][c] + l[c];
+    }
+    for (int c = 0; c < 3; ++c) l[c] = w.nee[v][c] + w.fcp[v][c] * cc[c];
+  }
+  for (int c = 0; c < 3; ++c) {
+    out[c] = w.mise[0][c] + l[c];
+    out_full[c] = w.emit[0][c] + l[c];
+  }
+}
+
 // incident_targets_kernel (kernels.py:315-338): walk i keys
 // stream_key(seed, P_TRAIN, frame, i, 0) and starts on the given ray.
 __global__ void k_incident_targets(nirc_scene_t scn, uint64_t seed, uint64_t frame, V3 o, V3 d,
@@ -1621,33 +1654,84 @@ __global__ void k_incident_targets(nirc_scene_t scn, uint64_t seed, uint64_t fra
   w.d = d;
   w.prev_pdf = pv_pdf;
   w.lns = pns;
-  w.v = 0;
-  w.esc = 0;
-  for (int c = 0; c < 3; ++c) w.env_m[c] = w.env_r[c] = 0.0;
-  while (!walk_vertex(scn, w, st)) {
+  walk_incident(scn, w, st, out + 3 * i, out_full + 3 * i);
+}
+
+// integrand_samples_kernel (kernels.py:342-421): draw k of pixel p (one
+// thread each, draws [q0, q0 + n) of the flattened (P, K) grid) at the
+// centre ray's primary hit; the draw keys stream_key(seed, P_BASELINE,
+// frame, p, k), samples the BSDF with dims (2, 3) and estimates the
+// incident radiance with one recording walk (stage slot = draw - q0).
+// Outputs the reference leaves untouched (missed / mirror pixels, dead
+// draws' dir / f / frc) are not written.
+__global__ void k_integrand_samples(nirc_scene_t scn, const double* cam, uint64_t seed,
+                                    uint64_t frame, int K, int64_t q0, int64_t n, Stage st,
+                                    double* o_dir, double* o_f, double* o_frc, double* o_pdf,
+                                    uint8_t* o_valid, double* o_spos, double* o_sns,
+                                    double* o_salb, double* o_srough) {
+  __shared__ __align__(16) unsigned char scene_sm[pt::kSceneSmemBytes];
+  pt::stage_scene(scn, scene_sm);
+  const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= n) return;
+  const int64_t q = q0 + slot, p = q / K;
+  const int k = (int)(q - p * K);
+  const int W = (int)cam[14];
+  const int ix = (int)(p % W), iy = (int)(p / W);
+  V3 o, d;
+  pt::camera_ray(cam, ix, iy, 0.5, 0.5, o, d);
+  const pt::Hit hh = pt::intersect<false>(scn, o, d, pt::T_FAR);
+  if (k == 0) o_valid[p] = 0;
+  if (hh.kind < 0) return;
+  const int mkind = scn.mat_kind[hh.mid];
+  if (mkind == pt::MAT_MIRROR) return;
+  const V3 wo = {-d.x, -d.y, -d.z};
+  const double flip = (hh.n.x * wo.x + hh.n.y * wo.y + hh.n.z * wo.z) >= 0.0 ? 1.0 : -1.0;
+  const V3 ns = {hh.n.x * flip, hh.n.y * flip, hh.n.z * flip};
+  const V3 alb = pt::ld3(scn.mat_albedo, hh.mid);
+  const double rough = scn.mat_rough[hh.mid];
+  if (k == 0) {
+    o_valid[p] = 1;
+    o_spos[3 * p] = hh.p.x; o_spos[3 * p + 1] = hh.p.y; o_spos[3 * p + 2] = hh.p.z;
+    o_sns[3 * p] = ns.x; o_sns[3 * p + 1] = ns.y; o_sns[3 * p + 2] = ns.z;
+    o_salb[3 * p] = alb.x; o_salb[3 * p + 1] = alb.y; o_salb[3 * p + 2] = alb.z;
+    o_srough[p] = rough;
   }
-  walk_finish(w, st);
-  // the incident estimate along the input ray (walk_record's return value)
-  const int n = w.v;
-  if (n == 0) {
-    for (int c = 0; c < 3; ++c) {
-      out[3 * i + c] = w.env_m[c];
-      out_full[3 * i + c] = w.env_r[c];
-    }
-    return;
-  }
-  double l[3] = {0.0, 0.0, 0.0};
-  for (int v = n - 1; v >= 0; --v) {
-    double cc[3];
-    for (int c = 0; c < 3; ++c) {
-      cc[c] = v == n - 1 ? (w.esc ? w.env_m[c] : 0.0) : w.mise[v + 1][c] + l[c];
-    }
-    for (int c = 0; c < 3; ++c) l[c] = w.nee[v][c] + w.fcp[v][c] * cc[c];
-  }
-  for (int c = 0; c < 3; ++c) {
-    out[3 * i + c] = w.mise[0][c] + l[c];
-    out_full[3 * i + c] = w.emit[0][c] + l[c];
-  }
+  o_pdf[q] = 0.0;
+  const uint64_t key = stream_key(seed, P_BASELINE, frame, (uint64_t)p, (uint64_t)k);
+  const pt::BsdfSample b =
+      pt::bsdf_sample(mkind, alb, rough, ns, wo, rand_uniform(key, 2), rand_uniform(key, 3));
+  if (b.pdf <= 0.0 || b.delta == 1) return;
+  const double ci = b.wi.x * ns.x + b.wi.y * ns.y + b.wi.z * ns.z;
+  if (ci <= 0.0) return;
+  const double sg = (hh.n.x * b.wi.x + hh.n.y * b.wi.y + hh.n.z * b.wi.z) > 0.0 ? 1.0 : -1.0;
+  WalkLane w;
+  w.p = slot;
+  w.key = key;
+  w.o = {hh.p.x + sg * scn.eps * hh.n.x, hh.p.y + sg * scn.eps * hh.n.y,
+         hh.p.z + sg * scn.eps * hh.n.z};
+  w.d = b.wi;
+  w.prev_pdf = b.pdf;
+  w.lns = ns;
+  double res[3], res_full[3];
+  walk_incident(scn, w, st, res, res_full);
+  o_dir[3 * q] = b.wi.x; o_dir[3 * q + 1] = b.wi.y; o_dir[3 * q + 2] = b.wi.z;
+  o_frc[3 * q] = b.f.x * ci; o_frc[3 * q + 1] = b.f.y * ci; o_frc[3 * q + 2] = b.f.z * ci;
+  o_f[3 * q] = res[0] * b.f.x * ci;
+  o_f[3 * q + 1] = res[1] * b.f.y * ci;
+  o_f[3 * q + 2] = res[2] * b.f.z * ci;
+  o_pdf[q] = b.pdf;
+}
+
+// occluded (geometry.py:206-210) over a batch of shadow rays.
+__global__ void k_occluded(nirc_scene_t scn, const double* o, const double* d, int64_t n,
+                           double t_max, uint8_t* out) {
+  __shared__ __align__(16) unsigned char scene_sm[pt::kSceneSmemBytes];
+  pt::stage_scene(scn, scene_sm);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const V3 oi = {o[3 * i], o[3 * i + 1], o[3 * i + 2]};
+  const V3 di = {d[3 * i], d[3 * i + 1], d[3 * i + 2]};
+  out[i] = pt::occluded(scn, oi, di, t_max) ? 1 : 0;
 }
 
 // pt_radiance (estimators.py:240-257): one MODE_PT sample of one pixel.
@@ -1708,6 +1792,51 @@ extern "C" int nirc_incident_targets(const nirc_scene_t* scene, uint64_t seed, u
                                                       count, st, out, out_full);
   NIRC_LAUNCH_CHECK("k_incident_targets");
   NIRC_CUDA_TRY(cudaFreeAsync(ws, s));
+  return NIRC_OK;
+}
+
+extern "C" int nirc_integrand_samples(const nirc_scene_t* scene, const double* cam,
+                                      uint64_t seed, uint64_t frame, int32_t per_round,
+                                      double* o_dir, double* o_f, double* o_frc, double* o_pdf,
+                                      uint8_t* o_valid, double* o_spos, double* o_sns,
+                                      double* o_salb, double* o_srough, void* stream) {
+  if (per_round <= 0) {
+    set_last_error("per_round must be positive");
+    return NIRC_E_CONFIG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  double dims[2];
+  NIRC_CUDA_TRY(cudaMemcpyAsync(dims, cam + 14, sizeof(dims), cudaMemcpyDeviceToHost, s));
+  NIRC_CUDA_TRY(cudaStreamSynchronize(s));
+  const int64_t P = (int64_t)dims[0] * (int64_t)dims[1], total = P * per_round;
+  if (total == 0) return NIRC_OK;
+  // the walks' per-vertex scratch is reused across chunks of draws
+  const int64_t chunk = total < (int64_t(1) << 18) ? total : (int64_t(1) << 18);
+  size_t bytes = 0;
+  carve_stage(chunk, nullptr, &bytes);
+  void* ws = nullptr;
+  NIRC_CUDA_TRY(cudaMallocAsync(&ws, bytes, s));
+  size_t b2 = 0;
+  Stage st = carve_stage(chunk, ws, &b2);
+  st.kind = REC_NIRC;
+  for (int64_t q0 = 0; q0 < total; q0 += chunk) {
+    const int64_t n = total - q0 < chunk ? total - q0 : chunk;
+    k_integrand_samples<<<(unsigned)((n + 63) / 64), 64, 0, s>>>(
+        *scene, cam, seed, frame, per_round, q0, n, st, o_dir, o_f, o_frc, o_pdf, o_valid,
+        o_spos, o_sns, o_salb, o_srough);
+    NIRC_LAUNCH_CHECK("k_integrand_samples");
+  }
+  NIRC_CUDA_TRY(cudaFreeAsync(ws, s));
+  return NIRC_OK;
+}
+
+extern "C" int nirc_occluded(const nirc_scene_t* scene, const double* origins,
+                             const double* dirs, int64_t n, double t_max, uint8_t* out,
+                             void* stream) {
+  if (n <= 0) return NIRC_OK;
+  k_occluded<<<(unsigned)((n + 127) / 128), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      *scene, origins, dirs, n, t_max, out);
+  NIRC_LAUNCH_CHECK("k_occluded");
   return NIRC_OK;
 }
 

@@ -20,6 +20,8 @@ import torch
 from . import _dev, _lib
 from .errors import ConfigError
 
+T_FAR = 1.0e30  # geometry.py:16
+
 MODES = {"pt": 0, "two-level": 1, "biased-nirc-bth": 2, "biased-nirc-sph": 3,
          "biased-nrc-sph": 4}
 MAX_DIRS = 28  # OFF_CACHE leaves room for 28 direction pairs per vertex
@@ -365,6 +367,65 @@ def estimate_Lr(scene, it, cache, n_r=1, seed=0, stream=0):
         pred = cache.nirc_query(it, dirs[k][None, :])[0]
         out += (li[0] - pred) * fval[k] * (cos[k] / pdf[k])
     return out / n_r
+
+
+def estimate_env_direct(scene, cache, it, n_c=15, n_r=1, seed=0, stream=0):
+    """Two-level estimate of reflected direct environment light at one
+    interaction (estimators.py:323-348): the cache's per-direction
+    prediction (a visibility cache scaled by the known environment radiance)
+    over n_c brdf draws, plus n_r shadow-rayed residual draws (device
+    occlusion queries, nirc_occluded)."""
+    if scene.pack.env_kind == 0:
+        raise ConfigError("scene has no environment light")
+    dirs, pdf, fval, cos = _surface_dirs(scene, it, n_c, seed, stream, 0)
+    out = np.zeros(3)
+    ok = pdf > 0.0
+    if np.any(ok):
+        pred = _env_prediction(scene, cache, it, dirs[ok])
+        wgt = cos[ok] / pdf[ok]
+        out += np.sum(pred * fval[ok] * wgt[:, None], axis=0) / n_c
+    dirs, pdf, fval, cos = _surface_dirs(scene, it, n_r, seed, stream, 1000)
+    ok = pdf > 0.0
+    if np.any(ok):
+        pred = _env_prediction(scene, cache, it, dirs[ok])
+        shadow = _shadowed(scene, it, dirs[ok])
+        true = np.zeros_like(pred)
+        for j, d in enumerate(dirs[ok]):
+            if not shadow[j]:
+                true[j] = scene.env_radiance(d)
+        wgt = cos[ok] / pdf[ok]
+        out += np.sum((true - pred) * fval[ok] * wgt[:, None], axis=0) / n_r
+    return out
+
+
+def _env_prediction(scene, cache, it, dirs):
+    """estimators.py:351-356."""
+    if cache.kind == "nvc":
+        vis = cache.nvc_query(it, dirs)
+        env = np.array([scene.env_radiance(d) for d in dirs])
+        return vis * env
+    return cache.nirc_query(it, dirs)
+
+
+def _shadowed(scene, it, wis):
+    """estimators.py:359-370 for a batch of directions: shadow rays spawned
+    eps along the side of the geometric normal facing each direction, any-hit
+    to T_FAR on the device."""
+    wis = np.atleast_2d(np.asarray(wis, np.float64))
+    n = wis.shape[0]
+    p, g = np.asarray(it.position, float), np.asarray(it.ng, float)
+    eps = float(scene.pack.eps)
+    org = np.empty((n, 3))
+    for k in range(n):
+        sgn = 1.0 if float(g @ wis[k]) > 0.0 else -1.0
+        org[k] = (p[0] + sgn * eps * g[0], p[1] + sgn * eps * g[1], p[2] + sgn * eps * g[2])
+    o_d, d_d = _dev.dev(org, torch.float64), _dev.dev(np.ascontiguousarray(wis), torch.float64)
+    res = _dev.zeros((n,), torch.uint8)
+    ds = scene.device()
+    lib = _lib.load()
+    _lib.check(lib.nirc_occluded(ds.ptr(), _dev.ptr(o_d), _dev.ptr(d_d), n, T_FAR, _dev.ptr(res),
+                                 _dev.stream()), "nirc_occluded")
+    return res.cpu().numpy().astype(bool)
 
 
 def pt_radiance(scene, ix, iy, seed=0, sample=0, frame=0):

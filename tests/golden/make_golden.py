@@ -376,10 +376,50 @@ def golden_api():
     mw = int(max(cache.spec.dims))
     out["y"] = np.array(mlp_forward_s(cache.spec, cache.theta, x.astype(np.float32),
                                       np.zeros(mw, np.float32), np.zeros(mw, np.float32)))
+    # estimate_env_direct (estimators.py:323-348) on MIXED's sky, NIRC and
+    # NVC caches
+    from nirclab.estimators import estimate_env_direct
+
+    mixed = load_scene(MIXED)
+    itm = mixed.intersect(np.array([0.6, 0.5, 0.3]), np.array([0.0, -1.0, 0.0]))
+    for kind in ("nirc", "nvc"):
+        cm = Cache.create(kind, mixed, seed=6, init="random")
+        out[f"env_{kind}"] = estimate_env_direct(mixed, cm, itm, n_c=8, n_r=5, seed=4,
+                                                 stream=2)
     np.savez_compressed(os.path.join(HERE, "api.npz"), **out)
 
 
+def golden_baseline():
+    """The control-variate baselines' integrand sampler (baselines.py:426-431
+    over kernels.py:342-421) and the cache evaluation at its live draws
+    (_nirc_grid_eval, baselines.py:434-446) on the BOX and MIXED scenes."""
+    from nirclab.baselines import _integrand_round, _nirc_grid_eval
+    from nirclab.caches import Cache
+    from nirclab.caches import _path_arrays
+    from nirclab.scene import load_scene
+
+    out = {}
+    for tag, sc, seed, frame, k_ in (("box", load_scene(BOX), 3, 0, 4),
+                                     ("box2", load_scene(BOX), 3, 2, 4),
+                                     ("mixed", load_scene(MIXED), 1, 5, 6)):
+        w, h = int(sc.camera[14]), int(sc.camera[15])
+        p_ = w * h
+        o = dict(dir=np.zeros((p_, k_, 3)), f=np.zeros((p_, k_, 3)),
+                 frc=np.zeros((p_, k_, 3)), pdf=np.zeros((p_, k_)),
+                 valid=np.zeros(p_, np.uint8), spos=np.zeros((p_, 3)),
+                 sns=np.zeros((p_, 3)), salb=np.zeros((p_, 3)), srough=np.zeros(p_))
+        scratch = [a[0] for a in _path_arrays(1).values()]
+        _integrand_round(sc, seed, frame, k_, scratch, o)
+        for k, v in o.items():
+            out[f"{tag}_{k}"] = v
+        cache = Cache.create("nirc", sc, seed=4, init="random")
+        out[f"{tag}_grid"] = _nirc_grid_eval(cache, o, o["pdf"] > 0.0)
+    np.savez_compressed(os.path.join(HERE, "baseline.npz"), **out)
+
+
 if __name__ == "__main__" and len(sys.argv) > 1:
+    if "baseline" in sys.argv:
+        golden_baseline()
     if "api" in sys.argv:
         golden_api()
     if "snapshot" in sys.argv:

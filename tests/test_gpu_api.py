@@ -113,3 +113,25 @@ def test_scalar_encode_and_forward_match_reference(box, golden):
     np.testing.assert_array_equal(xin, x)
     y = mlp_forward_s(cache.spec, cache.theta, x.astype(np.float32))
     np.testing.assert_allclose(y, g["y"], rtol=1e-4, atol=1e-7)
+
+
+def test_estimate_env_direct_matches_reference(golden):
+    """estimate_env_direct (estimators.py:323-348) on MIXED's sky: NIRC and
+    NVC caches, shadow rays through nirc_occluded."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2412_04634_b200.caches import Cache
+    from paper_2412_04634_b200.errors import ConfigError
+    from paper_2412_04634_b200.estimators import estimate_env_direct
+    from paper_2412_04634_b200.scene import load_scene
+
+    g = golden("api")
+    mixed = load_scene(_SRC.split('MIXED = """')[1].split('"""')[0])
+    it = mixed.intersect(np.array([0.6, 0.5, 0.3]), np.array([0.0, -1.0, 0.0]))
+    for kind in ("nirc", "nvc"):
+        cm = Cache.create(kind, mixed, seed=6, init="random")
+        got = estimate_env_direct(mixed, cm, it, n_c=8, n_r=5, seed=4, stream=2)
+        np.testing.assert_allclose(got, g[f"env_{kind}"], rtol=1e-4, atol=1e-7, err_msg=kind)
+    box = load_scene(BOX)
+    with pytest.raises(ConfigError):
+        estimate_env_direct(box, Cache.create("nirc", box, seed=1), _floor(box))
