@@ -347,6 +347,20 @@ int nirc_render_collect(const nirc_scene_t* scene, const double* cam,
 int64_t nirc_render_collect_workspace_bytes(const nirc_render_cfg_t* cfg,
                                             int64_t count);
 
+/* ---- scene acceleration (pkg/src/nirclab/geometry.py:213-274) ----------- */
+/* build_bvh on the device: the reference's median-split BVH (<= 4 prims per
+ * leaf, left child = next node, right child index in a, leaf iff b > 0 with
+ * prims prim[a : a+b]), node for node identical to the host build.  Inputs
+ * (device f64): tri_v0 / tri_e1 / tri_e2 (n_tri, 3), sph_c (n_sph, 3),
+ * sph_r (n_sph,).  Outputs (device): lo / hi (N, 3) f64, a / b (N,) i32,
+ * prim (n_tri + n_sph,) i32, N = nirc_bvh_node_count(n_tri + n_sph).
+ * Synchronises `stream` before returning. */
+int64_t nirc_bvh_node_count(int64_t n_prims);
+int nirc_build_bvh(const double* tri_v0, const double* tri_e1, const double* tri_e2,
+                   int64_t n_tri, const double* sph_c, const double* sph_r, int64_t n_sph,
+                   double* lo, double* hi, int32_t* a, int32_t* b, int32_t* prim,
+                   void* stream);
+
 #ifdef __cplusplus
 }
 #endif

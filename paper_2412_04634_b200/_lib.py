@@ -140,6 +140,8 @@ SIGNATURES = {
                                     P]),
     "nirc_integrand_samples": (I32, [C.POINTER(NircScene), P, U64, U64, I32, P, P, P, P, P, P,
                                      P, P, P, P]),
+    "nirc_bvh_node_count": (I64, [I64]),
+    "nirc_build_bvh": (I32, [P, P, P, I64, P, P, I64, P, P, P, P, P, P]),
     "nirc_occluded": (I32, [C.POINTER(NircScene), P, P, I64, F64, P, P]),
     "nirc_pt_radiance": (I32, [C.POINTER(NircScene), P, C.POINTER(NircRenderCfg), I32, I32, I32,
                                P, P]),

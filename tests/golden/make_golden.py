@@ -417,7 +417,31 @@ def golden_baseline():
     np.savez_compressed(os.path.join(HERE, "baseline.npz"), **out)
 
 
+def golden_big():
+    """A scene past HOST_BVH_MAX (tests/big_scene.py): the reference's
+    build_bvh arrays and its PT / two-level renders."""
+    sys.path.insert(0, os.path.dirname(HERE))
+    from big_scene import big_scene_text
+    from nirclab.caches import Cache
+    from nirclab.estimators import EstimatorConfig, render
+    from nirclab.scene import load_scene
+
+    sc = load_scene(big_scene_text())
+    p = sc.pack
+    out = {k: np.asarray(getattr(p, k)) for k in ("bvh_lo", "bvh_hi", "bvh_a", "bvh_b",
+                                                   "bvh_prim")}
+    r = render(sc, EstimatorConfig(mode="pt"), seed=5, spp=2)
+    out["pt_image"], out["pt_plen"] = r.image, r.path_length
+    cache = Cache.create("nirc", sc, seed=9, init="random")
+    r = render(sc, EstimatorConfig(mode="two-level", nc=(8, 4), max_cache_vertices=2), cache=cache,
+               seed=5, spp=2)
+    out["tl_image"], out["tl_plen"] = r.image, r.path_length
+    np.savez_compressed(os.path.join(HERE, "big.npz"), **out)
+
+
 if __name__ == "__main__" and len(sys.argv) > 1:
+    if "big" in sys.argv:
+        golden_big()
     if "baseline" in sys.argv:
         golden_baseline()
     if "api" in sys.argv:
