@@ -274,6 +274,78 @@ def frame_bench(frames, warmup, width=1920, height=1080, nc=(16,), comm=None, na
     }
 
 
+def convergence_bench(frames=100, width=1920, height=1080, ref_spp=64):
+    """BASELINE config 4: the teleport scene (its lamp jumps at frame 40) at
+    1920x1080, `frames` frames of continuous online training with the cfg3
+    estimator ("as cfg 3 per frame") through the device frame
+    loop (frame.run_frame = experiment.py:149-185's render / collect / train),
+    MRSE per frame against a ref_spp device-PT reference of each geometry
+    state (experiment.py's _ReferenceBank), computed on the device."""
+    import torch
+
+    from paper_2412_04634_b200.config import RunConfig
+    from paper_2412_04634_b200.estimators import EstimatorConfig, render_device
+    from paper_2412_04634_b200.experiment import REF_SEED_OFFSET, _make_cache
+    from paper_2412_04634_b200.frame import config3, run_frame
+    from paper_2412_04634_b200.scene import load_builtin
+
+    rc = RunConfig(scene="teleport", mode="two-level", nc=(16,), max_cache_vertices=1,
+                   frames=frames, seed=0, ref_spp=ref_spp)
+    scene = load_builtin("teleport").with_resolution(width, height)
+    cache = _make_cache(rc, scene)
+    est = config3((16,))
+    stream = torch.cuda.current_stream()
+    refs, ref_ms = {}, 0.0
+    ms, mrse = [], []
+    for f in range(frames):
+        scene = scene.at_frame(f)
+        cache.scene = scene
+        key = scene.content_hash()
+        if key not in refs:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            img, _, _, _ = render_device(scene, EstimatorConfig(mode="pt"), None,
+                                         rc.seed + REF_SEED_OFFSET, ref_spp, 0)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ref_ms += e0.elapsed_time(e1)
+            refs[key] = img / ref_spp
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        (img, _, _), _ = run_frame(scene, cache, est, rc.seed, f)
+        e1.record(stream)
+        ref = refs[key]
+        mrse.append(torch.mean((img - ref) ** 2 / (ref * ref + 0.01)))
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    m = [float(x.item()) for x in mrse]
+    # plain 1-spp PT on the same frames and pixels: what the cache buys
+    pt = []
+    for f in range(frames - 10, frames):
+        img, _, _, _ = render_device(scene.at_frame(f), EstimatorConfig(mode="pt"), None,
+                                     rc.seed, 1, f)
+        ref = refs[scene.at_frame(f).content_hash()]
+        pt.append(float(torch.mean((img - ref) ** 2 / (ref * ref + 0.01)).item()))
+
+    def win(lo, hi):
+        return sum(m[lo:hi]) / max(1, len(m[lo:hi]))
+
+    return {
+        "metric": f"ms_per_frame_{width}x{height}_teleport_{frames}f", "unit": "ms/frame",
+        "value": sorted(ms)[len(ms) // 2], "mean_ms": sum(ms) / len(ms),
+        "higher_is_better": False, "frames": frames, "n_gpus": 1,
+        "mrse_frame0": m[0], "mrse_mean_30_40": win(30, 40), "mrse_mean_40_50": win(40, 50),
+        "mrse_mean_last10": win(frames - 10, frames), "mrse_final": m[-1],
+        "pt_mrse_mean_last10": sum(pt) / len(pt),
+        "reference": f"device PT, {ref_spp} spp per geometry state ({len(refs)} states, "
+                     f"{ref_ms:.0f} ms, not in the frame time)",
+        "config": "cfg4: teleport 1920x1080 (lamp jumps at frame 40), two-level nc=(16,), "
+                  "spp 1, D=4 cache (zero-initialised output layer), collect 0.025 W H paths, "
+                  "4 Adam steps per frame; MRSE = mean((img-ref)^2/(ref^2+0.01)) "
+                  "(metrics.py) on the device",
+    }
+
+
 # ------------------------------------------------------------ GPU leg ----
 def run_b200(args, rank, world, local_rank):
     import numpy as np
@@ -376,6 +448,8 @@ def run_b200(args, rank, world, local_rank):
             fb["cfg1_128"]["reference_cpu_context"] = (
                 "SURVEY.md 6: 1.28 s/frame for cfg1 on 1 core (render 1084 + collect 12 + "
                 "train 179 ms)")
+        if world == 1 and not args.no_extra_frames:
+            fb["cfg4_teleport_1080p"] = convergence_bench()
     if rank != 0:
         return
     import json as _json
