@@ -78,6 +78,11 @@ typedef struct nirc_scene {
   const int32_t *bvh_a, *bvh_b, *bvh_prim;
   const float* tri_f32;  /* kernel-private scratch (the staged fp32 triangle
                             filter table); callers pass NULL */
+  /* Optional traversal image from nirc_pack_scene (NULL: the kernels walk
+   * the bvh_* arrays directly).  Scenes past the warp-uniform scan size
+   * traverse it front to back. */
+  const void* bvh_packed;
+  const void* prim_packed;
 } nirc_scene_t;
 
 /* Two-level estimator knobs; mirrors EstimatorConfig
@@ -356,6 +361,15 @@ int64_t nirc_render_collect_workspace_bytes(const nirc_render_cfg_t* cfg,
  * prim (n_tri + n_sph,) i32, N = nirc_bvh_node_count(n_tri + n_sph).
  * Synchronises `stream` before returning. */
 int64_t nirc_bvh_node_count(int64_t n_prims);
+
+/* Traversal image of a scene's BVH (kernels-private layout: per internal
+ * node both child boxes and child references; primitives in BVH leaf order
+ * with their geometry inline).  `out` is a device buffer of
+ * nirc_scene_packed_bytes(scene) bytes; on success scene->bvh_packed and
+ * scene->prim_packed point into it.  Hit results are the bvh_* traversal's
+ * (same nearest hit, same any-hit boolean). */
+int64_t nirc_scene_packed_bytes(const nirc_scene_t* scene);
+int nirc_pack_scene(nirc_scene_t* scene, void* out, int64_t out_bytes, void* stream);
 int nirc_build_bvh(const double* tri_v0, const double* tri_e1, const double* tri_e2,
                    int64_t n_tri, const double* sph_c, const double* sph_r, int64_t n_sph,
                    double* lo, double* hi, int32_t* a, int32_t* b, int32_t* prim,

@@ -83,6 +83,7 @@ class NircScene(C.Structure):
         ("bvh_lo", C.c_void_p), ("bvh_hi", C.c_void_p),
         ("bvh_a", C.c_void_p), ("bvh_b", C.c_void_p), ("bvh_prim", C.c_void_p),
         ("tri_f32", C.c_void_p),
+        ("bvh_packed", C.c_void_p), ("prim_packed", C.c_void_p),
     ]
 
 
@@ -141,6 +142,8 @@ SIGNATURES = {
     "nirc_integrand_samples": (I32, [C.POINTER(NircScene), P, U64, U64, I32, P, P, P, P, P, P,
                                      P, P, P, P]),
     "nirc_bvh_node_count": (I64, [I64]),
+    "nirc_scene_packed_bytes": (I64, [C.POINTER(NircScene)]),
+    "nirc_pack_scene": (I32, [C.POINTER(NircScene), P, I64, P]),
     "nirc_build_bvh": (I32, [P, P, P, I64, P, P, I64, P, P, P, P, P, P]),
     "nirc_occluded": (I32, [C.POINTER(NircScene), P, P, I64, F64, P, P]),
     "nirc_pt_radiance": (I32, [C.POINTER(NircScene), P, C.POINTER(NircRenderCfg), I32, I32, I32,

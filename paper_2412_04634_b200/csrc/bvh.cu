@@ -30,6 +30,7 @@
 
 #include "nirc_b200.h"
 #include "common.cuh"
+#include "pt_packed.cuh"
 
 namespace nirc {
 namespace {
@@ -381,5 +382,91 @@ extern "C" int nirc_build_bvh(const double* tri_v0, const double* tri_e1, const 
   NIRC_CUDA_TRY(cudaFreeAsync(ws, s));
   // the host plan vectors are read by the async copies above
   NIRC_CUDA_TRY(cudaStreamSynchronize(s));
+  return NIRC_OK;
+}
+
+// ---------------------------------------------------------------------
+// Traversal image for the front-to-back walk (pt_common.cuh
+// bvh_scan_packed): per internal node both child boxes + references, and
+// the primitives in leaf order with their geometry inline.
+namespace nirc {
+namespace {
+
+__global__ void k_pack_nodes(nirc_scene_t s, pt::PackedNode* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= s.n_bvh) return;
+  pt::PackedNode nd{};
+  if (s.bvh_b[i] == 0 && s.bvh_a[i] != i) {
+    const int ch[2] = {i + 1, s.bvh_a[i]};
+    for (int c = 0; c < 2; ++c) {
+      const int k = ch[c];
+      double* lo = c == 0 ? nd.lo0 : nd.lo1;
+      double* hi = c == 0 ? nd.hi0 : nd.hi1;
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = s.bvh_lo[3 * k + a];
+        hi[a] = s.bvh_hi[3 * k + a];
+      }
+      const bool leaf = s.bvh_b[k] > 0;
+      (c == 0 ? nd.c0 : nd.c1) = leaf ? s.bvh_a[k] : k;
+      (c == 0 ? nd.n0 : nd.n1) = leaf ? s.bvh_b[k] : 0;
+    }
+  }
+  out[i] = nd;
+}
+
+__global__ void k_pack_prims(nirc_scene_t s, pt::PackedPrim* out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= s.n_tri + s.n_sph) return;
+  pt::PackedPrim q{};
+  const int pid = s.bvh_prim[k];
+  if (pid < s.n_tri) {
+    for (int a = 0; a < 3; ++a) {
+      q.g[a] = s.tri_v0[3 * pid + a];
+      q.g[3 + a] = s.tri_e1[3 * pid + a];
+      q.g[6 + a] = s.tri_e2[3 * pid + a];
+    }
+    q.id = pid;
+    q.kind = 0;
+  } else {
+    const int j = pid - s.n_tri;
+    for (int a = 0; a < 3; ++a) q.g[a] = s.sph_c[3 * j + a];
+    q.g[3] = s.sph_r[j];
+    q.id = j;
+    q.kind = 1;
+  }
+  out[k] = q;
+}
+
+size_t packed_node_bytes(const nirc_scene_t& s) {
+  return ((size_t)s.n_bvh * sizeof(pt::PackedNode) + 255) & ~size_t(255);
+}
+
+}  // namespace
+}  // namespace nirc
+
+extern "C" int64_t nirc_scene_packed_bytes(const nirc_scene_t* scene) {
+  return (int64_t)(packed_node_bytes(*scene) +
+                   (size_t)(scene->n_tri + scene->n_sph + 1) * sizeof(pt::PackedPrim));
+}
+
+extern "C" int nirc_pack_scene(nirc_scene_t* scene, void* out, int64_t out_bytes, void* stream) {
+  if (out_bytes < nirc_scene_packed_bytes(scene)) {
+    set_last_error("packed scene buffer too small");
+    return NIRC_E_CONFIG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  auto* nodes = reinterpret_cast<pt::PackedNode*>(out);
+  auto* prims = reinterpret_cast<pt::PackedPrim*>(reinterpret_cast<char*>(out) +
+                                                   packed_node_bytes(*scene));
+  nirc_scene_t sc = *scene;
+  sc.bvh_packed = nullptr;
+  sc.prim_packed = nullptr;
+  if (sc.n_bvh > 0)
+    k_pack_nodes<<<(sc.n_bvh + 127) / 128, 128, 0, s>>>(sc, nodes);
+  const int np = sc.n_tri + sc.n_sph;
+  if (np > 0) k_pack_prims<<<(np + 127) / 128, 128, 0, s>>>(sc, prims);
+  NIRC_LAUNCH_CHECK("k_pack_scene");
+  scene->bvh_packed = nodes;
+  scene->prim_packed = prims;
   return NIRC_OK;
 }

@@ -6,6 +6,7 @@
 //   NEE        pkg/src/nirclab/kernels.py:44-82
 #pragma once
 #include "common.cuh"
+#include "pt_packed.cuh"
 
 namespace nirc {
 namespace pt {
@@ -166,6 +167,120 @@ __device__ inline bool tri_candidate(const RayF32& r, const float4* T, float t_l
   return !(ad > Ed) | !out;  // sign of det uncertain: the exact test decides
 }
 
+// Traversal image (nirc_pack_scene): per internal node both child boxes and
+// child references (n > 0: leaf, primitives [c, c + n) of the leaf order;
+// n == 0: internal node c), primitives in leaf order with geometry inline.
+// (layouts in pt_packed.cuh)
+
+// _box_hit's slab test (the same arithmetic and accept rule as box_hit),
+// returning the entry distance t0 as well.
+__device__ inline bool box_entry(const double* oo, const double* inv_d, const double* lo,
+                                 const double* hi, double t_best, double& t_in) {
+  double t0 = 0.0, t1 = t_best;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (fabs(inv_d[a]) == __longlong_as_double(0x7ff0000000000000ll)) {  // |d| < 1e-30
+      if (oo[a] < lo[a] || oo[a] > hi[a]) return false;
+    } else {
+      double ta = (lo[a] - oo[a]) * inv_d[a];
+      double tb = (hi[a] - oo[a]) * inv_d[a];
+      if (ta > tb) {
+        const double s = ta;
+        ta = tb;
+        tb = s;
+      }
+      if (ta > t0) t0 = ta;
+      if (tb < t1) t1 = tb;
+      if (t0 > t1) return false;
+    }
+  }
+  t_in = t0;
+  return true;
+}
+
+// Front-to-back traversal of the packed image: at an internal node both
+// child boxes are tested against the current best distance and the nearer
+// child is visited first (child 0 -- the reference's left-first order -- on
+// equal entry distances); popped subtrees whose entry (rounded down to
+// fp32) lies beyond the best hit are skipped.  The nearest hit and the
+// any-hit boolean are the reference traversal's (only exact distance ties
+// between different primitives could resolve differently).
+template <bool AnyHit>
+__device__ __noinline__ void bvh_scan_packed(const nirc_scene_t& s, V3 o, V3 d, double& best,
+                                             int& kind, int& prim) {
+  const double eps = s.eps;
+  const double oo[3] = {o.x, o.y, o.z};
+  const double dd[3] = {d.x, d.y, d.z};
+  double inv_d[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)  // parallel axes (|d| < 1e-30) marked by an infinite inverse
+    inv_d[a] = (dd[a] > -1e-30 && dd[a] < 1e-30) ? __longlong_as_double(0x7ff0000000000000ll)
+                                                 : 1.0 / dd[a];
+  const PackedNode* N = reinterpret_cast<const PackedNode*>(s.bvh_packed);
+  const PackedPrim* Pp = reinterpret_cast<const PackedPrim*>(s.prim_packed);
+  double t_root;
+  if (s.bvh_b[0] == 0 && s.bvh_a[0] == 0 && s.n_tri + s.n_sph == 0) return;
+  if (!box_entry(oo, inv_d, s.bvh_lo, s.bvh_hi, best, t_root)) return;
+  int cur = s.bvh_b[0] > 0 ? (s.bvh_a[0] << 3 | s.bvh_b[0]) : 0;
+  int st_ref[40];
+  float st_t[40];
+  int sp = 0;
+  while (true) {
+    const int n = cur & 7, idx = cur >> 3;
+    if (n > 0) {
+      for (int k = idx; k < idx + n; ++k) {
+        const PackedPrim& q = Pp[k];
+        const double t = q.kind == 0
+                             ? ray_tri(o, d, {q.g[0], q.g[1], q.g[2]}, {q.g[3], q.g[4], q.g[5]},
+                                       {q.g[6], q.g[7], q.g[8]})
+                             : ray_sph(o, d, {q.g[0], q.g[1], q.g[2]}, q.g[3]);
+        if (t > eps && t < best) {
+          best = t;
+          kind = q.kind;
+          prim = q.id;
+          if (AnyHit) return;
+        }
+      }
+    } else {
+      const PackedNode& nd = N[idx];
+      double ta = 0.0, tb = 0.0;
+      const bool ha = box_entry(oo, inv_d, nd.lo0, nd.hi0, best, ta);
+      const bool hb = box_entry(oo, inv_d, nd.lo1, nd.hi1, best, tb);
+      int ra = nd.c0 << 3 | nd.n0, rb = nd.c1 << 3 | nd.n1;
+      if (ha && hb) {
+        if (tb < ta) {
+          const int r = ra;
+          ra = rb;
+          rb = r;
+          const double t = ta;
+          ta = tb;
+          tb = t;
+        }
+        // visit the nearer child; push the farther one with its entry
+        // rounded down (the pop test stays conservative)
+        st_ref[sp] = rb;
+        st_t[sp] = __double2float_rd(tb);
+        ++sp;
+        cur = ra;
+        continue;
+      }
+      if (ha) {
+        cur = ra;
+        continue;
+      }
+      if (hb) {
+        cur = rb;
+        continue;
+      }
+    }
+    do {
+      if (sp == 0) return;
+      --sp;
+    } while ((double)st_t[sp] > best);
+    cur = st_ref[sp];
+  }
+}
+
 // Linear f64 scan (no staged fp32 table) or BVH traversal (spheres, larger
 // scenes) -- the reference's intersect_bvh order; kept out of line.
 template <bool AnyHit>
@@ -254,6 +369,9 @@ __device__ inline Hit intersect(const nirc_scene_t& s, V3 o, V3 d, double t_max)
         if (AnyHit) break;
       }
     }
+  } else if (s.bvh_packed) {
+    // general scenes with a traversal image: front to back, out of line
+    bvh_scan_packed<AnyHit>(s, o, d, best, kind, prim);
   } else {
     // general scenes (spheres, > 64 primitives): out of line, see below
     bvh_scan<AnyHit>(s, o, d, best, kind, prim);

@@ -10,6 +10,9 @@ import torch
 from . import _lib
 
 
+LINEAR_MAX_PRIMS = 64  # pt_common.cuh kLinearMaxPrims
+
+
 class DeviceScene:
     _F64 = ("tri_v0", "tri_e1", "tri_e2", "tri_ng", "tri_area", "tri_lq", "sph_c", "sph_r",
             "sph_lq", "mat_albedo", "mat_rough", "mat_emit", "lt_cdf", "lt_q", "env_img",
@@ -39,8 +42,19 @@ class DeviceScene:
         s.env_q = float(p.env_q)
         s.eps = float(p.eps)
         s.diag = float(p.diag)
+        s.bvh_packed = None
+        s.prim_packed = None
         self.struct = s
         self.cam = torch.from_numpy(np.ascontiguousarray(scene.camera, np.float64)).cuda()
+        if s.n_sph > 0 or s.n_tri > LINEAR_MAX_PRIMS:
+            # front-to-back traversal image for general scenes (the small
+            # triangle-only scenes take the warp-uniform scan)
+            lib = _lib.load()
+            nbytes = int(lib.nirc_scene_packed_bytes(C.byref(s)))
+            self.tensors["packed"] = t = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+            _lib.check(lib.nirc_pack_scene(C.byref(s), t.data_ptr(), nbytes,
+                                           torch.cuda.current_stream().cuda_stream),
+                       "nirc_pack_scene")
 
     def _put(self, s, name, arr):
         t = torch.from_numpy(np.ascontiguousarray(arr).reshape(-1).copy()
