@@ -648,10 +648,15 @@ struct WalkJob {
 #ifndef NIRC_TRACE_MINB
 #define NIRC_TRACE_MINB 3  // measured with the fp32 pre-test: 3 CTAs/SM (168 regs) beat 4 and 2
 #endif
+#ifndef NIRC_TRACE_MINB_BVH
+#define NIRC_TRACE_MINB_BVH 4  // BVH-traversed scenes: latency-bound, 4 CTAs/SM measured best
+#endif
 // kWalks: the launch also traces the frame's training walks (render+collect);
-// render-only launches are compiled without the walk lanes' state.
-template <bool kBiased, bool kWalks>
-__global__ void __launch_bounds__(128, NIRC_TRACE_MINB)
+// render-only launches are compiled without the walk lanes' state.  kMinB:
+// CTAs per SM the register budget is sized for (the warp-uniform scan of
+// small scenes wants registers, BVH traversal of larger ones wants warps).
+template <bool kBiased, bool kWalks, int kMinB>
+__global__ void __launch_bounds__(128, kMinB)
     k_trace(nirc_scene_t scn, const double* __restrict__ cam, nirc_render_cfg_t cfg, TraceOut out,
             WalkJob job) {
   __shared__ __align__(16) unsigned char scene_sm[pt::kSceneSmemBytes];
@@ -1336,10 +1341,17 @@ static int render_impl(const nirc_scene_t* scene, const double* cam, const nirc_
     return NIRC_OK;
   };
   int tst;
+  constexpr int kS = NIRC_TRACE_MINB, kB = NIRC_TRACE_MINB_BVH;
+  const bool bvh = scene->bvh_packed != nullptr;  // general scene: packed BVH traversal
   if (c.mode >= 2)
-    tst = job.n > 0 ? launch_trace(k_trace<true, true>) : launch_trace(k_trace<true, false>);
+    tst = job.n > 0 ? launch_trace(k_trace<true, true, kS>)
+                    : launch_trace(k_trace<true, false, kS>);
+  else if (bvh)
+    tst = job.n > 0 ? launch_trace(k_trace<false, true, kB>)
+                    : launch_trace(k_trace<false, false, kB>);
   else
-    tst = job.n > 0 ? launch_trace(k_trace<false, true>) : launch_trace(k_trace<false, false>);
+    tst = job.n > 0 ? launch_trace(k_trace<false, true, kS>)
+                    : launch_trace(k_trace<false, false, kS>);
   if (tst) return tst;
   NIRC_LAUNCH_CHECK("k_trace");
   if (tl) {
