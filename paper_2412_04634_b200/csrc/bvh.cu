@@ -308,9 +308,9 @@ extern "C" int nirc_build_bvh(const double* tri_v0, const double* tri_e1, const 
   const size_t b_cb = up((size_t)max_in * 6 * sizeof(uint64_t));
   const size_t total = b_pd + b_perm + b_keys + b_k2 + b_plan + b_nodes + b_ab + b_cb +
                        up(sort_bytes);
-  char* ws = nullptr;
-  NIRC_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ws), total, s));
-  char* q = ws;
+  AsyncBuf wsb(s);
+  NIRC_CUDA_TRY(wsb.alloc(total));
+  char* q = static_cast<char*>(wsb.p);
   double* plo = reinterpret_cast<double*>(q);
   double* phi = plo + 3 * P;
   double* cent = phi + 3 * P;
@@ -379,7 +379,6 @@ extern "C" int nirc_build_bvh(const double* tri_v0, const double* tri_e1, const 
   NIRC_CUDA_TRY(cudaMemcpyAsync(a, d_a, N * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
   NIRC_CUDA_TRY(cudaMemcpyAsync(b, d_b, N * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
   NIRC_CUDA_TRY(cudaMemcpyAsync(prim, perm, P * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-  NIRC_CUDA_TRY(cudaFreeAsync(ws, s));
   // the host plan vectors are read by the async copies above
   NIRC_CUDA_TRY(cudaStreamSynchronize(s));
   return NIRC_OK;

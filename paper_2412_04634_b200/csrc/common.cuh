@@ -310,6 +310,20 @@ int check_cuda(cudaError_t e, const char* what);
     if (_e != cudaSuccess) return nirc::check_cuda(_e, #expr);     \
   } while (0)
 
+// Stream-ordered temporary: cudaFreeAsync on every exit path of the entry
+// point that allocated it (early error returns included).
+struct AsyncBuf {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  explicit AsyncBuf(cudaStream_t st) : s(st) {}
+  AsyncBuf(const AsyncBuf&) = delete;
+  AsyncBuf& operator=(const AsyncBuf&) = delete;
+  cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes, s); }
+  ~AsyncBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
 #define NIRC_LAUNCH_CHECK(what)                                    \
   do {                                                             \
     cudaError_t _e = cudaGetLastError();                           \

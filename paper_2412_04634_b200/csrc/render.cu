@@ -1394,9 +1394,9 @@ static int render_impl(const nirc_scene_t* scene, const double* cam, const nirc_
     if (ng == 0) {
       // generic layouts: SIMT rows into a row buffer, then per-vertex combine
       const int64_t cap = ns * c.max_cv;
-      double* rowbuf = nullptr;
-      NIRC_CUDA_TRY(cudaMallocAsync((void**)&rowbuf, (size_t)cap * R * 24 + 24, s));
-      a.rowbuf = rowbuf;
+      AsyncBuf rowbuf(s);
+      NIRC_CUDA_TRY(rowbuf.alloc((size_t)cap * R * 24 + 24));
+      a.rowbuf = static_cast<double*>(rowbuf.p);
       const size_t sm = (size_t)(spec->theta_len - spec->grid_len) * 4;
       NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)k_infer_simt,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -1404,7 +1404,6 @@ static int render_impl(const nirc_scene_t* scene, const double* cam, const nirc_
       NIRC_LAUNCH_CHECK("k_infer_simt");
       k_combine_rows<<<(int)((cap + 127) / 128), 128, 0, s>>>(a);
       NIRC_LAUNCH_CHECK("k_combine_rows");
-      NIRC_CUDA_TRY(cudaFreeAsync(rowbuf, s));
     }
   }
   const int64_t npix = (int64_t)(c.row1 - c.row0) * c.width;
@@ -1792,10 +1791,10 @@ extern "C" int nirc_incident_targets(const nirc_scene_t* scene, uint64_t seed, u
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   size_t bytes = 0;
   carve_stage(count, nullptr, &bytes);
-  void* ws = nullptr;
-  NIRC_CUDA_TRY(cudaMallocAsync(&ws, bytes, s));
+  AsyncBuf ws(s);
+  NIRC_CUDA_TRY(ws.alloc(bytes));
   size_t b2 = 0;
-  Stage st = carve_stage(count, ws, &b2);
+  Stage st = carve_stage(count, ws.p, &b2);
   st.kind = REC_NIRC;
   const V3 o = {origin_host[0], origin_host[1], origin_host[2]};
   const V3 d = {dir_host[0], dir_host[1], dir_host[2]};
@@ -1803,7 +1802,6 @@ extern "C" int nirc_incident_targets(const nirc_scene_t* scene, uint64_t seed, u
   k_incident_targets<<<(count + 63) / 64, 64, 0, s>>>(*scene, seed, frame, o, d, prev_pdf, pns,
                                                       count, st, out, out_full);
   NIRC_LAUNCH_CHECK("k_incident_targets");
-  NIRC_CUDA_TRY(cudaFreeAsync(ws, s));
   return NIRC_OK;
 }
 
@@ -1826,10 +1824,10 @@ extern "C" int nirc_integrand_samples(const nirc_scene_t* scene, const double* c
   const int64_t chunk = total < (int64_t(1) << 18) ? total : (int64_t(1) << 18);
   size_t bytes = 0;
   carve_stage(chunk, nullptr, &bytes);
-  void* ws = nullptr;
-  NIRC_CUDA_TRY(cudaMallocAsync(&ws, bytes, s));
+  AsyncBuf ws(s);
+  NIRC_CUDA_TRY(ws.alloc(bytes));
   size_t b2 = 0;
-  Stage st = carve_stage(chunk, ws, &b2);
+  Stage st = carve_stage(chunk, ws.p, &b2);
   st.kind = REC_NIRC;
   for (int64_t q0 = 0; q0 < total; q0 += chunk) {
     const int64_t n = total - q0 < chunk ? total - q0 : chunk;
@@ -1838,7 +1836,6 @@ extern "C" int nirc_integrand_samples(const nirc_scene_t* scene, const double* c
         o_spos, o_sns, o_salb, o_srough);
     NIRC_LAUNCH_CHECK("k_integrand_samples");
   }
-  NIRC_CUDA_TRY(cudaFreeAsync(ws, s));
   return NIRC_OK;
 }
 
