@@ -274,6 +274,62 @@ def frame_bench(frames, warmup, width=1920, height=1080, nc=(16,), comm=None, na
     }
 
 
+def frame_bench_overlap(frames, warmup, width=1920, height=1080, nc=(16,), name="cfg3"):
+    """The same frame as frame_bench on one GPU through frame.FramePipeline:
+    render(f) (+ the walks collecting frame f+1's records) on the render
+    stream while train(f) runs on a second stream against a theta_f snapshot
+    (SURVEY.md 8(e)).  Frame time = device time from the frame's start on
+    the render stream to the later of the two streams' ends (CUDA events)."""
+    import torch
+
+    from paper_2412_04634_b200.caches import Cache
+    from paper_2412_04634_b200.frame import FramePipeline, config3
+    from paper_2412_04634_b200.scene import load_builtin
+
+    scene = load_builtin("cornell").with_resolution(width, height)
+    cache = Cache.create("nirc", scene, seed=0, init="random")
+    pipe = FramePipeline(scene, cache, config3(nc), seed=0)
+    frame_ms, render_ms, train_ms, queries, records = [], [], [], [], []
+    for f in range(warmup + frames):
+        e0, er = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(pipe.s_render)
+        _, st = pipe.step(f)
+        er.record(pipe.s_render)
+        torch.cuda.synchronize()
+        if f >= warmup:
+            r = e0.elapsed_time(er)
+            t = 0.0
+            end = r
+            if pipe.train_events is not None:
+                t0, t1 = pipe.train_events
+                t = t0.elapsed_time(t1)
+                end = max(r, e0.elapsed_time(t1))
+            frame_ms.append(end)
+            render_ms.append(r)
+            train_ms.append(t)
+            queries.append(st.queries)
+            records.append(st.records)
+    med = lambda v: sorted(v)[len(v) // 2]  # noqa: E731
+    return {
+        "metric": f"ms_per_frame_{width}x{height}", "value": med(frame_ms), "unit": "ms/frame",
+        "higher_is_better": False, "frames": frames, "warmup": warmup, "n_gpus": 1,
+        "render_collect_ms": med(render_ms), "train_stream_span_ms": med(train_ms),
+        "queries_per_frame": queries[-1], "records_per_frame": records[-1],
+        "render_queries_per_sec": queries[-1] / (med(render_ms) * 1e-3),
+        "phases": "render_collect = the render stream (snapshot copy, one nirc_render_collect "
+                  "launch set: path tracer with the NEXT frame's training walks as its first "
+                  "work items, fused inference, accumulation, record compaction); "
+                  "train_stream_span = first to last event of the train stream (4 steps on "
+                  "this frame's records), which shares the SMs with the render stream -- its "
+                  "kernels' own time is the sequential leg's train_ms",
+        "overlap": True,
+        "config": f"{name}: cornell {width}x{height}, two-level nc={tuple(nc)}, spp 1, D=4 "
+                  f"cache, collect 0.025 W H paths, 4 x min(16384, records) train steps; "
+                  "render(f) || train(f) (frame.FramePipeline)",
+        "reference_cpu_context": "SURVEY.md 6: 122.6 s/frame on 1 core (not re-timed here)",
+    }
+
+
 def convergence_bench(frames=100, width=1920, height=1080, ref_spp=64):
     """BASELINE config 4: the teleport scene (its lamp jumps at frame 40) at
     1920x1080, `frames` frames of continuous online training with the cfg3
@@ -436,15 +492,27 @@ def run_b200(args, rank, world, local_rank):
         from paper_2412_04634_b200 import distributed as D
 
         comm = D.Comm() if world > 1 else None
-        fb = frame_bench(args.frame_steps, 3, comm=comm)
+        if world == 1:
+            # one GPU: render(f) || train(f) (frame.FramePipeline); the
+            # sequential loop's numbers ride along for comparison
+            fb = frame_bench_overlap(args.frame_steps, 3)
+            fb["sequential"] = frame_bench(args.frame_steps, 3)
+        else:
+            fb = frame_bench(args.frame_steps, 3, comm=comm)
         if not args.no_extra_frames:
             # BASELINE cfg5 (4K, 32 NIRC samples/pixel as nc=(16,16): the
             # reference caps N_c at 28 per vertex) and cfg1 (the reference's
             # CPU-runnable 128^2 frame), both sharded like cfg3 when N > 1
-            fb["cfg5_4k"] = frame_bench(max(3, args.frame_steps // 2), 2, 3840, 2160, (16, 16),
-                                        comm=comm, name="cfg5")
-            fb["cfg1_128"] = frame_bench(args.frame_steps, 3, 128, 128, (8,), comm=comm,
-                                         name="cfg1")
+            if world == 1:
+                fb["cfg5_4k"] = frame_bench_overlap(max(3, args.frame_steps // 2), 2, 3840,
+                                                    2160, (16, 16), name="cfg5")
+                fb["cfg1_128"] = frame_bench_overlap(args.frame_steps, 3, 128, 128, (8,),
+                                                     name="cfg1")
+            else:
+                fb["cfg5_4k"] = frame_bench(max(3, args.frame_steps // 2), 2, 3840, 2160,
+                                            (16, 16), comm=comm, name="cfg5")
+                fb["cfg1_128"] = frame_bench(args.frame_steps, 3, 128, 128, (8,), comm=comm,
+                                             name="cfg1")
             fb["cfg1_128"]["reference_cpu_context"] = (
                 "SURVEY.md 6: 1.28 s/frame for cfg1 on 1 core (render 1084 + collect 12 + "
                 "train 179 ms)")

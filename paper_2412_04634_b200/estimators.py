@@ -126,12 +126,13 @@ def _v1_device(v1_map, w, h):
 
 
 def render_device(scene, config=None, cache=None, seed=0, spp=1, frame=0, force_cache=False,
-                  rows=None, out=None, precision=None, v1_map=None):
+                  rows=None, out=None, precision=None, v1_map=None, theta=None):
     """Device-resident render: returns (img, img2, term, queries) CUDA
     tensors of sums (callers divide by spp).  ``rows`` renders a band of
     pixel rows (multi-GPU tiles); ``out`` accumulates into given buffers;
     ``v1_map`` flags the pixels where the *_sph modes may stop at the first
-    vertex (estimators.py:173-217)."""
+    vertex (estimators.py:173-217); ``theta`` renders with a snapshot buffer
+    of the cache's layout instead of cache.theta."""
     if config is None:
         config = EstimatorConfig()
     mode = MODES[config.mode]
@@ -153,7 +154,7 @@ def render_device(scene, config=None, cache=None, seed=0, spp=1, frame=0, force_
     ws = _RenderWs.get(lib.nirc_render_workspace_bytes(C.byref(cfg)))
     if cache_on:
         cs = _lib.make_c_spec(cache.spec)
-        spec_p, theta_p = C.byref(cs), _dev.ptr(cache.theta)
+        spec_p, theta_p = C.byref(cs), _dev.ptr(cache.theta if theta is None else theta)
     else:
         spec_p, theta_p = None, None
     _lib.check(lib.nirc_render(ds.ptr(), _dev.ptr(ds.cam), C.byref(cfg), spec_p, theta_p,
@@ -163,13 +164,17 @@ def render_device(scene, config=None, cache=None, seed=0, spp=1, frame=0, force_
 
 
 def render_and_collect(scene, config, cache, seed=0, spp=1, frame=0, count=None,
-                       train_frame=None, rows=None, paths=None, out=None, precision=None):
+                       train_frame=None, rows=None, paths=None, out=None, precision=None,
+                       theta=None, defer=False):
     """render_device + cache.collect of the same frame in ONE device pass
     (C ABI nirc_render_collect: the training walks are the first work items
     of the persistent path tracer).  Equivalent to calling render_device and
     then collect_training_records(scene, cache.seed, count, cache.record_kind,
     train_frame).  ``paths`` = (p0, p1) collects a path shard (multi-GPU).
-    Returns (img, img2, term, queries, records_packed_or_Records)."""
+    ``theta`` renders with another parameter buffer of the cache's layout
+    (a snapshot); ``defer`` returns a callable that yields the Records once
+    the launch is done instead of waiting for the record count here.
+    Returns (img, img2, term, queries, Records or its callable)."""
     from .caches import Records, default_train_count
     from .records import _KIND, _check_kind, record_buffers
 
@@ -198,16 +203,20 @@ def render_and_collect(scene, config, cache, seed=0, spp=1, frame=0, count=None,
     rec_out, ro = record_buffers(max(p1 - p0, 1))
     ws = _RenderWs.get(lib.nirc_render_collect_workspace_bytes(C.byref(cfg), max(p1 - p0, 1)))
     cs = _lib.make_c_spec(cache.spec)
+    th = cache.theta if theta is None else theta
     _lib.check(lib.nirc_render_collect(
         ds.ptr(), _dev.ptr(ds.cam), C.byref(cfg), C.byref(cs) if cache_on else None,
-        _dev.ptr(cache.theta) if cache_on else None, _dev.ptr(img), _dev.ptr(img2),
+        _dev.ptr(th) if cache_on else None, _dev.ptr(img), _dev.ptr(img2),
         _dev.ptr(term), _dev.ptr(queries), int(cache.seed), int(train_frame), p0,
         max(p1 - p0, 1), _KIND[cache.record_kind], C.byref(ro), _dev.ptr(n_out), _dev.ptr(ws),
         int(ws.numel()), _dev.stream()), "nirc_render_collect")
-    n = int(n_out.item()) if p1 > p0 else 0
-    rec = Records(kind=cache.record_kind, frame=train_frame, n=n,
-                  **{k: v[:n] for k, v in rec_out.items()})
-    return img, img2, term, queries, rec
+
+    def finish():
+        n = int(n_out.item()) if p1 > p0 else 0
+        return Records(kind=cache.record_kind, frame=train_frame, n=n,
+                       **{k: v[:n] for k, v in rec_out.items()})
+
+    return img, img2, term, queries, (finish if defer else finish())
 
 
 def render(scene, config=None, cache=None, seed=0, spp=1, frame=0, v1_map=None,
