@@ -334,7 +334,8 @@ def convergence_bench(frames=100, width=1920, height=1080, ref_spp=64):
     """BASELINE config 4: the teleport scene (its lamp jumps at frame 40) at
     1920x1080, `frames` frames of continuous online training with the cfg3
     estimator ("as cfg 3 per frame") through the device frame
-    loop (frame.run_frame = experiment.py:149-185's render / collect / train),
+    loop (frame.FramePipeline: experiment.py:149-185's render / collect / train
+    with render(f) || train(f)),
     MRSE per frame against a ref_spp device-PT reference of each geometry
     state (experiment.py's _ReferenceBank), computed on the device."""
     import torch
@@ -342,7 +343,7 @@ def convergence_bench(frames=100, width=1920, height=1080, ref_spp=64):
     from paper_2412_04634_b200.config import RunConfig
     from paper_2412_04634_b200.estimators import EstimatorConfig, render_device
     from paper_2412_04634_b200.experiment import REF_SEED_OFFSET, _make_cache
-    from paper_2412_04634_b200.frame import config3, run_frame
+    from paper_2412_04634_b200.frame import FramePipeline, config3
     from paper_2412_04634_b200.scene import load_builtin
 
     rc = RunConfig(scene="teleport", mode="two-level", nc=(16,), max_cache_vertices=1,
@@ -350,12 +351,12 @@ def convergence_bench(frames=100, width=1920, height=1080, ref_spp=64):
     scene = load_builtin("teleport").with_resolution(width, height)
     cache = _make_cache(rc, scene)
     est = config3((16,))
-    stream = torch.cuda.current_stream()
+    pipe = FramePipeline(scene, cache, est, rc.seed)
+    stream = pipe.s_render
     refs, ref_ms = {}, 0.0
     ms, mrse = [], []
     for f in range(frames):
         scene = scene.at_frame(f)
-        cache.scene = scene
         key = scene.content_hash()
         if key not in refs:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -368,7 +369,8 @@ def convergence_bench(frames=100, width=1920, height=1080, ref_spp=64):
             refs[key] = img / ref_spp
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        (img, _, _), _ = run_frame(scene, cache, est, rc.seed, f)
+        (img, _, _), _ = pipe.step(f)
+        stream.wait_stream(pipe.s_train)
         e1.record(stream)
         ref = refs[key]
         mrse.append(torch.mean((img - ref) ** 2 / (ref * ref + 0.01)))
