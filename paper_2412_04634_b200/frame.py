@@ -85,10 +85,11 @@ class FramePipeline:
     def step(self, frame, out=None):
         """Frame `frame`: returns ((img, img2, term), FrameStats)."""
         cache = self.cache
-        scene = self.scene.at_frame(frame)
+        scene = self.scene = self.scene.at_frame(frame)  # a new object only at a boundary
         cache.scene = scene
-        nxt = self.scene.at_frame(frame + 1)
-        same_geometry = nxt is scene or nxt.content_hash() == scene.content_hash()
+        # does an animation fire between this frame and the next?
+        same_geometry = not any((a.frame <= frame + 1) != (a.frame <= frame)
+                                for a in scene.desc.anims)
         if self.pending is not None and self.pending[0] == frame:
             rec = self.pending[1]
             rec = rec() if callable(rec) else rec
@@ -104,7 +105,7 @@ class FramePipeline:
         if same_geometry:
             img, img2, term, queries, nxt_rec = render_and_collect(
                 scene, self.config, cache, self.seed, self.spp, frame,
-                count=self._count(nxt), train_frame=frame + 1, out=out, theta=self.theta_r,
+                count=self._count(scene), train_frame=frame + 1, out=out, theta=self.theta_r,
                 defer=True)
             self.pending = (frame + 1, nxt_rec)
         else:
