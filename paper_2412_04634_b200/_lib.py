@@ -84,6 +84,7 @@ class NircScene(C.Structure):
         ("bvh_a", C.c_void_p), ("bvh_b", C.c_void_p), ("bvh_prim", C.c_void_p),
         ("tri_f32", C.c_void_p),
         ("bvh_packed", C.c_void_p), ("prim_packed", C.c_void_p),
+        ("filter_items", C.c_void_p), ("n_filter", C.c_int32), ("pad_filter", C.c_int32),
     ]
 
 

@@ -134,8 +134,14 @@ __device__ inline RayF32 ray_f32(V3 o, V3 d) {
   r.no = (fabsf(r.ox) + fabsf(r.oy) + fabsf(r.oz)) * 1.0001f;
   return r;
 }
+// One scan item: a triangle (cu = 1: u, v >= 0, u + v <= 1) or a
+// parallelogram v0 + u e1 + v e2 (cu = 0: u, v in [0, 1]) covering two
+// scan-order triangles (v0, e1, e1 + e2) and (v0, e1 + e2, e2) -- their
+// union, so the test stays conservative for both.  `slack` is the
+// barycentric tolerance the item needs (the reference's 1e-9, doubled for a
+// parallelogram whose triangles carry it in their own coordinates).
 __device__ inline bool tri_candidate(const RayF32& r, const float4* T, float t_lo, float t_hi) {
-  const float4 A = T[0], B = T[1], C = T[2];
+  const float4 A = T[0], B = T[1], C = T[2], D = T[3];
   const float px = r.dy * C.z - r.dz * C.y;
   const float py = r.dz * C.x - r.dx * C.z;
   const float pz = r.dx * C.y - r.dy * C.x;
@@ -157,14 +163,22 @@ __device__ inline bool tri_candidate(const RayF32& r, const float4* T, float t_l
   const float sgn = det > 0.0f ? 1.0f : -1.0f;
   const float u = un * sgn, v = vn * sgn, t = tn * sgn;
   const float hi = ad + Ed, lo = ad - Ed;
+  const float cu = D.x, sl = D.y;
   // branch-free: every condition is a predicate, the scan loop stays straight
-  const bool out = (u + Eu < -1.000001e-9f * hi) |        // u < -1e-9
-                   (u - Eu > 1.000001f * hi) |            // u > 1 + 1e-9
-                   (v + Ev < -1.000001e-9f * hi) |        // v < -1e-9
-                   (u + v - Eu - Ev > 1.000001f * hi) |   // u + v > 1 + 1e-9
-                   (t + Et < t_lo * lo * 0.999999f) |     // t <= t_lo (t_lo > 0)
-                   (t - Et > t_hi * hi * 1.000001f);      // t >= t_hi (inf: never)
+  const bool out = (u + Eu < -sl * hi) |                        // u < -slack
+                   (u - Eu > (1.0f + sl) * hi) |                // u > 1 + slack
+                   (v + Ev < -sl * hi) |                        // v < -slack
+                   (v - Ev > (1.0f + 2.0f * sl) * hi) |         // v > 1 + 2 slack
+                   (cu * (u - Eu) + v - Ev > (1.0f + sl) * hi) |  // u + v > 1 + slack
+                   (t + Et < t_lo * lo * 0.999999f) |           // t <= t_lo (t_lo > 0)
+                   (t - Et > t_hi * hi * 1.000001f);            // t >= t_hi (inf: never)
   return !(ad > Ed) | !out;  // sign of det uncertain: the exact test decides
+}
+// scan-order triangles an item covers, as a candidate bit mask
+__device__ inline uint64_t item_bits(const float4* T) {
+  const uint32_t b = __float_as_uint(T[3].z);
+  const uint64_t k1 = b & 0xffu, k2 = (b >> 8) & 0xffu;
+  return (1ull << k1) | ((b >> 16) & 1u ? (1ull << k2) : 0ull);
 }
 
 // Traversal image (nirc_pack_scene): per internal node both child boxes and
@@ -348,15 +362,15 @@ __device__ inline Hit intersect(const nirc_scene_t& s, V3 o, V3 d, double t_max)
     // warp-uniform fp32 pre-test over the scan order, then ray_tri (f64,
     // the reference's arithmetic) on each lane's own candidates in scan
     // order: the accepted hit (and any-hit boolean) equal the full scan's
-    const int np = s.n_tri;
+    const int ni = s.n_filter;
     const RayF32 r = ray_f32(o, d);
     const float4* T = reinterpret_cast<const float4*>(s.tri_f32);
     const float f_lo = (float)eps;
     const float f_hi = t_max < 1e29 ? (float)t_max : __int_as_float(0x7f800000);
     uint64_t cand = 0;
 #pragma unroll(kFilterUnroll)
-    for (int k = 0; k < np; ++k)
-      cand |= (uint64_t)tri_candidate(r, T + 3 * k, f_lo, f_hi) << k;
+    for (int k = 0; k < ni; ++k)
+      cand |= tri_candidate(r, T + 4 * k, f_lo, f_hi) ? item_bits(T + 4 * k) : 0ull;
     while (cand) {
       const int k = __ffsll((long long)cand) - 1;
       cand &= cand - 1;
@@ -752,7 +766,7 @@ constexpr int kSceneSmemBytes = 40 * 1024;
 __host__ __device__ inline size_t scene_smem_bytes(const nirc_scene_t& s) {
   return (size_t)s.n_tri * (4 * 3 * 8 + 4) + (size_t)s.n_sph * (4 * 8 + 4) +
          (size_t)s.n_bvh * (6 * 8 + 8) + (size_t)(s.n_tri + s.n_sph) * 4 + 64 +
-         (size_t)s.n_tri * 48 + 16;  // fp32 filter table
+         (size_t)s.n_tri * 64 + 16;  // fp32 filter table
 }
 
 __device__ inline void stage_scene(nirc_scene_t& s, unsigned char* sm) {
@@ -790,22 +804,31 @@ __device__ inline void stage_scene(nirc_scene_t& s, unsigned char* sm) {
     uintptr_t a = reinterpret_cast<uintptr_t>(ip);
     a = (a + 15) & ~(uintptr_t)15;
     float* f = reinterpret_cast<float*>(a);
-    __syncthreads();  // the staged doubles / prim order are read below
-    for (int k = threadIdx.x; k < s.n_tri; k += blockDim.x) {
-      const int pid = s.bvh_prim[k];
-      const double* v0 = s.tri_v0 + 3 * pid;
-      const double* e1 = s.tri_e1 + 3 * pid;
-      const double* e2 = s.tri_e2 + 3 * pid;
-      float* row = f + 12 * k;
-      for (int c = 0; c < 3; ++c) {
-        row[c] = (float)v0[c];
-        row[4 + c] = (float)e1[c];
-        row[8 + c] = (float)e2[c];
+    if (s.filter_items) {  // host-built items (paired parallelograms)
+      for (int i = threadIdx.x; i < 16 * s.n_filter; i += blockDim.x) f[i] = s.filter_items[i];
+    } else {
+      __syncthreads();  // the staged doubles / prim order are read below
+      for (int k = threadIdx.x; k < s.n_tri; k += blockDim.x) {
+        const int pid = s.bvh_prim[k];
+        const double* v0 = s.tri_v0 + 3 * pid;
+        const double* e1 = s.tri_e1 + 3 * pid;
+        const double* e2 = s.tri_e2 + 3 * pid;
+        float* row = f + 16 * k;
+        for (int c = 0; c < 3; ++c) {
+          row[c] = (float)v0[c];
+          row[4 + c] = (float)e1[c];
+          row[8 + c] = (float)e2[c];
+        }
+        // L1 norms of the fp32-rounded vectors, rounded up
+        row[3] = (fabsf(row[4]) + fabsf(row[5]) + fabsf(row[6])) * 1.0001f;
+        row[7] = (fabsf(row[8]) + fabsf(row[9]) + fabsf(row[10])) * 1.0001f;
+        row[11] = (fabsf(row[0]) + fabsf(row[1]) + fabsf(row[2])) * 1.0001f;
+        row[12] = 1.0f;            // triangle
+        row[13] = 1.000001e-9f;    // the reference's barycentric slack
+        row[14] = __uint_as_float((uint32_t)k);
+        row[15] = 0.0f;
       }
-      // L1 norms of the fp32-rounded vectors, rounded up
-      row[3] = (fabsf(row[4]) + fabsf(row[5]) + fabsf(row[6])) * 1.0001f;
-      row[7] = (fabsf(row[8]) + fabsf(row[9]) + fabsf(row[10])) * 1.0001f;
-      row[11] = (fabsf(row[0]) + fabsf(row[1]) + fabsf(row[2])) * 1.0001f;
+      s.n_filter = s.n_tri;
     }
     s.tri_f32 = f;
   }
