@@ -164,6 +164,15 @@ int nirc_full_forward(const nirc_spec_t* spec, const float* theta,
                       const double* dirs, int64_t n, float* Y,
                       int32_t precision, void* stream);
 
+/* Cache._query / nirc_query (pkg/src/nirclab/caches.py:211-233): n_dirs
+ * directions, direction i against surface dir_to_surf[i]; surf rows
+ * (n_surf, 10) = pos.xyz, ns.xyz, albedo.rgb, roughness (device f64);
+ * dirs (n_dirs, 3) f64; Y (n_dirs, dout) f32; precision as nirc_full_forward.
+ * NIRC_E_CONFIG for an index outside [0, n_surf) (synchronises the stream). */
+int nirc_query(const nirc_spec_t* spec, const float* theta, const double* surf,
+               int64_t n_surf, const double* dirs, const int32_t* dir_to_surf,
+               int64_t n_dirs, float* Y, int32_t precision, void* stream);
+
 /* ---- losses (pkg/src/nirclab/losses.py) --------------------------------- */
 /* kind: 0 l2, 1 relative_l2, 2 variance, 3 bce.  Y (n,3) f32, target (n,3)
  * f64, pdf (n,) f64 (unused for bce), running_mean (3,) f64 (variance).

@@ -142,6 +142,7 @@ SIGNATURES = {
                                     P]),
     "nirc_integrand_samples": (I32, [C.POINTER(NircScene), P, U64, U64, I32, P, P, P, P, P, P,
                                      P, P, P, P]),
+    "nirc_query": (I32, [SPEC, P, P, I64, P, P, I64, P, I32, P]),
     "nirc_bvh_node_count": (I64, [I64]),
     "nirc_scene_packed_bytes": (I64, [C.POINTER(NircScene)]),
     "nirc_pack_scene": (I32, [C.POINTER(NircScene), P, I64, P]),

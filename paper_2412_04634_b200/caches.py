@@ -248,17 +248,16 @@ class Cache:
 
     # -- queries ---------------------------------------------------------
     def _query(self, surface, dirs):
-        from .mlp import full_forward
+        """caches.py:211-233: one surface, N directions (C ABI nirc_query)."""
+        from .mlp import query
 
         pack = self.scene.pack
         m = surface.mat
         dirs = np.atleast_2d(np.asarray(dirs, float))
-        n = dirs.shape[0]
-        pos = np.tile(np.asarray(surface.position, float), (n, 1))
-        ns = np.tile(np.asarray(surface.ns, float), (n, 1))
-        alb = np.tile(np.asarray(pack.mat_albedo[m], float), (n, 1))
-        rough = np.full(n, float(pack.mat_rough[m]))
-        y = full_forward(self.spec, self.theta, pos, ns, alb, rough, dirs)
+        surf = np.concatenate([np.asarray(surface.position, float), np.asarray(surface.ns, float),
+                               np.asarray(pack.mat_albedo[m], float),
+                               [float(pack.mat_rough[m])]])[None, :]
+        y = query(self.spec, self.theta, surf, dirs, np.zeros(dirs.shape[0], np.int32))
         return np.asarray(y, np.float64)
 
     def nirc_query(self, surface, dirs):

@@ -319,3 +319,63 @@ extern "C" int nirc_full_forward(const nirc_spec_t* spec, const float* theta, co
   NIRC_LAUNCH_CHECK("k_full_forward_tc");
   return NIRC_OK;
 }
+
+// ---------------------------------------------------------------------
+// Cache._query / nirc_query (caches.py:211-233): directions against a set
+// of shared surfaces.  Each direction's surface row (pos, ns, albedo,
+// roughness) is gathered next to it and the rows go through the fused
+// encode + MLP kernel; directions of one surface hit the same hash cells, so
+// their repeated gathers are L1 hits.
+namespace nirc {
+__global__ void k_gather_surfaces(const double* __restrict__ surf, int64_t n_surf,
+                                  const int32_t* __restrict__ dir_to_surf, int64_t n,
+                                  double* pos, double* ns, double* alb, double* rough,
+                                  int32_t* bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t k = dir_to_surf[i];
+  if (k < 0 || k >= n_surf) {
+    atomicOr(bad, 1);
+    return;
+  }
+  const double* r = surf + 10 * (int64_t)k;
+  for (int c = 0; c < 3; ++c) {
+    pos[3 * i + c] = r[c];
+    ns[3 * i + c] = r[3 + c];
+    alb[3 * i + c] = r[6 + c];
+  }
+  rough[i] = r[9];
+}
+}  // namespace nirc
+
+extern "C" int nirc_query(const nirc_spec_t* spec, const float* theta, const double* surf,
+                          int64_t n_surf, const double* dirs, const int32_t* dir_to_surf,
+                          int64_t n_dirs, float* Y, int32_t precision, void* stream) {
+  if (!spec) return NIRC_E_CONFIG;
+  if (n_dirs <= 0) return NIRC_OK;
+  if (n_surf <= 0) {
+    set_last_error("directions given without surfaces");
+    return NIRC_E_CONFIG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  AsyncBuf buf(s);
+  NIRC_CUDA_TRY(buf.alloc((size_t)n_dirs * 10 * sizeof(double) + 16));
+  double* pos = static_cast<double*>(buf.p);
+  double* ns = pos + 3 * n_dirs;
+  double* alb = ns + 3 * n_dirs;
+  double* rough = alb + 3 * n_dirs;
+  int32_t* bad = reinterpret_cast<int32_t*>(rough + n_dirs);
+  NIRC_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int32_t), s));
+  k_gather_surfaces<<<(unsigned)((n_dirs + 255) / 256), 256, 0, s>>>(surf, n_surf, dir_to_surf,
+                                                                   n_dirs, pos, ns, alb, rough,
+                                                                   bad);
+  NIRC_LAUNCH_CHECK("k_gather_surfaces");
+  int32_t h_bad = 0;
+  NIRC_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  NIRC_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h_bad) {
+    set_last_error("dir_to_surf index outside [0, n_surf)");
+    return NIRC_E_CONFIG;
+  }
+  return nirc_full_forward(spec, theta, pos, ns, alb, rough, dirs, n_dirs, Y, precision, stream);
+}

@@ -209,6 +209,33 @@ def _full_forward_pipelined(spec, th, host, precision, out=None, chunk=1 << 19):
     return y_host
 
 
+def query(spec, theta, surf, dirs, dir_to_surf, precision=PRECISION_F16X2):
+    """Directions against shared surfaces (Cache._query, caches.py:211-233,
+    batched): surf (n_s, 10) rows pos.xyz | ns.xyz | albedo.rgb | roughness,
+    dirs (n, 3), dir_to_surf (n,) -> (n, dout) f32, through the C ABI's
+    nirc_query (surface rows gathered on the device, fused encode + MLP).
+    numpy in -> numpy out; CUDA tensors stay on the device."""
+    host = _dev.is_host(dirs)
+    th = _dev.dev(theta, torch.float32)
+    S = _dev.dev(surf, torch.float64)
+    D = _dev.dev(dirs, torch.float64)
+    idx = _dev.dev(dir_to_surf, torch.int32)
+    n = int(D.shape[0])
+    Y = _dev.empty((n, int(spec.dims[-1])), torch.float32)
+    if n:
+        lib = _lib.load()
+        st = lib.nirc_query(_lib.make_c_spec(spec), _dev.ptr(th), _dev.ptr(S), int(S.shape[0]),
+                            _dev.ptr(D), _dev.ptr(idx), n, _dev.ptr(Y), int(precision),
+                            _dev.stream())
+        if st == _lib.NIRC_E_UNSUPPORTED:  # non-default layouts: generic device path
+            il = idx.long()
+            Y = full_forward(spec, th, S[il, 0:3], S[il, 3:6], S[il, 6:9], S[il, 9], D,
+                             precision=precision)
+        else:
+            _lib.check(st, "nirc_query")
+    return Y.cpu().numpy() if host else Y
+
+
 def full_forward(spec, theta, pos, normal, albedo, rough, dirs, training=False,
                  precision=PRECISION_F16X2, out=None):
     """encode_batch + mlp_forward (mlp.py:216-224).  Inference runs the fused

@@ -135,3 +135,35 @@ def test_estimate_env_direct_matches_reference(golden):
     box = load_scene(BOX)
     with pytest.raises(ConfigError):
         estimate_env_direct(box, Cache.create("nirc", box, seed=1), _floor(box))
+
+
+def test_query_batches_surfaces():
+    """nirc_query (Cache._query batched over surfaces, caches.py:211-233):
+    bit-identical to full_forward on the gathered rows; a bad surface index
+    is a ConfigError."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2412_04634_b200.errors import ConfigError
+    from paper_2412_04634_b200.mlp import full_forward, init_theta, make_spec, query
+
+    spec = make_spec(depth=4)
+    theta = init_theta(spec, seed=4, out_scale=0.2)
+    rng = np.random.default_rng(5)
+    ns_ = 37
+    nrm = rng.normal(size=(ns_, 3))
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    surf = np.concatenate([rng.uniform(size=(ns_, 3)), nrm, rng.uniform(size=(ns_, 3)),
+                           rng.uniform(size=(ns_, 1))], axis=1)
+    n = 1000
+    idx = rng.integers(0, ns_, n).astype(np.int32)
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    y = query(spec, theta, surf, d, idx)
+    s = surf[idx]
+    y2 = full_forward(spec, theta, s[:, 0:3], s[:, 3:6], s[:, 6:9], s[:, 9], d)
+    assert y.shape == (n, 3)
+    np.testing.assert_array_equal(y, np.asarray(y2))
+    bad = idx.copy()
+    bad[17] = ns_
+    with pytest.raises(ConfigError):
+        query(spec, theta, surf, d, bad)
