@@ -81,13 +81,17 @@ class RenderResult:
 
 
 class _RenderWs:
-    buf = None
+    """Render workspaces, one per CUDA stream (launches on different streams
+    may overlap)."""
+    bufs = {}
 
     @classmethod
     def get(cls, nbytes):
-        if cls.buf is None or cls.buf.numel() < nbytes:
-            cls.buf = _dev.empty((max(int(nbytes), 256),), torch.uint8)
-        return cls.buf
+        key = torch.cuda.current_stream().cuda_stream
+        buf = cls.bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = cls.bufs[key] = _dev.empty((max(int(nbytes), 256),), torch.uint8)
+        return buf
 
 
 def _c_cfg(config, scene, spp, seed, frame, cache_on, rows=None, precision=None, v1=None):
