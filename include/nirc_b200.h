@@ -86,7 +86,8 @@ typedef struct nirc_scene {
   /* Optional fp32 pre-test items for the warp-uniform scan of small
    * triangle-only scenes (NULL: one item per triangle, built in-kernel):
    * n_filter rows of 16 floats -- (v0.xyz, |e1|_1), (e1.xyz, |e2|_1),
-   * (e2.xyz, |v0|_1), (cu, slack, bits(k1 | k2 << 8 | paired << 16), 0):
+   * (e2.xyz, |v0|_1), (cu, slack, mask_lo, mask_hi) -- the 64-bit mask of
+   * the scan positions the item covers, as two u32 bit patterns:
    * a triangle (cu = 1) or a parallelogram covering two scan-order
    * triangles that share v0 and their diagonal (cu = 0). */
   const float* filter_items;

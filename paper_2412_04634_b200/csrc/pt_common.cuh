@@ -174,11 +174,10 @@ __device__ inline bool tri_candidate(const RayF32& r, const float4* T, float t_l
                    (t - Et > t_hi * hi * 1.000001f);            // t >= t_hi (inf: never)
   return !(ad > Ed) | !out;  // sign of det uncertain: the exact test decides
 }
-// scan-order triangles an item covers, as a candidate bit mask
+// scan-order triangles an item covers, as a candidate bit mask (stored as
+// two 32-bit words in the row's last two lanes)
 __device__ inline uint64_t item_bits(const float4* T) {
-  const uint32_t b = __float_as_uint(T[3].z);
-  const uint64_t k1 = b & 0xffu, k2 = (b >> 8) & 0xffu;
-  return (1ull << k1) | ((b >> 16) & 1u ? (1ull << k2) : 0ull);
+  return ((uint64_t)__float_as_uint(T[3].w) << 32) | __float_as_uint(T[3].z);
 }
 
 // Traversal image (nirc_pack_scene): per internal node both child boxes and
@@ -825,8 +824,8 @@ __device__ inline void stage_scene(nirc_scene_t& s, unsigned char* sm) {
         row[11] = (fabsf(row[0]) + fabsf(row[1]) + fabsf(row[2])) * 1.0001f;
         row[12] = 1.0f;            // triangle
         row[13] = 1.000001e-9f;    // the reference's barycentric slack
-        row[14] = __uint_as_float((uint32_t)k);
-        row[15] = 0.0f;
+        row[14] = __uint_as_float(k < 32 ? 1u << k : 0u);  // candidate mask
+        row[15] = __uint_as_float(k >= 32 ? 1u << (k - 32) : 0u);
       }
       s.n_filter = s.n_tri;
     }

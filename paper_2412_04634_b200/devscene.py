@@ -54,18 +54,18 @@ def filter_items(p):
         if j >= 0:  # k and j: the item is v0 + u a + v b over the unit square
             ka, kb = (k, j) if e2[k].tobytes() == e1[j].tobytes() else (j, k)
             ea, eb = e1[ka], e2[kb]
-            cu, slack, bits = 0.0, PAIR_SLACK, k | (j << 8) | (1 << 16)
+            cu, slack, bits = 0.0, PAIR_SLACK, (1 << k) | (1 << j)
             done[j] = True
         else:
             ka, ea, eb = k, e1[k], e2[k]
-            cu, slack, bits = 1.0, TRI_SLACK, k
+            cu, slack, bits = 1.0, TRI_SLACK, 1 << k
         f0, fa, fb = (v0[ka].astype(np.float32), ea.astype(np.float32),
                       eb.astype(np.float32))
         row[0:3], row[3] = f0, _l1_up(fa)
         row[4:7], row[7] = fa, _l1_up(fb)
         row[8:11], row[11] = fb, _l1_up(f0)
         row[12], row[13] = cu, slack
-        row[14] = np.array([bits], np.uint32).view(np.float32)[0]
+        row[14:16] = np.array([bits & 0xFFFFFFFF, bits >> 32], np.uint32).view(np.float32)
         done[k] = True
         rows.append(row)
     return np.stack(rows) if rows else np.zeros((0, 16), np.float32)
