@@ -318,7 +318,23 @@ struct AsyncBuf {
   explicit AsyncBuf(cudaStream_t st) : s(st) {}
   AsyncBuf(const AsyncBuf&) = delete;
   AsyncBuf& operator=(const AsyncBuf&) = delete;
-  cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes, s); }
+  cudaError_t alloc(size_t bytes) {
+    keep_pool();
+    return cudaMallocAsync(&p, bytes, s);
+  }
+  // the device's default pool keeps freed blocks (threshold = max) so the
+  // per-call temporaries are recycled instead of returned at every sync
+  static void keep_pool() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done_dev = dev;
+  }
   ~AsyncBuf() {
     if (p) cudaFreeAsync(p, s);
   }

@@ -223,15 +223,44 @@ __device__ __forceinline__ void tmem_get(uint32_t taddr, float* v) {
   tc::tmem_wait_ld();
 }
 
+// The step's weight image in the kernel's shared-memory layout: W (dout x
+// ldw) and W^T (din x ldt) zero padded, and the biases, per layer -- built
+// once per step so that every tile CTA stages it with TMA bulk copies.
+__global__ void k_pack_train_weights(nirc_spec_t sp, FusedLayout L,
+                                     const float* __restrict__ theta, float* __restrict__ img) {
+  const int l = blockIdx.y;
+  const float* Wg = theta + sp.w_off[l];
+  const int din = L.din[l], dout = L.dout[l], ldw = L.ldw[l], ldt = L.ldt[l];
+  const int nw = up4(dout) * ldw, nt = up4(din) * ldt;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nw + nt + kMaxW;
+       e += gridDim.x * blockDim.x) {
+    float v;
+    if (e < nw) {
+      const int j = e / ldw, i = e - j * ldw;
+      v = (j < dout && i < din) ? Wg[j * din + i] : 0.0f;
+      img[L.w_off[l] + e] = v;
+    } else if (e < nw + nt) {
+      const int i = (e - nw) / ldt, j = (e - nw) - i * ldt;
+      v = (j < dout && i < din) ? Wg[j * din + i] : 0.0f;
+      img[L.t_off[l] + (e - nw)] = v;
+    } else {
+      const int j = e - nw - nt;
+      img[L.b_off[l] + j] = j < dout ? theta[sp.b_off[l] + j] : 0.0f;
+    }
+  }
+}
+
 // One 128-row tile of the batch per CTA (tiles tile0 + blockIdx.x); rows
 // idx[tile*128 + r]; thread (r, h) = (tid & 127, tid >> 7).
 __global__ void __launch_bounds__(kTT, 1)
     k_train_tile(nirc_spec_t sp, FusedLayout L, const float* __restrict__ theta,
-                 nirc_records_t rec, const int64_t* __restrict__ idx, int64_t B, int loss_kind,
-                 double loss_eps, float* __restrict__ grad, float* __restrict__ partials,
+                 const float* __restrict__ wimg, nirc_records_t rec,
+                 const int64_t* __restrict__ idx, int64_t B, int loss_kind, double loss_eps,
+                 float* __restrict__ grad, float* __restrict__ partials,
                  double* __restrict__ loss_part, int32_t* __restrict__ flags, int64_t tile0) {
   extern __shared__ __align__(16) float fsm[];
   __shared__ uint32_t tmem_holder;
+  __shared__ __align__(8) uint64_t wbar;
   if (flags[0] & 3) return;
   const int tid = threadIdx.x;
   const int r = tid & (kTR - 1), h = tid / kTR;
@@ -239,35 +268,21 @@ __global__ void __launch_bounds__(kTT, 1)
   const int lane_base = ((tid >> 5) & 3) * 32;
   const int64_t row = (tile0 + blockIdx.x) * kTR + r;
   const bool live = row < B;
-  // ---- weights: W (dout x ldw) and W^T (din x ldt), zero padded; 8 loads
-  // in flight per thread before the shared-memory stores ------------------
-  for (int l = 0; l < L.nl; ++l) {
-    const float* Wg = theta + sp.w_off[l];
-    const int din = L.din[l], dout = L.dout[l], ldw = L.ldw[l], ldt = L.ldt[l];
-    const int nw = up4(dout) * ldw, nt = up4(din) * ldt;
-    for (int e0 = tid; e0 < nw + nt; e0 += 8 * kTT) {
-      float v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int e = e0 + u * kTT;
-        int j, i;
-        if (e < nw) {
-          j = e / ldw;
-          i = e - j * ldw;
-        } else {
-          i = (e - nw) / ldt;
-          j = (e - nw) - i * ldt;
-        }
-        v[u] = (e < nw + nt && j < dout && i < din) ? __ldg(Wg + j * din + i) : 0.0f;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int e = e0 + u * kTT;
-        if (e < nw + nt) fsm[(e < nw ? L.w_off[l] : L.t_off[l] - nw) + e] = v[u];
-      }
+  // ---- weights: the step's image by TMA bulk copies, in flight during the
+  // encode below (waited for before the forward) --------------------------
+  const uint32_t wb = tc::smem_u32(&wbar);
+  if (tid == 0) {
+    tc::mbar_init(wb, 1);
+    tc::mbar_init_fence();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const uint32_t bytes = (uint32_t)L.dz_off * 4u;
+    tc::mbar_expect_tx(wb, bytes);
+    for (uint32_t off = 0; off < bytes; off += 32768u) {
+      const uint32_t sz = bytes - off < 32768u ? bytes - off : 32768u;
+      tc::bulk_g2s(tc::smem_u32(fsm) + off, reinterpret_cast<const uint8_t*>(wimg) + off, sz, wb);
     }
-    for (int j = tid; j < kMaxW; j += kTT)
-      fsm[L.b_off[l] + j] = j < dout ? theta[sp.b_off[l] + j] : 0.0f;
   }
   if (tid < 32) tc::tmem_alloc(tc::smem_u32(&tmem_holder), (uint32_t)L.tmem_cols);
   tc::fence_before();
@@ -325,6 +340,7 @@ __global__ void __launch_bounds__(kTT, 1)
     for (int i = 0; i < kCols; ++i) x[i] = (c0 + i) < sp.in_dim ? A[(c0 + i) * kLD2 + r] : 0.0f;
     tmem_put(tbase + L.x_col + c0, x);
   }
+  tc::mbar_wait(wb, 0);  // the weight image has landed
   // ---- forward: hidden layers stash z in TMEM, write relu(z) as next input
   const int NL = L.nl;
   for (int l = 0; l < NL - 1; ++l) {
@@ -510,9 +526,15 @@ int launch_fused_train(const nirc_spec_t& sp, const float* theta, const nirc_rec
   const int ntiles = (int)(tile1 > tile0 ? tile1 - tile0 : 0);
   NIRC_CUDA_TRY(cudaMemsetAsync(grad, 0, sp.grid_len * 4, s));
   if (adam_bad) NIRC_CUDA_TRY(cudaMemsetAsync(adam_bad, 0, 4, s));
+  AsyncBuf img(s);
   if (ntiles > 0) {
-    k_train_tile<<<ntiles, kTT, sm, s>>>(sp, L, theta, rec, idx, B, loss_kind, loss_eps, grad,
-                                         partials, loss_part, flags, tile0);
+    NIRC_CUDA_TRY(img.alloc((size_t)L.dz_off * 4));
+    k_pack_train_weights<<<dim3(16, L.nl), 256, 0, s>>>(sp, L, theta,
+                                                       static_cast<float*>(img.p));
+    NIRC_LAUNCH_CHECK("k_pack_train_weights");
+    k_train_tile<<<ntiles, kTT, sm, s>>>(sp, L, theta, static_cast<const float*>(img.p), rec,
+                                         idx, B, loss_kind, loss_eps, grad, partials, loss_part,
+                                         flags, tile0);
     NIRC_LAUNCH_CHECK("k_train_tile");
   }
   const int np = (int)(sp.theta_len - sp.grid_len);
