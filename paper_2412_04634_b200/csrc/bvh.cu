@@ -399,11 +399,11 @@ __global__ void k_pack_nodes(nirc_scene_t s, pt::PackedNode* out) {
     const int ch[2] = {i + 1, s.bvh_a[i]};
     for (int c = 0; c < 2; ++c) {
       const int k = ch[c];
-      double* lo = c == 0 ? nd.lo0 : nd.lo1;
-      double* hi = c == 0 ? nd.hi0 : nd.hi1;
+      float* lo = c == 0 ? nd.lo0 : nd.lo1;
+      float* hi = c == 0 ? nd.hi0 : nd.hi1;
       for (int a = 0; a < 3; ++a) {
-        lo[a] = s.bvh_lo[3 * k + a];
-        hi[a] = s.bvh_hi[3 * k + a];
+        lo[a] = __double2float_rd(s.bvh_lo[3 * k + a]);
+        hi[a] = __double2float_ru(s.bvh_hi[3 * k + a]);
       }
       const bool leaf = s.bvh_b[k] > 0;
       (c == 0 ? nd.c0 : nd.c1) = leaf ? s.bvh_a[k] : k;

@@ -211,13 +211,58 @@ __device__ inline bool box_entry(const double* oo, const double* inv_d, const do
   return true;
 }
 
+// Conservative fp32 slab test of a packed (outward-rounded) child box: accepts
+// every box _box_hit accepts for the f64 ray (it may accept a few more,
+// which only costs primitive tests).  Each slab distance is widened by the
+// fp32 rounding of the origin (w = |o| 2^-22 |1/d|, precomputed per ray) and
+// of the subtraction / inverse / product (2^-20 relative); t_in is a lower
+// bound of the f64 entry distance.
+struct RayBox32 {
+  float o[3], inv[3], w[3];
+  bool par[3];  // |d| < 1e-30: the reference's parallel-slab case
+};
+__device__ inline RayBox32 ray_box32(V3 o, V3 d) {
+  RayBox32 r;
+  const double oo[3] = {o.x, o.y, o.z}, dd[3] = {d.x, d.y, d.z};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    r.o[a] = (float)oo[a];
+    r.par[a] = dd[a] > -1e-30 && dd[a] < 1e-30;
+    r.inv[a] = r.par[a] ? 0.0f : (float)(1.0 / dd[a]);
+    r.w[a] = (fabsf(r.o[a]) * 2.384185791e-7f + 1e-30f) * fabsf(r.inv[a]);  // 2^-22
+  }
+  return r;
+}
+__device__ inline bool box_entry32(const RayBox32& r, const float* lo, const float* hi,
+                                   float t_best, float& t_in) {
+  float t0 = 0.0f, t1 = t_best;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (r.par[a]) {
+      const float m = fabsf(r.o[a]) * 2.384185791e-7f + 1e-30f;
+      if (r.o[a] < lo[a] - m || r.o[a] > hi[a] + m) return false;
+    } else {
+      const float ta = (lo[a] - r.o[a]) * r.inv[a];
+      const float tb = (hi[a] - r.o[a]) * r.inv[a];
+      const float tn = fminf(ta, tb), tf = fmaxf(ta, tb);
+      const float tn_w = tn - (fabsf(tn) * 9.5367431640625e-7f + r.w[a]);  // 2^-20
+      const float tf_w = tf + (fabsf(tf) * 9.5367431640625e-7f + r.w[a]);
+      t0 = fmaxf(t0, tn_w);
+      t1 = fminf(t1, tf_w);
+    }
+  }
+  t_in = t0;
+  return t0 <= t1;
+}
+
 // Front-to-back traversal of the packed image: at an internal node both
-// child boxes are tested against the current best distance and the nearer
-// child is visited first (child 0 -- the reference's left-first order -- on
-// equal entry distances); popped subtrees whose entry (rounded down to
-// fp32) lies beyond the best hit are skipped.  The nearest hit and the
-// any-hit boolean are the reference traversal's (only exact distance ties
-// between different primitives could resolve differently).
+// child boxes are tested (fp32, conservatively) against the current best
+// distance and the nearer child is visited first (child 0 on equal entry
+// distances); popped subtrees whose entry lies beyond the best hit are
+// skipped.  The reference's left-first walk meets primitives in leaf order
+// and keeps the first of equal distances, so its hit is the minimum of
+// (t, leaf index): ties here resolve the same way, and the nearest hit (kind,
+// primitive, t) and the any-hit boolean equal the reference's exactly.
 template <bool AnyHit>
 __device__ __noinline__ void bvh_scan_packed(const nirc_scene_t& s, V3 o, V3 d, double& best,
                                              int& kind, int& prim) {
@@ -234,7 +279,9 @@ __device__ __noinline__ void bvh_scan_packed(const nirc_scene_t& s, V3 o, V3 d, 
   double t_root;
   if (s.bvh_b[0] == 0 && s.bvh_a[0] == 0 && s.n_tri + s.n_sph == 0) return;
   if (!box_entry(oo, inv_d, s.bvh_lo, s.bvh_hi, best, t_root)) return;
+  const RayBox32 rb32 = ray_box32(o, d);
   int cur = s.bvh_b[0] > 0 ? (s.bvh_a[0] << 3 | s.bvh_b[0]) : 0;
+  int best_k = 0x7fffffff;
   int st_ref[40];
   float st_t[40];
   int sp = 0;
@@ -247,8 +294,11 @@ __device__ __noinline__ void bvh_scan_packed(const nirc_scene_t& s, V3 o, V3 d, 
                              ? ray_tri(o, d, {q.g[0], q.g[1], q.g[2]}, {q.g[3], q.g[4], q.g[5]},
                                        {q.g[6], q.g[7], q.g[8]})
                              : ray_sph(o, d, {q.g[0], q.g[1], q.g[2]}, q.g[3]);
-        if (t > eps && t < best) {
+        // equal distances resolve to the earlier leaf-order primitive: the
+        // one the reference's left-first walk meets first
+        if (t > eps && (t < best || (t == best && kind >= 0 && k < best_k))) {
           best = t;
+          best_k = k;
           kind = q.kind;
           prim = q.id;
           if (AnyHit) return;
@@ -256,23 +306,24 @@ __device__ __noinline__ void bvh_scan_packed(const nirc_scene_t& s, V3 o, V3 d, 
       }
     } else {
       const PackedNode& nd = N[idx];
-      double ta = 0.0, tb = 0.0;
-      const bool ha = box_entry(oo, inv_d, nd.lo0, nd.hi0, best, ta);
-      const bool hb = box_entry(oo, inv_d, nd.lo1, nd.hi1, best, tb);
+      float ta = 0.0f, tb = 0.0f;
+      const float best_up = __double2float_ru(best);
+      const bool ha = box_entry32(rb32, nd.lo0, nd.hi0, best_up, ta);
+      const bool hb = box_entry32(rb32, nd.lo1, nd.hi1, best_up, tb);
       int ra = nd.c0 << 3 | nd.n0, rb = nd.c1 << 3 | nd.n1;
       if (ha && hb) {
         if (tb < ta) {
           const int r = ra;
           ra = rb;
           rb = r;
-          const double t = ta;
+          const float t = ta;
           ta = tb;
           tb = t;
         }
-        // visit the nearer child; push the farther one with its entry
-        // rounded down (the pop test stays conservative)
+        // visit the nearer child; push the farther one with its entry (a
+        // lower bound: the pop test stays conservative)
         st_ref[sp] = rb;
-        st_t[sp] = __double2float_rd(tb);
+        st_t[sp] = tb;
         ++sp;
         cur = ra;
         continue;

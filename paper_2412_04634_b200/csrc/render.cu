@@ -1538,11 +1538,13 @@ extern "C" void nirc_debug_infer_probe(long long* buf) { nirc::g_infer_probe = b
 // primitive or t bit pattern, or occlusion boolean), counts[1] = hits.
 namespace nirc {
 __global__ void k_debug_intersect(nirc_scene_t scn, int64_t n, uint64_t seed,
-                                  unsigned long long* counts) {
+                                  unsigned long long* counts, double* detail, int aim) {
   __shared__ __align__(16) unsigned char scene_sm[pt::kSceneSmemBytes];
   pt::stage_scene(scn, scene_sm);
-  nirc_scene_t plain = scn;
+  nirc_scene_t plain = scn;  // the reference-order f64 scan / stack walk
   plain.tri_f32 = nullptr;
+  plain.bvh_packed = nullptr;
+  plain.prim_packed = nullptr;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t key = stream_key(seed, 77, 0, (uint64_t)i, 0);
@@ -1551,7 +1553,7 @@ __global__ void k_debug_intersect(nirc_scene_t scn, int64_t n, uint64_t seed,
     V3 o = {scn.bbox_min[0] + U(0) / scn.bbox_inv_ext[0], scn.bbox_min[1] + U(1) / scn.bbox_inv_ext[1],
             scn.bbox_min[2] + U(2) / scn.bbox_inv_ext[2]};
     V3 d = {U(3) - 0.5, U(4) - 0.5, U(5) - 0.5};
-    if (U(6) < 0.33 && scn.n_tri > 0) {  // aim at a vertex or an edge point of a triangle
+    if (aim && U(6) < 0.33 && scn.n_tri > 0) {  // aim at a vertex or an edge point of a triangle
       const int t = (int)(U(7) * scn.n_tri) % scn.n_tri;
       const V3 v0 = pt::ld3(scn.tri_v0, t), e1 = pt::ld3(scn.tri_e1, t), e2 = pt::ld3(scn.tri_e2, t);
       const double a = U(8) < 0.5 ? 0.0 : U(9), b = U(10) < 0.5 ? 0.0 : 1.0 - a;
@@ -1565,22 +1567,46 @@ __global__ void k_debug_intersect(nirc_scene_t scn, int64_t n, uint64_t seed,
     (void)ext;
     const pt::Hit a = pt::intersect<false>(scn, o, d, pt::T_FAR);
     const pt::Hit b = pt::intersect<false>(plain, o, d, pt::T_FAR);
+    // counts: [0] nearest-hit mismatches, [1] hits, [2] occlusion mismatches
+    // at t_max = t and one ulp either side of the hit
     bool bad = a.kind != b.kind || a.prim != b.prim ||
                (a.kind >= 0 && __double_as_longlong(a.t) != __double_as_longlong(b.t));
+    bool bad_occ = false;
     if (b.kind >= 0) {
       atomicAdd(counts + 1, 1ull);
       const double tm[3] = {b.t, nextafter(b.t, 0.0), nextafter(b.t, 1e300)};
       for (int q = 0; q < 3; ++q)
-        bad |= pt::occluded(scn, o, d, tm[q]) != pt::occluded(plain, o, d, tm[q]);
+        bad_occ |= pt::occluded(scn, o, d, tm[q]) != pt::occluded(plain, o, d, tm[q]);
     }
-    if (bad) atomicAdd(counts, 1ull);
+    if (bad_occ) atomicAdd(counts + 2, 1ull);
+    if (bad || bad_occ) {
+      const unsigned long long m = bad ? atomicAdd(counts, 1ull) : 16ull;
+      if (detail && m < 16) {  // first mismatches: ray, both hits, occlusion answers
+        double* q = detail + 16 * m;
+        q[0] = o.x; q[1] = o.y; q[2] = o.z; q[3] = d.x; q[4] = d.y; q[5] = d.z;
+        q[6] = a.kind; q[7] = a.prim; q[8] = a.t; q[9] = b.kind; q[10] = b.prim; q[11] = b.t;
+        if (b.kind >= 0) {
+          q[12] = pt::occluded(scn, o, d, b.t);
+          q[13] = pt::occluded(plain, o, d, b.t);
+          q[14] = pt::occluded(scn, o, d, nextafter(b.t, 1e300));
+          q[15] = pt::occluded(plain, o, d, nextafter(b.t, 1e300));
+        }
+      }
+    }
   }
 }
 }  // namespace nirc
 
 extern "C" int nirc_debug_intersect_check(const nirc_scene_t* scene, int64_t n, uint64_t seed,
                                           unsigned long long* counts) {
-  nirc::k_debug_intersect<<<148 * 4, 128>>>(*scene, n, seed, counts);
+  nirc::k_debug_intersect<<<148 * 4, 128>>>(*scene, n, seed, counts, nullptr, 1);
+  return cudaGetLastError() == cudaSuccess ? 0 : 5;
+}
+
+extern "C" int nirc_debug_intersect_detail(const nirc_scene_t* scene, int64_t n, uint64_t seed,
+                                           unsigned long long* counts, double* detail,
+                                           int32_t aim) {
+  nirc::k_debug_intersect<<<148 * 4, 128>>>(*scene, n, seed, counts, detail, aim);
   return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }
 
