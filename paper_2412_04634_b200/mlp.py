@@ -159,13 +159,18 @@ def _pinned_host(arrays):
     return all(isinstance(a, torch.Tensor) and not a.is_cuda and a.is_pinned() for a in arrays)
 
 
-def _full_forward_pipelined(spec, th, host, precision, out=None, chunk=1 << 19):
+_PIPE_CHUNK = int(__import__("os").environ.get("NIRC_PIPE_CHUNK", 1 << 19))
+
+
+def _full_forward_pipelined(spec, th, host, precision, out=None, chunk=None):
     """Host-resident (pinned) query rows: chunked H2D copies on one stream,
     the fused kernel on the caller's stream, D2H of the outputs on a third,
     double-buffered so PCIe transfers in both directions overlap the compute.
     Returns a pinned host tensor; the caller's stream is ordered after it."""
     n = int(host[0].shape[0])
     dout = int(spec.dims[-1])
+    if chunk is None:
+        chunk = _PIPE_CHUNK
     cur = torch.cuda.current_stream()
     s_in, s_out = _pipe_streams()
     y_host = out if out is not None else torch.empty((n, dout), dtype=torch.float32,
