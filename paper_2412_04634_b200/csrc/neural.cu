@@ -927,9 +927,12 @@ TrainWs carve_train(const nirc_spec_t& sp, int64_t n, int64_t B, int steps, void
   w.grad = (float*)take(sp.theta_len * 4);
   w.partial = (double*)take((B / kLossThreads + 2) * 3 * 8);
   w.adam_bad = (int32_t*)take(16);
+  // partial slots: one per CTA; a launch of k tiles runs k, 2k or 4k CTAs
+  // with 4k, 2k <= the SM count (train_fused.cu tile_rows_for)
   const int64_t ntiles = (B + kFusedTileRows - 1) / kFusedTileRows;
-  w.fpart = (float*)take(ntiles * (sp.theta_len - sp.grid_len) * 4);
-  w.floss = (double*)take(ntiles * 8);
+  const int64_t slots = ntiles > 256 ? ntiles : 256;
+  w.fpart = (float*)take(slots * (sp.theta_len - sp.grid_len) * 4);
+  w.floss = (double*)take(slots * 8);
   w.bytes = off;
   return w;
 }
