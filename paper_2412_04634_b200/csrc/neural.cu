@@ -473,25 +473,37 @@ __global__ void k_adam_apply4(float* __restrict__ theta, float* __restrict__ m,
     if (blockIdx.x == 0 && threadIdx.x == 0) skipped[0] += 1;
     return;
   }
-  // bias corrections once per block (f64 pow, the reference's python float
-  // arithmetic), t read before block 0 publishes (see k_adam_tick)
-  __shared__ float s_bc[2];
-  if (threadIdx.x == 0) {
-    const int64_t tn = t[0] + 1;
-    s_bc[0] = (float)(1.0 - pow(b1, (double)tn));
-    s_bc[1] = (float)(1.0 - pow(b2, (double)tn));
-  }
-  __syncthreads();
   const float c1 = (float)(1.0 - b1);
   const float c2 = (float)(1.0 - b2);
-  const float bc1 = s_bc[0], bc2 = s_bc[1];
   const int64_t n4 = n >> 2;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // this thread's first float4s are requested before the bias corrections
+  // (f64 pow, the reference's python float arithmetic; one lane per warp,
+  // broadcast by shuffle) are computed, so their latencies overlap; t is
+  // read before block 0 publishes (see k_adam_tick)
+  const bool first = tid < n4;
+  float4 th = make_float4(0.f, 0.f, 0.f, 0.f), mi = th, vi = th, gi = th;
+  if (first) {
+    th = reinterpret_cast<float4*>(theta)[tid];
+    mi = reinterpret_cast<float4*>(m)[tid];
+    vi = reinterpret_cast<float4*>(v)[tid];
+    gi = reinterpret_cast<const float4*>(g)[tid];
+  }
+  float bc1 = 0.0f, bc2 = 0.0f;
+  if ((threadIdx.x & 31) == 0) {
+    const int64_t tn = t[0] + 1;
+    bc1 = (float)(1.0 - pow(b1, (double)tn));
+    bc2 = (float)(1.0 - pow(b2, (double)tn));
+  }
+  bc1 = __shfl_sync(0xffffffffu, bc1, 0);
+  bc2 = __shfl_sync(0xffffffffu, bc2, 0);
   for (int64_t i = tid; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-    float4 th = reinterpret_cast<float4*>(theta)[i];
-    float4 mi = reinterpret_cast<float4*>(m)[i];
-    float4 vi = reinterpret_cast<float4*>(v)[i];
-    const float4 gi = reinterpret_cast<const float4*>(g)[i];
+    if (i != tid) {
+      th = reinterpret_cast<float4*>(theta)[i];
+      mi = reinterpret_cast<float4*>(m)[i];
+      vi = reinterpret_cast<float4*>(v)[i];
+      gi = reinterpret_cast<const float4*>(g)[i];
+    }
     adam_one(th.x, mi.x, vi.x, gi.x, c1, c2, bc1, bc2, lr, eps);
     adam_one(th.y, mi.y, vi.y, gi.y, c1, c2, bc1, bc2, lr, eps);
     adam_one(th.z, mi.z, vi.z, gi.z, c1, c2, bc1, bc2, lr, eps);
