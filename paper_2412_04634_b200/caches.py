@@ -335,7 +335,7 @@ def _dump_diagnostics(cache, step, value):
     path = os.path.join(out_dir, f"diverged_{cache.kind}_frame{cache.frame}.nncache")
     cache.save(path)
     return (f"non-finite loss ({value}) at frame {cache.frame} step {step}; "
-            f"state dumped to {path}")
+            f"state dumped to {path}"), path
 
 
 def train_frame(cache, records, steps=4, batch=None):
@@ -351,6 +351,7 @@ def train_frame(cache, records, steps=4, batch=None):
         raise InvalidSampleError("sample pdf must be positive")
     if res.flags & 2:
         s = res.diverged_step
-        raise DivergenceError(_dump_diagnostics(cache, s, res.trace[s]))
+        msg, path = _dump_diagnostics(cache, s, res.trace[s])
+        raise DivergenceError(msg, snapshot_path=path)
     cache.frame += 1
     return res.trace

@@ -259,11 +259,12 @@ def train_frame_sharded(cache, records, comm, steps=4, batch=None, ops=None):
         raise InvalidSampleError("sample pdf must be positive")
     if flags & 2:
         s = next(i for i, v in enumerate(trace) if not math.isfinite(v))
+        path = None
         if comm.rank == 0:
-            msg = _dump_diagnostics(cache, s, trace[s])
+            msg, path = _dump_diagnostics(cache, s, trace[s])
         else:
             msg = f"non-finite loss ({trace[s]}) at frame {cache.frame} step {s} (rank {comm.rank})"
-        raise DivergenceError(msg)
+        raise DivergenceError(msg, snapshot_path=path)
     cache.frame += 1
     return trace
 

@@ -160,3 +160,37 @@ def test_env_record_kinds(cuda):
     assert np.array_equal(v[:, 0], v[:, 1]) and np.array_equal(v[:, 1], v[:, 2])
     lit = v[:, 0] == 1.0
     assert np.all(r[~lit] == 0.0) and np.all(r[lit] > 0.0)
+
+
+def test_divergence_and_nonfinite_guards(cuda, tmp_path):
+    """The reference's guards (caches.py:347-353, mlp.py:104-105,
+    adam.py:22-24; its tests test_caches.py:304-312, test_neural.py:178-183):
+    a non-finite loss raises DivergenceError after dumping the cache state
+    (one .nncache, its path in the message) and leaves the frame counter;
+    mlp_forward refuses a non-finite theta."""
+    from paper_2412_04634_b200.caches import Cache, Records
+    from paper_2412_04634_b200.errors import DivergenceError
+    from paper_2412_04634_b200.mlp import init_theta, make_spec, mlp_forward
+
+    sc = _scene(ROOM.replace("EMIT", "8 8 8"))
+    cache = Cache.create("nirc", sc, seed=7, loss="l2")
+    cache.snapshot_dir = str(tmp_path)
+    rng = np.random.default_rng(3)
+    n = 64
+    nrm = rng.normal(size=(n, 3))
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    rec = Records(kind="nirc", frame=0, pos=rng.uniform(size=(n, 3)), ns=nrm,
+                  alb=rng.uniform(size=(n, 3)), rough=np.ones(n), dirs=nrm.copy(),
+                  target=np.full((n, 3), np.inf), pdf=np.full(n, 0.3))
+    frame0 = cache.frame
+    with pytest.raises(DivergenceError) as err:
+        cache.train_frame(rec)
+    dumps = list(tmp_path.iterdir())
+    assert len(dumps) == 1 and str(dumps[0]) in str(err.value)
+    assert err.value.snapshot_path == str(dumps[0])
+    assert cache.frame == frame0
+    spec = make_spec(depth=2)
+    theta = init_theta(spec, seed=1)
+    theta[spec.grid_len + 3] = np.nan
+    with pytest.raises(DivergenceError):
+        mlp_forward(spec, theta, np.zeros((1, spec.in_dim), np.float32))
