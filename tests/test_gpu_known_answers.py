@@ -194,3 +194,47 @@ def test_divergence_and_nonfinite_guards(cuda, tmp_path):
     theta[spec.grid_len + 3] = np.nan
     with pytest.raises(DivergenceError):
         mlp_forward(spec, theta, np.zeros((1, spec.in_dim), np.float32))
+
+
+def _const_records(n, seed, target, pdf=1.0):
+    from paper_2412_04634_b200.caches import Records
+
+    rng = np.random.default_rng(seed)
+    ns = rng.normal(size=(n, 3))
+    ns /= np.linalg.norm(ns, axis=1, keepdims=True)
+    dirs = rng.normal(size=(n, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    return Records(kind="nirc", frame=0, pos=rng.uniform(0, 1, (n, 3)), ns=ns,
+                   alb=np.full((n, 3), 0.45), rough=np.ones(n), dirs=dirs,
+                   target=np.broadcast_to(np.asarray(target, float), (n, 3)).copy(),
+                   pdf=np.full(n, pdf))
+
+
+def test_training_learns_constant_and_zero_targets(cuda):
+    """Online training behaves like the reference's (its
+    tests/test_caches.py:277-301): constant targets are learned to within 1 %
+    of their mean after 2000 optimizer steps from the zero-initialised output
+    layer, and zero targets drive a random cache's output down."""
+    from paper_2412_04634_b200.caches import Cache
+    from paper_2412_04634_b200.mlp import full_forward
+
+    sc = _scene(ROOM.replace("EMIT", "8 8 8"))
+    target = np.array([0.6, 0.45, 0.25])
+    cache = Cache.create("nirc", sc, seed=6)
+    rec = _const_records(256, 8, target)
+    for _ in range(500):  # 2000 optimizer steps
+        cache.train_frame(rec)
+    pred = np.asarray(full_forward(cache.spec, cache.theta, rec.pos, rec.ns, rec.alb, rec.rough,
+                                   rec.dirs))
+    assert np.all(np.abs(pred.mean(axis=0) - target) / target < 0.01)
+
+    cache = Cache.create("nirc", sc, seed=5, init="random", loss="l2")
+    rec = _const_records(512, 21, 0.0)
+    before = np.asarray(full_forward(cache.spec, cache.theta, rec.pos, rec.ns, rec.alb,
+                                     rec.rough, rec.dirs))
+    for _ in range(100):
+        cache.train_frame(rec)
+    after = np.asarray(full_forward(cache.spec, cache.theta, rec.pos, rec.ns, rec.alb, rec.rough,
+                                    rec.dirs))
+    assert np.abs(before).mean() > 1e-3
+    assert np.abs(after).mean() < 1e-3
