@@ -238,3 +238,32 @@ def test_training_learns_constant_and_zero_targets(cuda):
                                     rec.dirs))
     assert np.abs(before).mean() > 1e-3
     assert np.abs(after).mean() < 1e-3
+
+
+def test_path_tracer_analytic_scenes(cuda):
+    """Analytic answers of the device path tracer (the reference's
+    tests/test_estimators.py:124-144 on scenes of our own): an empty scene
+    is exactly its constant environment with zero path length; a huge
+    Lambert floor under a unit sky reflects its albedo; the builtin furnace
+    (unit albedo in a unit sky) converges to 1 everywhere."""
+    from paper_2412_04634_b200.estimators import EstimatorConfig, render
+    from paper_2412_04634_b200.scene import load_builtin
+
+    empty = _scene("""
+camera { position 0 0 0  look_at 0 1 1  up 0 1 0  fov 50  resolution 10 6 }
+environment { kind constant  color 1.7 1.7 1.7 }
+""")
+    out = render(empty, EstimatorConfig(mode="pt"), seed=4, spp=3)
+    assert np.all(out.image == 1.7)
+    assert out.avg_path_length == 0.0
+    floor = _scene("""
+camera { position 0 30 0.001  look_at 0 0 0  up 0 1 0  fov 25  resolution 10 10 }
+material m { kind lambert  albedo 0.35 0.35 0.35 }
+quad ground { material m  p0 -400 0 -400  p1 400 0 -400  p2 400 0 400  p3 -400 0 400 }
+environment { kind constant  color 1.0 1.0 1.0 }
+""")
+    out = render(floor, EstimatorConfig(mode="pt"), seed=2, spp=64)
+    assert np.max(np.abs(out.image - 0.35)) < 5e-3
+    out = render(load_builtin("furnace"), EstimatorConfig(mode="pt"), seed=1, spp=256)
+    assert abs(float(out.image.mean()) - 1.0) < 0.01
+    assert np.max(np.abs(out.image - 1.0)) < 0.01
