@@ -267,3 +267,38 @@ environment { kind constant  color 1.0 1.0 1.0 }
     out = render(load_builtin("furnace"), EstimatorConfig(mode="pt"), seed=1, spp=256)
     assert abs(float(out.image.mean()) - 1.0) < 0.01
     assert np.max(np.abs(out.image - 1.0)) < 0.01
+
+
+def test_nvc_cache_bounds_guard_and_learning(cuda):
+    """The visibility cache (NVC, sigmoid head) after the reference's
+    tests/test_caches.py:236-250,343-353: outputs in (0, 1), queries need an
+    environment light, and online training on the occlusion scene learns
+    ray-cast visibility of fresh (surface, direction) pairs."""
+    from paper_2412_04634_b200.caches import Cache
+    from paper_2412_04634_b200.errors import ConfigError
+    from paper_2412_04634_b200.mlp import full_forward
+    from paper_2412_04634_b200.records import collect_training_records
+    from paper_2412_04634_b200.scene import load_builtin
+
+    sky = load_builtin("occlusion")
+    cache = Cache.create("nvc", sky, seed=2, init="random")
+    it = sky.intersect([0.0, 3.0, 0.0], [0.0, -1.0, 0.0])
+    rng = np.random.default_rng(4)
+    dirs = rng.normal(size=(50, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    out = cache.nvc_query(it, dirs)
+    assert np.all(out > 0.0) and np.all(out < 1.0)
+    room = _scene(ROOM.replace("EMIT", "8 8 8"))
+    no_env = Cache.create("nvc", room, seed=2)
+    with pytest.raises(ConfigError):
+        no_env.nvc_query(room.intersect([0.5, 0.5, 0.5], [0.0, -1.0, 0.0]), dirs)
+
+    cache = Cache.create("nvc", sky, seed=13)
+    for f in range(256):
+        rec = cache.collect()
+        if len(rec):
+            cache.train_frame(rec)
+    rec = collect_training_records(sky, seed=999, count=200, kind="nvc")
+    pred = full_forward(cache.spec, cache.theta, rec.pos, rec.ns, rec.alb, rec.rough, rec.dirs)
+    mae = float((pred[:, 0].double() - rec.target[:, 0]).abs().mean())
+    assert mae < 0.12
