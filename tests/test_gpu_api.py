@@ -167,3 +167,24 @@ def test_query_batches_surfaces():
     bad[17] = ns_
     with pytest.raises(ConfigError):
         query(spec, theta, surf, d, bad)
+
+
+def test_query_zero_cache_and_amortization(box):
+    """Cache queries after the reference's tests/test_caches.py:201-223: a
+    zero cache answers exactly 0; one batched query equals the per-direction
+    queries bit for bit (rows are independent in the fused kernel), and the
+    outgoing-radiance form (nrc_query) goes through the same path."""
+    from paper_2412_04634_b200.caches import Cache
+
+    it = _floor(box)
+    zero = Cache.create("nirc", box, seed=1)
+    assert zero.is_zero
+    assert np.all(zero.nirc_query(it, np.array([[0.0, 1.0, 0.0], [0.6, 0.8, 0.0]])) == 0.0)
+    cache = Cache.create("nirc", box, seed=3, init="random")
+    rng = np.random.default_rng(0)
+    dirs = rng.normal(size=(25, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    batch = cache.nirc_query(it, dirs)
+    singles = np.vstack([cache.nirc_query(it, d[None, :]) for d in dirs])
+    assert np.array_equal(batch, singles)
+    assert np.array_equal(cache.nrc_query(it, dirs[0]), batch[0])
