@@ -659,7 +659,9 @@ template <bool kBiased, bool kWalks, int kMinB>
 __global__ void __launch_bounds__(128, kMinB)
     k_trace(nirc_scene_t scn, const double* __restrict__ cam, nirc_render_cfg_t cfg, TraceOut out,
             WalkJob job) {
-  __shared__ __align__(16) unsigned char scene_sm[pt::kSceneSmemBytes];
+  // the staged scene, sized to it (dynamic: the rest of the SM's 256 KB
+  // stays L1 for the lanes' local state)
+  extern __shared__ __align__(16) unsigned char scene_sm[];
   pt::stage_scene(scn, scene_sm);
   const int64_t nsamp = (int64_t)(cfg.row1 - cfg.row0) * cfg.width * cfg.spp;
   const int64_t nwalk = kWalks ? job.n : 0;
@@ -1330,14 +1332,19 @@ static int render_impl(const nirc_scene_t* scene, const double* cam, const nirc_
   NIRC_CUDA_TRY(cudaMemsetAsync(w.counters, 0, 64, s));
   if (tl) NIRC_CUDA_TRY(cudaMemsetAsync(w.result, 0, ns * c.max_cv * 24, s));
   TraceOut to{w.acc, w.term, w.cv, w.counters};
+  const size_t scene_bytes = pt::scene_smem_bytes(*scene);
+  const size_t dyn = scene_bytes <= (size_t)pt::kSceneSmemBytes ? (scene_bytes + 15) & ~15ull : 0;
   auto launch_trace = [&](auto kern) -> int {
     int per_sm = 0;
-    NIRC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0));
+    NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)kern,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       pt::kSceneSmemBytes));
+    NIRC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, dyn));
     if (per_sm < 1) per_sm = 1;
     const int64_t tgrid_max = (ns + job.n + 127) / 128;
     const int64_t tgrid_pers = (int64_t)sm_count() * per_sm;
-    kern<<<(int)(tgrid_max < tgrid_pers ? tgrid_max : tgrid_pers), 128, 0, s>>>(*scene, cam, c,
-                                                                                to, job);
+    kern<<<(int)(tgrid_max < tgrid_pers ? tgrid_max : tgrid_pers), 128, dyn, s>>>(*scene, cam, c,
+                                                                                  to, job);
     return NIRC_OK;
   };
   int tst;
