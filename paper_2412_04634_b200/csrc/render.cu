@@ -649,7 +649,7 @@ struct WalkJob {
 #define NIRC_TRACE_MINB 3  // measured with the fp32 pre-test: 3 CTAs/SM (168 regs) beat 4 and 2
 #endif
 #ifndef NIRC_TRACE_MINB_BVH
-#define NIRC_TRACE_MINB_BVH 4  // BVH-traversed scenes: latency-bound, 4 CTAs/SM measured best
+#define NIRC_TRACE_MINB_BVH 8  // BVH-traversed scenes: latency-bound, 8 CTAs/SM measured best (4..12)
 #endif
 // kWalks: the launch also traces the frame's training walks (render+collect);
 // render-only launches are compiled without the walk lanes' state.  kMinB:
