@@ -1350,7 +1350,10 @@ static int render_impl(const nirc_scene_t* scene, const double* cam, const nirc_
   int tst;
   constexpr int kS = NIRC_TRACE_MINB, kB = NIRC_TRACE_MINB_BVH;
   const bool bvh = scene->bvh_packed != nullptr;  // general scene: packed BVH traversal
-  if (c.mode >= 2)
+  if (c.mode >= 2 && bvh)
+    tst = job.n > 0 ? launch_trace(k_trace<true, true, kB>)
+                    : launch_trace(k_trace<true, false, kB>);
+  else if (c.mode >= 2)
     tst = job.n > 0 ? launch_trace(k_trace<true, true, kS>)
                     : launch_trace(k_trace<true, false, kS>);
   else if (bvh)
