@@ -466,7 +466,7 @@ def run_b200(args, rank, world, local_rank):
     # streams them through its chunked H2D / kernel / D2H pipeline
     host = [torch.from_numpy(np.ascontiguousarray(a.cpu().numpy())).pin_memory() for a in q_dev]
     y_host = torch.empty((n, 3), dtype=torch.float32).pin_memory()
-    e2e_steps = max(3, min(args.steps, 20))
+    e2e_steps = max(3, min(args.steps, 40))
     y_last = [None]
 
     def e2e_step():
@@ -477,11 +477,15 @@ def run_b200(args, rank, world, local_rank):
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    eps_ = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps + 1)]
     e0.record(stream)
-    for _ in range(e2e_steps):
+    eps_[0].record(stream)
+    for k in range(e2e_steps):
         e2e_step()
+        eps_[k + 1].record(stream)
     e1.record(stream)
     barrier()
+    e2e_per_step = sorted(eps_[k].elapsed_time(eps_[k + 1]) for k in range(e2e_steps))
     e_ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
     if dist is not None:
         dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
@@ -579,6 +583,13 @@ def run_b200(args, rank, world, local_rank):
         "clocks": csum,
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                "median_step_value": world * n / (e2e_per_step[len(e2e_per_step) // 2] * 1e-3),
+                "step_ms_min_median_max": [round(e2e_per_step[0], 3),
+                                           round(e2e_per_step[len(e2e_per_step) // 2], 3),
+                                           round(e2e_per_step[-1], 3)],
+                "variance_note": "value = all steps' mean; on some boxes single steps (and "
+                                 "rarely whole windows) of the host copies run slower, so "
+                                 "the per-step median is given beside it",
                 "path": "paper_2412_04634_b200.mlp.full_forward on pinned host tensors (chunked "
                         "H2D / fused kernel / D2H pipeline inside the call)"},
         "gpu_launches": 2 * args.steps,
