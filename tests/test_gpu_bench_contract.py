@@ -52,3 +52,31 @@ def test_reference_arm_line():
     assert d["impl"] == "reference"
     assert d["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_bench_two_ranks_line():
+    """bench.py under torchrun with 2 ranks (gloo, both on this GPU): one
+    JSON line from rank 0 with n_gpus = 2, the sharded frame's replicas
+    identical; the reference arm prints once."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, NIRC_DIST_BACKEND="gloo")
+
+    def run(port, *args):
+        out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                              "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                              "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                              "--gpus", "2", *args],
+                             capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+        assert out.returncode == 0, out.stderr[-2000:]
+        lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+        assert len(lines) == 1, out.stdout[-2000:]
+        return json.loads(lines[0])
+
+    # (torchrun's own parser would take bench.py's --n for one of its options)
+    d = run(29611, "--steps", "3", "--warmup", "3", "--frame-steps", "2", "--no-extra-frames",
+            "--no-cpu-baseline")
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["frame_1080p"]["replicas_identical"] is True
+    r = run(29612, "--impl", "reference", "--steps", "1", "--warmup", "0")
+    assert r["impl"] == "reference" and r["n_gpus"] == 2
