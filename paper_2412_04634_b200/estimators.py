@@ -122,6 +122,16 @@ def _c_cfg(config, scene, spp, seed, frame, cache_on, rows=None, precision=None,
     return c
 
 
+def _is_zero(cache, theta=None):
+    """Cache.is_zero (caches.py:206-209) of the parameters a render will
+    read: the cache's own, or the snapshot passed as ``theta`` (the frame
+    pipeline trains the cache's buffer concurrently)."""
+    if theta is None:
+        return cache.is_zero
+    lo = int(cache.spec.w_off[-1])
+    return not bool(torch.any(theta[lo:] != 0).item())
+
+
 def _v1_device(v1_map, w, h):
     if v1_map is None:
         return None
@@ -142,7 +152,7 @@ def render_device(scene, config=None, cache=None, seed=0, spp=1, frame=0, force_
     mode = MODES[config.mode]
     w, h = int(scene.camera[14]), int(scene.camera[15])
     cache_on = 0
-    if mode >= 1 and cache is not None and (force_cache or not cache.is_zero):
+    if mode >= 1 and cache is not None and (force_cache or not _is_zero(cache, theta)):
         cache_on = 1
     v1 = _v1_device(v1_map, w, h) if mode in (3, 4) else None
     cfg = _c_cfg(config, scene, spp, seed, frame, cache_on, rows, precision, v1)
@@ -192,7 +202,7 @@ def render_and_collect(scene, config, cache, seed=0, spp=1, frame=0, count=None,
         train_frame = frame
     p0, p1 = (0, int(count)) if paths is None else (int(paths[0]), int(paths[1]))
     w, h = int(scene.camera[14]), int(scene.camera[15])
-    cache_on = 1 if (mode >= 1 and not cache.is_zero) else 0
+    cache_on = 1 if (mode >= 1 and not _is_zero(cache, theta)) else 0
     cfg = _c_cfg(config, scene, spp, seed, frame, cache_on, rows, precision)
     lib = _lib.load()
     ds = scene.device()
