@@ -428,9 +428,11 @@ def run_b200(args, rank, world, local_rank):
     ptrs = [_dev.ptr(a) for a in q_dev]
     stream = torch.cuda.current_stream()
 
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+
     def step():
         _lib.check(lib.nirc_full_forward(cs, _dev.ptr(theta), *ptrs, n, _dev.ptr(Y), PRECISION,
-                                         _dev.stream()), "nirc_full_forward")
+                                         _dev.ptr(flags), _dev.stream()), "nirc_full_forward")
 
     def barrier():
         if dist is not None:

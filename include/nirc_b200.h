@@ -40,6 +40,13 @@ enum {
   NIRC_E_UNSUPPORTED = 6
 };
 
+/* Bits of the device-side status word (`int32_t* status_flags`) that the
+ * asynchronous entries set instead of returning; the shim reads it with the
+ * call's results and raises the matching exception. */
+#define NIRC_FLAG_BAD_PDF 1     /* InvalidSampleError (losses.py:18-20) */
+#define NIRC_FLAG_DIVERGED 2    /* DivergenceError: non-finite loss or theta (mlp.py:104-105) */
+#define NIRC_FLAG_BAD_INDEX 4   /* ConfigError: dir_to_surf index outside [0, n_surf) */
+
 /* Network layout; mirrors NetSpec (pkg/src/nirclab/mlp.py:26-62).
  * theta = [hash tables (levels*2^table_log2*feats)] ++ per layer W (dout x din,
  * row-major) ++ b.  sh_k[l*8+m] holds NORM[l,0] for m == 0 and
@@ -156,23 +163,33 @@ int nirc_mlp_backward(const nirc_spec_t* spec, const float* theta,
 
 /* full_forward (mlp.py:216-224) = encode_batch + mlp_forward fused in one
  * persistent sm_100a kernel: hash-grid + SH + aux encoding written straight
- * into the SMEM A-tile, every layer a 3xTF32 tcgen05.mma with the fp32
- * accumulator in TMEM.  precision: 0 = tcgen05 3xTF32, 1 = fp32 SIMT twin,
- * 2 = tcgen05 2xFP16 split (3 products; |activations| < 65504). */
+ * into the A operand, every layer a tcgen05.mma with the fp32 accumulator in
+ * TMEM.  precision: 0 = tcgen05 3xTF32, 1 = fp32 SIMT twin, 2 = tcgen05
+ * 2xFP16 split (3 products).  The 2xFP16 path guards the fp16 range: 32-row
+ * units holding an input, weight or activation >= 65000 (or NaN) are
+ * recomputed by the fp32 twin in a fix-up launch (stream-ordered, no sync).
+ * status_flags (nullable): |= NIRC_FLAG_DIVERGED if theta holds a non-finite
+ * value (the reference raises DivergenceError, mlp.py:104-105). */
 int nirc_full_forward(const nirc_spec_t* spec, const float* theta,
                       const double* pos, const double* normal,
                       const double* albedo, const double* rough,
                       const double* dirs, int64_t n, float* Y,
-                      int32_t precision, void* stream);
+                      int32_t precision, int32_t* status_flags, void* stream);
 
-/* Cache._query / nirc_query (pkg/src/nirclab/caches.py:211-233): n_dirs
- * directions, direction i against surface dir_to_surf[i]; surf rows
- * (n_surf, 10) = pos.xyz, ns.xyz, albedo.rgb, roughness (device f64);
- * dirs (n_dirs, 3) f64; Y (n_dirs, dout) f32; precision as nirc_full_forward.
- * NIRC_E_CONFIG for an index outside [0, n_surf) (synchronises the stream). */
+/* Cache._query / nirc_query (pkg/src/nirclab/caches.py:211-233), amortised
+ * as the reference does it: n_dirs directions, direction i against surface
+ * dir_to_surf[i]; each surface's hash block is encoded once, then every
+ * direction row adds its SH block and runs the fused tcgen05 network.
+ * surf rows (n_surf, 10) = pos.xyz, ns.xyz, albedo.rgb, roughness (device
+ * f64); dirs (n_dirs, 3) f64; Y (n_dirs, dout) f32; precision 2 = tcgen05
+ * 2xFP16 (range-guarded as nirc_full_forward), otherwise the fp32 twin.
+ * Fully asynchronous: an index outside [0, n_surf) sets
+ * NIRC_FLAG_BAD_INDEX in status_flags (required) and NaN in its row; a
+ * non-finite theta sets NIRC_FLAG_DIVERGED. */
 int nirc_query(const nirc_spec_t* spec, const float* theta, const double* surf,
                int64_t n_surf, const double* dirs, const int32_t* dir_to_surf,
-               int64_t n_dirs, float* Y, int32_t precision, void* stream);
+               int64_t n_dirs, float* Y, int32_t precision, int32_t* status_flags,
+               void* stream);
 
 /* ---- losses (pkg/src/nirclab/losses.py) --------------------------------- */
 /* kind: 0 l2, 1 relative_l2, 2 variance, 3 bce.  Y (n,3) f32, target (n,3)

@@ -114,7 +114,7 @@ SIGNATURES = {
     "nirc_scatter_grid_grad": (I32, [SPEC, P, P, P, P, I64, I64, P]),
     "nirc_mlp_forward": (I32, [SPEC, P, P, I64, P, P, P, P]),
     "nirc_mlp_backward": (I32, [SPEC, P, P, P, P, I64, P, P, P, P]),
-    "nirc_full_forward": (I32, [SPEC, P, P, P, P, P, P, I64, P, I32, P]),
+    "nirc_full_forward": (I32, [SPEC, P, P, P, P, P, P, I64, P, I32, P, P]),
     "nirc_loss": (I32, [I32, P, P, P, P, F64, I64, P, P, P, P, P]),
     "nirc_adam_step": (I32, [P, P, P, P, I64, P, P, F64, F64, F64, F64, P, P, P]),
     "nirc_train_step": (I32, [SPEC, P, P, P, P, P, C.POINTER(NircRecords), U64, I64, I32,
@@ -142,7 +142,7 @@ SIGNATURES = {
                                     P]),
     "nirc_integrand_samples": (I32, [C.POINTER(NircScene), P, U64, U64, I32, P, P, P, P, P, P,
                                      P, P, P, P]),
-    "nirc_query": (I32, [SPEC, P, P, I64, P, P, I64, P, I32, P]),
+    "nirc_query": (I32, [SPEC, P, P, I64, P, P, I64, P, I32, P, P]),
     "nirc_bvh_node_count": (I64, [I64]),
     "nirc_scene_packed_bytes": (I64, [C.POINTER(NircScene)]),
     "nirc_pack_scene": (I32, [C.POINTER(NircScene), P, I64, P]),
@@ -188,6 +188,23 @@ def last_error():
     buf = C.create_string_buffer(512)
     load().nirc_last_error(buf, 512)
     return buf.value.decode(errors="replace")
+
+
+FLAG_BAD_PDF = 1       # include/nirc_b200.h NIRC_FLAG_*
+FLAG_DIVERGED = 2
+FLAG_BAD_INDEX = 4
+
+
+def check_flags(flags, what="nirc call"):
+    """Raise the reference's exception for a device status word (reads it:
+    synchronises with the stream that wrote it)."""
+    v = int(flags[0].item()) if hasattr(flags, "item") else int(flags)
+    if v & FLAG_DIVERGED:
+        raise DivergenceError(f"{what}: non-finite network parameter")
+    if v & FLAG_BAD_PDF:
+        raise InvalidSampleError(f"{what}: pdf <= 0")
+    if v & FLAG_BAD_INDEX:
+        raise ConfigError(f"{what}: dir_to_surf index outside [0, n_surf)")
 
 
 def check(status, what="nirc call"):

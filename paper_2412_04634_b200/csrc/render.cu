@@ -27,7 +27,7 @@ namespace nirc {
 extern long long* g_infer_probe;
 int sm_count();
 int pack_weights(const nirc_spec_t& sp, const tc::TcNet& net, const float* theta, cudaStream_t s,
-                 uint8_t** img, float** bias);
+                 AsyncBuf& buf, PackedNet* out);
 int tc_groups_for(const tc::TcNet& net, uint32_t extra_per_group);
 bool default_layout(const nirc_spec_t& sp);
 
@@ -846,6 +846,8 @@ struct InferArgs {
   int rows_per_vertex;  // R = max(nc) + 1
   int verts_per_tile;   // S = 128 / R
   long long* dbg;       // optional phase timestamps (CTA 0, group 0, thread 0)
+  const int32_t* w_unsafe;  // F16x2: a weight outside the fp16 range (every tile flagged)
+  int32_t* fix;             // F16x2 range guard: [count, tile ids...] for k_infer_fix
 };
 
 // Deferred vertex term from its rows' contributions (row k at rows[3k]):
@@ -907,6 +909,9 @@ __global__ void __launch_bounds__(NG * 128, 1)
   const int64_t ntiles = (nverts + S - 1) / S;
   uint32_t phase = 0;
   const bool probe = a.dbg && blockIdx.x == 0 && threadIdx.x == 0;
+  __shared__ int s_unsafe[NG];
+  if (tg == 0) s_unsafe[group] = 0;
+  const bool all_unsafe = kTS && *a.w_unsafe != 0;
   int it = 0;
   for (int64_t tile = (int64_t)blockIdx.x * NG + group; tile < ntiles;
        tile += (int64_t)gridDim.x * NG, ++it) {
@@ -955,9 +960,13 @@ __global__ void __launch_bounds__(NG * 128, 1)
     }
     float y[4];
     if constexpr (kTS) {
+      bool unsafe = all_unsafe || tc::f16_unsafe(x, 48);
       tc::write_a_row_ts<48>(tmem_d + 64 + lane_off, tmem_d + 96 + lane_off, x);
       if (pb) pb[2] = clock64();
-      tc::run_chain_ts(net, s0 + L.w_off, s_bias, group, tg, tmem_d, mbar, phase, y);
+      tc::run_chain_ts(net, s0 + L.w_off, s_bias, group, tg, tmem_d, mbar, phase, y, unsafe);
+      // fp16 range guard: the tile is recomputed in fp32 by k_infer_fix
+      if (__any_sync(0xffffffffu, unsafe && rd.kind != 0) && (tg & 31) == 0)
+        atomicOr(&s_unsafe[group], 1);
     } else {
       tc::write_a_row<P, 48>(a_hi, a_lo, tg, x);
       if (pb) pb[2] = clock64();
@@ -988,10 +997,79 @@ __global__ void __launch_bounds__(NG * 128, 1)
       a.result[3 * r.slot + 1] = o[1];
       a.result[3 * r.slot + 2] = o[2];
     }
+    if (kTS && tg == 0 && s_unsafe[group]) {
+      s_unsafe[group] = 0;
+      a.fix[1 + atomicAdd(a.fix, 1)] = (int32_t)tile;
+    }
     tc::named_bar_sync(1 + group, tc::kGroupThreads);
     if (pb) pb[4] = clock64();
   }
   tc::tc_epilogue(tmem_base, NG, P::kId);
+}
+
+// fp16 range fix-up of k_infer_tc<F16x2>: recomputes every vertex of the
+// flagged tiles (a.fix) with the fp32 twin -- same rows, same k-ordered
+// combine -- and overwrites their results.  A no-op when nothing was flagged.
+__global__ void __launch_bounds__(128) k_infer_fix(nirc_spec_t sp, const float* __restrict__ theta,
+                                                   InferArgs a) {
+  extern __shared__ float wsm[];
+  __shared__ double s_con[128 * 3];
+  const int cnt = a.fix[0];
+  if (cnt == 0) return;
+  const int np = (int)(sp.theta_len - sp.grid_len);
+  for (int i = threadIdx.x; i < np; i += blockDim.x) wsm[i] = theta[sp.grid_len + i];
+  __syncthreads();
+  const int R = a.rows_per_vertex, S = a.verts_per_tile;
+  const int64_t nverts = (int64_t)a.counters[0];
+  const uint32_t T = 1u << sp.table_log2;
+  const int tg = threadIdx.x;
+  for (int e = blockIdx.x; e < cnt; e += gridDim.x) {
+    const int64_t v0 = (int64_t)a.fix[1 + e] * S;
+    const int j = tg / R, k = tg % R;
+    const int64_t vid = v0 + j;
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+    if (j < S && vid < nverts) {
+      const CacheVertex& r = a.cv[vid];
+      const RowDir rd = row_direction_fast(r, k);
+      if (rd.kind != 0) {
+        float feat[24];
+        const float ux = norm_coord(r.pos[0], sp.bb_min[0], sp.bb_inv[0]);
+        const float uy = norm_coord(r.pos[1], sp.bb_min[1], sp.bb_inv[1]);
+        const float uz = norm_coord(r.pos[2], sp.bb_min[2], sp.bb_inv[2]);
+        for (int lvl = 0; lvl < 12; ++lvl) {
+          const float2 f = level_features2(theta + (size_t)lvl * T * 2,
+                                           level_cell(ux, uy, uz, sp.res[lvl]), T - 1u);
+          feat[2 * lvl] = f.x;
+          feat[2 * lvl + 1] = f.y;
+        }
+        float x[64], b[64];
+        build_row_fast(feat, r, rd.wi, sp.sh_k, x);
+        simt_net_row(sp, wsm, x, b);
+        if (rd.kind == 1) {
+          c0 = (double)x[0] * rd.f.x * rd.s;
+          c1 = (double)x[1] * rd.f.y * rd.s;
+          c2 = (double)x[2] * rd.f.z * rd.s;
+        } else {
+          c0 = (double)x[0];
+          c1 = (double)x[1];
+          c2 = (double)x[2];
+        }
+      }
+    }
+    s_con[3 * tg] = c0;
+    s_con[3 * tg + 1] = c1;
+    s_con[3 * tg + 2] = c2;
+    __syncthreads();
+    if (tg < S && v0 + tg < nverts) {
+      const CacheVertex& r = a.cv[v0 + tg];
+      double o[3];
+      vertex_result(r, s_con + 3 * (tg * R), o);
+      a.result[3 * r.slot] = o[0];
+      a.result[3 * r.slot + 1] = o[1];
+      a.result[3 * r.slot + 2] = o[2];
+    }
+    __syncthreads();
+  }
 }
 
 // Generic-shape fallback of the same stage (any NetSpec): one thread per
@@ -1230,6 +1308,7 @@ size_t aup(size_t x) { return (x + 255) & ~(size_t)255; }
 struct RenderWs {
   double *acc, *result, *rowbuf;
   int32_t* term;
+  int32_t* fix;  // F16x2 range-guard tile list (count + ids)
   CacheVertex* cv;
   unsigned long long* counters;
   size_t bytes;
@@ -1261,6 +1340,7 @@ RenderWs carve_render(const nirc_render_cfg_t& c, void* base) {
   w.result = (double*)take(ncv * 24 + 24);
   w.cv = (CacheVertex*)take(ncv * sizeof(CacheVertex) + 16);
   w.counters = (unsigned long long*)take(64);
+  w.fix = (int32_t*)take((ncv + 2) * 4);
   w.rowbuf = (double*)take(0);  // sized on demand for the SIMT fallback
   w.bytes = off;
   return w;
@@ -1367,7 +1447,7 @@ static int render_impl(const nirc_scene_t* scene, const double* cam, const nirc_
   if (tl) {
     if (!spec || !theta) return NIRC_E_CONFIG;
     const int R = rows_per_vertex(c);
-    InferArgs a{w.cv, w.counters, w.result, nullptr, R, 128 / R, g_infer_probe};
+    InferArgs a{w.cv, w.counters, w.result, nullptr, R, 128 / R, g_infer_probe, nullptr, w.fix};
     const int prec = c.precision == 2 ? tc::PrecF16x2::kId : tc::PrecTF32x3::kId;
     tc::TcNet net;
     const bool tc_ok =
@@ -1375,18 +1455,22 @@ static int render_impl(const nirc_scene_t* scene, const double* cam, const nirc_
     const uint32_t extra =
         (uint32_t)(128 * 3 * 8 + a.verts_per_tile * 24 * 4 + 16 + a.verts_per_tile * sizeof(CacheVertex));
     const int ng = tc_ok ? tc_groups_for(net, extra) : 0;
+    AsyncBuf wbuf(s);
     if (ng > 0) {
-      uint8_t* img_w;
-      float* bias;
-      int st = pack_weights(*spec, net, theta, s, &img_w, &bias);
+      PackedNet pn;
+      int st = pack_weights(*spec, net, theta, s, wbuf, &pn);
       if (st) return st;
+      a.w_unsafe = pn.unsafe;
+      const bool ts = prec == tc::PrecF16x2::kId;
+      const size_t fix_sm = (size_t)(spec->theta_len - spec->grid_len) * 4;
+      if (ts) NIRC_CUDA_TRY(cudaMemsetAsync(w.fix, 0, 4, s));
       const tc::TcSmem L = tc::tc_smem_layout(net, ng, ng * extra);
       const int grid = sm_count();
       auto launch = [&](auto kern, int threads) -> int {
         NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)kern,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)L.total));
-        kern<<<grid, threads, L.total, s>>>(*spec, net, L, theta, img_w, bias, a);
+        kern<<<grid, threads, L.total, s>>>(*spec, net, L, theta, pn.img, pn.bias, a);
         return NIRC_OK;
       };
       if (prec == tc::PrecF16x2::kId) {
@@ -1400,6 +1484,13 @@ static int render_impl(const nirc_scene_t* scene, const double* cam, const nirc_
       }
       if (st) return st;
       NIRC_LAUNCH_CHECK("k_infer_tc");
+      if (ts) {
+        NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)k_infer_fix,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)fix_sm));
+        k_infer_fix<<<sm_count(), 128, fix_sm, s>>>(*spec, theta, a);
+        NIRC_LAUNCH_CHECK("k_infer_fix");
+      }
     }
     if (ng == 0) {
       // generic layouts: SIMT rows into a row buffer, then per-vertex combine

@@ -288,6 +288,21 @@ __device__ __forceinline__ void run_chain(const TcNet& net, uint32_t w_base,
 // fp16 element (row m, k) sits at lane m, column k/2, half k%2.
 constexpr uint32_t kTsColsPerGroup = 128;
 
+// fp16 range guard of the F16x2 split: an operand must round to a finite
+// fp16 hi part.  Rows holding a value at or above this bound (or a NaN) are
+// flagged by the chain and recomputed by the fp32 SIMT fix-up kernels.
+constexpr float kF16Max = 65000.0f;
+
+__device__ __forceinline__ bool f16_unsafe(const float* x, int n) {
+  float m = 0.0f;
+  bool nan = false;
+  for (int i = 0; i < n; ++i) {
+    m = fmaxf(m, fabsf(x[i]));
+    nan |= x[i] != x[i];
+  }
+  return nan || !(m < kF16Max);
+}
+
 // Writes this thread's row (K values, K % 16 == 0) into A_hi / A_lo (TMEM).
 template <int K>
 __device__ __forceinline__ void write_a_row_ts(uint32_t a_hi, uint32_t a_lo, const float* x) {
@@ -328,10 +343,11 @@ __device__ __forceinline__ void issue_layer_ts(const TcNet& net, int l, uint32_t
 
 // Runs the network for the group's tile; precondition: this thread wrote its
 // layer-0 row with write_a_row_ts and waited (tcgen05.wait::st).
+// `unsafe` accumulates the fp16 range guard over every hidden activation.
 __device__ __forceinline__ void run_chain_ts(const TcNet& net, uint32_t w_base,
                                              const float* __restrict__ s_bias, int group, int tg,
                                              uint32_t tmem_grp, uint32_t mbar, uint32_t& phase,
-                                             float* y) {
+                                             float* y, bool& unsafe) {
   const uint32_t lane_off = (uint32_t)((tg >> 5) * 32) << 16;
   const uint32_t tmem_d = tmem_grp, a_hi = tmem_grp + 64, a_lo = tmem_grp + 96;
   tmem_wait_st();
@@ -361,11 +377,14 @@ __device__ __forceinline__ void run_chain_ts(const TcNet& net, uint32_t w_base,
           *reinterpret_cast<float4*>(bq + 4 * j) =
               *reinterpret_cast<const float4*>(b + half * 32 + 4 * j);
         tmem_wait_ld();
+        float hm = 0.0f;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const float z = h[j] + bq[j];
           h[j] = z > 0.0f ? z : 0.0f;
+          hm = fmaxf(hm, h[j]);
         }
+        unsafe |= !(hm < kF16Max);
         uint32_t hh[16], ll[16];
 #pragma unroll
         for (int c = 0; c < 4; ++c) PrecF16x2::split8(h + 8 * c, hh + 4 * c, ll + 4 * c);
@@ -461,4 +480,34 @@ __device__ __forceinline__ void tc_epilogue(uint32_t tmem_base, int ngroups, int
 }
 
 }  // namespace tc
+
+// fp32 network of one encoded row (in a[], result in a[0..dout)); W is the
+// shared-memory copy of theta[grid_len:].
+__device__ inline void simt_net_row(const nirc_spec_t& sp, const float* __restrict__ W, float* a,
+                                    float* b) {
+  for (int l = 0; l < sp.n_layers; ++l) {
+    const int din = sp.dims[l], dout = sp.dims[l + 1];
+    const float* w = W + (sp.w_off[l] - sp.grid_len);
+    const float* bias = W + (sp.b_off[l] - sp.grid_len);
+    const bool last = l == sp.n_layers - 1;
+#pragma unroll 4
+    for (int j = 0; j < dout; ++j) {
+      float acc = 0.0f;
+#pragma unroll 8
+      for (int i = 0; i < din; ++i) acc = fmaf(a[i], w[j * din + i], acc);
+      const float z = acc + bias[j];
+      b[j] = (!last || sp.out_act == 0) ? (z > 0.0f ? z : 0.0f) : 1.0f / (1.0f + expf(-z));
+    }
+    for (int j = 0; j < dout; ++j) a[j] = b[j];
+  }
+}
+
+// One launch's packed weight image (k_pack_weights), in a caller-owned
+// stream-ordered buffer; `unsafe` = a weight outside the F16x2 range.
+struct PackedNet {
+  uint8_t* img;
+  float* bias;
+  int32_t* unsafe;
+};
+
 }  // namespace nirc

@@ -185,6 +185,7 @@ def _full_forward_pipelined(spec, th, host, precision, out=None, chunk=None):
     ev_out = [torch.cuda.Event() for _ in range(2)]
     lib = _lib.load()
     cs = _lib.make_c_spec(spec)
+    flags = _dev.zeros((1,), torch.int32)
     s_in.wait_stream(cur)
     for k, lo in enumerate(range(0, n, m)):
         hi = min(n, lo + m)
@@ -199,7 +200,8 @@ def _full_forward_pipelined(spec, th, host, precision, out=None, chunk=None):
         if k >= 2:
             cur.wait_event(ev_out[b])  # chunk k-2's outputs left ybuf[b]
         st = lib.nirc_full_forward(cs, _dev.ptr(th), *[_dev.ptr(d) for d in bufs[b]], hi - lo,
-                                   _dev.ptr(ybuf[b]), int(precision), _dev.stream())
+                                   _dev.ptr(ybuf[b]), int(precision),
+                                   _dev.ptr(flags) if k == 0 else _dev.ptr(None), _dev.stream())
         _lib.check(st, "nirc_full_forward")
         ev_comp[b].record(cur)
         with torch.cuda.stream(s_out):
@@ -211,6 +213,11 @@ def _full_forward_pipelined(spec, th, host, precision, out=None, chunk=None):
             d.record_stream(s_in)
         ybuf[b].record_stream(s_out)
     cur.wait_stream(s_out)
+    # the host result is complete only when the last D2H copy has landed:
+    # wait for it before handing the buffer to the caller (and raise the
+    # reference's DivergenceError on a non-finite theta, mlp.py:104-105)
+    s_out.synchronize()
+    _lib.check_flags(flags, "full_forward")
     return y_host
 
 
@@ -229,15 +236,19 @@ def query(spec, theta, surf, dirs, dir_to_surf, precision=PRECISION_F16X2):
     Y = _dev.empty((n, int(spec.dims[-1])), torch.float32)
     if n:
         lib = _lib.load()
+        flags = _dev.zeros((1,), torch.int32)
         st = lib.nirc_query(_lib.make_c_spec(spec), _dev.ptr(th), _dev.ptr(S), int(S.shape[0]),
                             _dev.ptr(D), _dev.ptr(idx), n, _dev.ptr(Y), int(precision),
-                            _dev.stream())
+                            _dev.ptr(flags), _dev.stream())
         if st == _lib.NIRC_E_UNSUPPORTED:  # non-default layouts: generic device path
             il = idx.long()
+            if int(il.min()) < 0 or int(il.max()) >= int(S.shape[0]):
+                raise _lib.ConfigError("nirc_query: dir_to_surf index outside [0, n_surf)")
             Y = full_forward(spec, th, S[il, 0:3], S[il, 3:6], S[il, 6:9], S[il, 9], D,
                              precision=precision)
         else:
             _lib.check(st, "nirc_query")
+            _lib.check_flags(flags, "nirc_query")
     return Y.cpu().numpy() if host else Y
 
 
@@ -266,14 +277,18 @@ def full_forward(spec, theta, pos, normal, albedo, rough, dirs, training=False,
     n = int(args[0].shape[0])
     Y = _dev.empty((n, int(spec.dims[-1])), torch.float32)
     lib = _lib.load()
+    flags = _dev.zeros((1,), torch.int32)
     st = lib.nirc_full_forward(_lib.make_c_spec(spec), _dev.ptr(th),
                                *[_dev.ptr(a) for a in args], n, _dev.ptr(Y), int(precision),
-                               _dev.stream())
+                               _dev.ptr(flags), _dev.stream())
     if st == _lib.NIRC_E_UNSUPPORTED:
         # non-default layouts (tests' tiny nets) take the generic device path
         X, _, _ = encode_batch(spec, th, *args)
         return _dev.out(mlp_forward(spec, th, X), host)
     _lib.check(st, "nirc_full_forward")
+    # mlp.py:104-105: a non-finite theta raises DivergenceError (reads the
+    # device flag, i.e. waits for the launch)
+    _lib.check_flags(flags, "full_forward")
     return _dev.out(Y, host)
 
 

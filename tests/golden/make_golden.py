@@ -115,6 +115,34 @@ def golden_train():
     np.savez_compressed(os.path.join(HERE, "train_step.npz"), **out)
 
 
+def golden_train1():
+    """ONE train_frame step per record set (m starts at 0, so the Adam
+    moment m = f32(0.1) * g and v = f32(0.01) * g^2 expose the reference's
+    raw gradient of the step: mlp_backward + scatter_grid_grad)."""
+    from nirclab.adam import AdamState
+    from nirclab.caches import Records, train_frame
+    from nirclab.mlp import init_theta, make_spec
+
+    class _C:
+        pass
+
+    out = {}
+    for tag, n in (("small", 3000), ("big", 20000)):
+        rec = synth_records(n, seed=5)
+        spec = make_spec(table=2 ** 12, depth=4, bb_min=np.zeros(3), bb_ext=np.ones(3))
+        theta = init_theta(spec, seed=3, out_scale=0.05)
+        c = _C()
+        c.spec, c.theta, c.adam = spec, theta, AdamState(theta)
+        c.seed, c.frame, c.loss_kind, c.loss_eps = 7, 2, "relative_l2", 0.01
+        c.running_mean = np.zeros(3)
+        c.kind, c.snapshot_dir = "nirc", None
+        trace = train_frame(c, Records(kind="nirc", frame=2, **rec), steps=1)
+        out[f"{tag}_trace"] = np.array(trace)
+        out[f"{tag}_m"] = c.adam.m
+        out[f"{tag}_v"] = c.adam.v
+    np.savez_compressed(os.path.join(HERE, "train1.npz"), **out)
+
+
 def golden_losses_adam():
     """Known-answer loss values and 20 Adam steps (incl. a skipped one)."""
     from nirclab.adam import AdamState, adam_step
@@ -439,7 +467,76 @@ def golden_big():
     np.savez_compressed(os.path.join(HERE, "big.npz"), **out)
 
 
+def _corn_text(res, emit_scale=1.0):
+    """The reference's Cornell box edited like tests/scene_texts.py."""
+    import nirclab
+
+    sys.path.insert(0, os.path.dirname(HERE))
+    from scene_texts import edit_scene
+
+    path = os.path.join(os.path.dirname(nirclab.__file__), "data", "cornell.scene")
+    return edit_scene(open(path).read(), res, emit_scale)
+
+
+def golden_trained():
+    """Caches TRAINED by the reference ("a trained
+    Cornell snapshot"): collect + train_frame(steps=4) per frame on the
+    Cornell box at 64^2 (D = 2, the cfg2 network, 24 frames) and on a
+    Cornell box with a 100x brighter lamp (D = 4, 16 frames).  Stores the
+    trained theta, the reference's full_forward on 4096 queries inside each
+    cache's bounding box, a range-stress variant of the D = 2 net (first
+    layer x 2^17, output layer x 2^-17: hidden activations far beyond the
+    fp16 range) with its reference outputs, and two-level renders with the
+    trained caches."""
+    from nirclab.caches import Cache
+    from nirclab.estimators import EstimatorConfig, render
+    from nirclab.mlp import full_forward, mlp_forward
+    from nirclab.encoding import encode_batch
+    from nirclab.scene import load_scene
+
+    out = {}
+    n = 4096
+    for tag, scale, depth, frames in (("corn", 1.0, 2, 24), ("bright", 100.0, 4, 16)):
+        sc = load_scene(_corn_text(64, scale))
+        c = Cache.create("nirc", sc, seed=5, depth=depth)
+        for f in range(frames):
+            rec = c.collect(frame=f)
+            c.train_frame(rec, steps=4)
+        spec = c.spec
+        pos, nrm, alb, rough, dirs = measure_queries(n, seed=7)
+        bb_min = np.asarray(spec.bb_min, float)
+        bb_ext = 1.0 / np.asarray(spec.bb_inv, float)
+        pos = bb_min + pos * bb_ext
+        out[f"{tag}_theta"] = c.theta.copy()
+        out[f"{tag}_bb_min"] = bb_min
+        out[f"{tag}_bb_ext"] = bb_ext
+        out[f"{tag}_q"] = np.concatenate([pos, nrm, alb, rough[:, None], dirs], axis=1)
+        out[f"{tag}_Y"] = full_forward(spec, c.theta, pos, nrm, alb, rough, dirs)
+        out[f"{tag}_frame"] = np.int64(c.frame)
+        r = render(sc, EstimatorConfig(mode="two-level", nc=(8,), max_cache_vertices=1), cache=c,
+                   seed=3, spp=1, frame=c.frame)
+        out[f"{tag}_tl_image"] = r.image
+        out[f"{tag}_tl_plen"] = r.path_length
+        if tag == "corn":
+            th = c.theta.copy()
+            w0, b0 = int(spec.w_off[0]), int(spec.b_off[0])
+            th[w0: b0 + int(spec.dims[1])] *= np.float32(2.0 ** 17)
+            wl = int(spec.w_off[-1])
+            th[wl:] *= np.float32(2.0 ** -17)
+            X, _, _ = encode_batch(spec, th, pos, nrm, alb, rough, dirs)
+            out["stress_theta_scale"] = np.float64(2.0 ** 17)
+            out["stress_Y"] = mlp_forward(spec, th, X)
+            h1 = np.maximum(X @ th[w0: w0 + int(spec.dims[0]) * int(spec.dims[1])].reshape(
+                int(spec.dims[1]), int(spec.dims[0])).T + th[b0: b0 + int(spec.dims[1])], 0.0)
+            out["stress_h1_max"] = np.float64(h1.max())
+    np.savez_compressed(os.path.join(HERE, "trained.npz"), **out)
+
+
 if __name__ == "__main__" and len(sys.argv) > 1:
+    if "trained" in sys.argv:
+        golden_trained()
+    if "train1" in sys.argv:
+        golden_train1()
     if "big" in sys.argv:
         golden_big()
     if "baseline" in sys.argv:
