@@ -744,7 +744,11 @@ int launch_fused_train(const nirc_spec_t& sp, const float* theta, const nirc_rec
                        const int64_t* idx, int64_t B, int loss_kind, double loss_eps,
                        float* grad, float* partials, double* loss_part, double* loss_out,
                        int32_t* flags, int32_t* adam_bad, cudaStream_t s, int64_t tile0,
-                       int64_t tile1, int mode);
+                       int64_t tile1, int mode, const float* rstat);
+int64_t train_static_bytes(int64_t n);
+int launch_record_static(const nirc_spec_t& sp, const nirc_records_t& rec, float* out,
+                         cudaStream_t s);
+bool train_tc_supported(const nirc_spec_t& sp);
 constexpr int kFusedTileRows = 128;  // rows per k_train_tile CTA (train_fused.cu kTR)
 }  // namespace nirc
 
@@ -908,6 +912,7 @@ struct TrainWs {
   int32_t* adam_bad;
   float* fpart;      // fused path: per-tile MLP gradient partials
   double* floss;     // fused path: per-tile loss partials
+  float* rstat;      // tcgen05 path: per-record static encoding (u, SH, aux)
   size_t bytes;
 };
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -945,6 +950,7 @@ TrainWs carve_train(const nirc_spec_t& sp, int64_t n, int64_t B, int steps, void
   const int64_t slots = ntiles > 256 ? ntiles : 256;
   w.fpart = (float*)take(slots * (sp.theta_len - sp.grid_len) * 4);
   w.floss = (double*)take(slots * 8);
+  w.rstat = (float*)take(train_static_bytes(n));
   w.bytes = off;
   return w;
 }
@@ -1004,7 +1010,7 @@ static int step_body(const nirc_spec_t* spec, float* theta, float* m, float* v, 
                      int64_t* skipped, const nirc_records_t* rec, const int64_t* idx,
                      int64_t B, int32_t loss_kind, double loss_eps, double lr,
                      double* running_mean, double* loss_out, int32_t* status_flags,
-                     const TrainWs& w, void* stream) {
+                     const TrainWs& w, void* stream, const float* rstat) {
   cudaStream_t s = S(stream);
   int st;
   if (use_fused(*spec, loss_kind)) {
@@ -1012,7 +1018,7 @@ static int step_body(const nirc_spec_t* spec, float* theta, float* m, float* v, 
     const int64_t ntiles = (B + kFusedTileRows - 1) / kFusedTileRows;
     if ((st = launch_fused_train(*spec, theta, *rec, idx, B, loss_kind, loss_eps, w.grad,
                                  w.fpart, w.floss, loss_out, status_flags, w.adam_bad, s, 0,
-                                 ntiles, 0)))
+                                 ntiles, 0, rstat)))
       return st;
     return launch_adam(theta, m, v, w.grad, spec->theta_len, t, skipped, (float)lr, w.adam_bad,
                        status_flags, s);
@@ -1070,7 +1076,7 @@ extern "C" int nirc_train_step(const nirc_spec_t* spec, float* theta, float* m, 
   if (batch_idx_out)
     NIRC_CUDA_TRY(cudaMemcpyAsync(batch_idx_out, w.sel.sidx, B * 8, cudaMemcpyDeviceToDevice, s));
   return step_body(spec, theta, m, v, t, skipped, rec, w.sel.sidx, B, loss_kind, loss_eps, lr,
-                   running_mean, loss_out, status_flags, w, stream);
+                   running_mean, loss_out, status_flags, w, stream, nullptr);
 }
 
 extern "C" int nirc_train_frame(const nirc_spec_t* spec, float* theta, float* m, float* v,
@@ -1091,10 +1097,15 @@ extern "C" int nirc_train_frame(const nirc_spec_t* spec, float* theta, float* m,
     return NIRC_E_CONFIG;
   }
   if ((st = select_batches(w, seed, frame, 0, steps, n, B, status_flags, S(stream)))) return st;
+  const float* rstat = nullptr;  // theta-independent encoding blocks: once for all steps
+  if (use_fused(*spec, loss_kind) && train_tc_supported(*spec)) {
+    if ((st = launch_record_static(*spec, *rec, w.rstat, S(stream)))) return st;
+    rstat = w.rstat;
+  }
   for (int k = 0; k < steps; ++k)
     if ((st = step_body(spec, theta, m, v, t, skipped, rec, w.sel.sidx + (int64_t)k * n, B,
                         loss_kind, loss_eps, lr, running_mean, loss_out + k, status_flags, w,
-                        stream)))
+                        stream, rstat)))
       return st;
   return NIRC_OK;
 }
@@ -1138,7 +1149,8 @@ extern "C" int nirc_train_grad(const nirc_spec_t* spec, const float* theta,
   if (batch_idx_out)
     NIRC_CUDA_TRY(cudaMemcpyAsync(batch_idx_out, w.sel.sidx, B * 8, cudaMemcpyDeviceToDevice, s));
   return launch_fused_train(*spec, theta, *rec, w.sel.sidx, B, loss_kind, loss_eps, grad, w.fpart,
-                            w.floss, aux, status_flags, nullptr, s, tile_begin, tile_end, 1);
+                            w.floss, aux, status_flags, nullptr, s, tile_begin, tile_end, 1,
+                            nullptr);
 }
 
 namespace nirc {

@@ -18,6 +18,7 @@
 //
 // fp32 SIMT: the reference's accuracy class.
 #include <cmath>
+#include <cstdlib>
 #include "common.cuh"
 #include "tc_common.cuh"
 
@@ -93,7 +94,9 @@ __device__ __forceinline__ float relu(float z) { return z > 0.0f ? z : 0.0f; }
 // ldw) and W^T (din x ldt) zero padded, and the biases, per layer -- built
 // once per step so that every tile CTA stages it with TMA bulk copies.
 __global__ void k_pack_train_weights(nirc_spec_t sp, FusedLayout L,
-                                     const float* __restrict__ theta, float* __restrict__ img) {
+                                     const float* __restrict__ theta, float* __restrict__ img,
+                                     const int32_t* __restrict__ gate = nullptr) {
+  if (gate != nullptr && gate[0] == 0) return;  // fix-up list empty: nothing to pack
   const int l = blockIdx.y;
   const float* Wg = theta + sp.w_off[l];
   const int din = L.din[l], dout = L.dout[l], ldw = L.ldw[l], ldt = L.ldt[l];
@@ -202,14 +205,64 @@ __global__ void k_reduce_grad(nirc_spec_t sp, const float* __restrict__ partials
 }
 
 
+bool train_tc_supported(const nirc_spec_t& sp);
+int launch_train_tc(const nirc_spec_t& sp, const float* theta, const float* rstat,
+                    const nirc_records_t& rec, const int64_t* idx, int64_t B, int loss_kind,
+                    double loss_eps, float* grad, float* partials, double* loss_part,
+                    int32_t* flags, cudaStream_t s, int64_t tile0, int64_t tile1, int32_t* fix,
+                    float* dx_out);
+int64_t train_static_bytes(int64_t n);
+int launch_record_static(const nirc_spec_t& sp, const nirc_records_t& rec, float* out,
+                         cudaStream_t s);
+
 // Tiles [tile0, tile1) of the batch (all of it on one GPU; one shard of it
-// per GPU in the multi-GPU frame, mode 1).
+// per GPU in the multi-GPU frame, mode 1).  The default layout trains on
+// tcgen05 (train_tc.cu) with the fp32 SIMT kernel as the fp16-range fix-up;
+// other layouts (or NIRC_TRAIN_SIMT=1) run the SIMT kernel throughout.
 int launch_fused_train(const nirc_spec_t& sp, const float* theta, const nirc_records_t& rec,
                        const int64_t* idx, int64_t B, int loss_kind, double loss_eps,
                        float* grad, float* partials, double* loss_part, double* loss_out,
                        int32_t* flags, int32_t* adam_bad, cudaStream_t s, int64_t tile0,
-                       int64_t tile1, int mode) {
+                       int64_t tile1, int mode, const float* rstat) {
   const int ntiles = (int)(tile1 > tile0 ? tile1 - tile0 : 0);
+  const bool force_simt = getenv("NIRC_TRAIN_SIMT") != nullptr;  // read per call (tests switch it)
+  if (!force_simt && train_tc_supported(sp)) {
+    NIRC_CUDA_TRY(cudaMemsetAsync(grad, 0, sp.grid_len * 4, s));
+    if (adam_bad) NIRC_CUDA_TRY(cudaMemsetAsync(adam_bad, 0, 4, s));
+    if (ntiles > 0) {
+      AsyncBuf fb(s), img(s), sb(s);
+      NIRC_CUDA_TRY(fb.alloc((size_t)(ntiles + 1) * 4));
+      int32_t* fix = static_cast<int32_t*>(fb.p);
+      NIRC_CUDA_TRY(cudaMemsetAsync(fix, 0, 4, s));
+      if (rstat == nullptr) {  // per-record static encoding (train_frame computes it once)
+        NIRC_CUDA_TRY(sb.alloc((size_t)train_static_bytes(rec.n)));
+        int st = launch_record_static(sp, rec, static_cast<float*>(sb.p), s);
+        if (st) return st;
+        rstat = static_cast<const float*>(sb.p);
+      }
+      int st = launch_train_tc(sp, theta, rstat, rec, idx, B, loss_kind, loss_eps, grad, partials,
+                               loss_part, flags, s, tile0, tile1, fix, nullptr);
+      if (st) return st;
+      // fp32 fix-up of the tiles beyond the fp16 range (CTAs past the list exit)
+      const FusedLayout L = fused_layout(sp, kTileRows);
+      const size_t sm = (size_t)L.total_floats * 4;
+      NIRC_CUDA_TRY(img.alloc((size_t)L.dz_off * 4));
+      k_pack_train_weights<<<dim3(16, L.nl), 256, 0, s>>>(sp, L, theta,
+                                                         static_cast<float*>(img.p), fix);
+      NIRC_LAUNCH_CHECK("k_pack_train_weights");
+      NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)t128::k_train_tile,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      t128::k_train_tile<<<ntiles < 32 ? ntiles : 32, kTT, sm, s>>>(
+          sp, L, theta, static_cast<const float*>(img.p), rec, idx, B, loss_kind, loss_eps, grad,
+          partials, loss_part, flags, tile0, fix);
+      NIRC_LAUNCH_CHECK("k_train_tile(fix)");
+    }
+    const int np = (int)(sp.theta_len - sp.grid_len);
+    k_reduce_grad<<<(np + 31) / 32, 256, 0, s>>>(sp, partials, ntiles, loss_part, B, grad,
+                                                 loss_out, flags, adam_bad, mode);
+    NIRC_LAUNCH_CHECK("k_reduce_grad");
+    return NIRC_OK;
+  }
   const int tr = tile_rows_for(ntiles);
   const int nsub = kTileRows / tr;
   const FusedLayout L = fused_layout(sp, tr);
@@ -227,7 +280,7 @@ int launch_fused_train(const nirc_spec_t& sp, const float* theta, const nirc_rec
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       kern<<<ntiles * nsub, kTT, sm, s>>>(sp, L, theta, static_cast<const float*>(img.p), rec,
                                           idx, B, loss_kind, loss_eps, grad, partials, loss_part,
-                                          flags, tile0);
+                                          flags, tile0, nullptr);
       return NIRC_OK;
     };
     int st = tr == 32 ? launch(t32::k_train_tile)

@@ -153,17 +153,20 @@ __global__ void __launch_bounds__(kTT, 1)
                  const float* __restrict__ wimg, nirc_records_t rec,
                  const int64_t* __restrict__ idx, int64_t B, int loss_kind, double loss_eps,
                  float* __restrict__ grad, float* __restrict__ partials,
-                 double* __restrict__ loss_part, int32_t* __restrict__ flags, int64_t tile0) {
+                 double* __restrict__ loss_part, int32_t* __restrict__ flags, int64_t tile0,
+                 const int32_t* __restrict__ tile_list) {
   extern __shared__ __align__(16) float fsm[];
   __shared__ uint32_t tmem_holder;
   __shared__ __align__(8) uint64_t wbar;
   if (flags[0] & 3) return;
+  // list mode (kTR == 128): the fp16-range fix-up of k_train_tc -- the CTAs
+  // loop over the API tiles tile_list[1 ..] and write those tiles' partial
+  // slots (a no-op launch when the list is empty)
+  if (tile_list != nullptr && (int)blockIdx.x >= tile_list[0]) return;
   const int tid = threadIdx.x;
   const int r = tid & (kTR - 1), h = tid / kTR;
   const int c0 = kCols * h;
   const int lane_base = ((tid >> 5) & 3) * 32;
-  const int64_t row = tile0 * kTileRows + (int64_t)blockIdx.x * kTR + r;
-  const bool live = row < B;
   // ---- weights: the step's image by TMA bulk copies, in flight during the
   // encode below (waited for before the forward) --------------------------
   const uint32_t wb = tc::smem_u32(&wbar);
@@ -185,6 +188,16 @@ __global__ void __launch_bounds__(kTT, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tbase = tmem_holder + ((uint32_t)lane_base << 16);
+  const int nitems = tile_list != nullptr ? tile_list[0] : (int)blockIdx.x + 1;
+  for (int item = blockIdx.x; item < nitems; item += (tile_list != nullptr ? gridDim.x : nitems)) {
+  int64_t slot = item, row0 = tile0 * kTileRows + (int64_t)item * kTR;
+  if (tile_list != nullptr) {
+    const int64_t t = tile_list[1 + item];
+    slot = t - tile0;
+    row0 = t * kTileRows;
+  }
+  const int64_t row = row0 + r;
+  const bool live = row < B;
   float* A = fsm + L.a_off;   // [feature][row]: the current layer's input
   float* DZ = fsm + L.dz_off;
   // ---- encode (bit-exact): levels kLvl*h ..; h == 0 also SH + aux ---------
@@ -293,10 +306,10 @@ __global__ void __launch_bounds__(kTT, 1)
   if (tid == 0) {
     double t = 0.0;
     for (int w = 0; w < kTT / 32; ++w) t += red[w];
-    loss_part[blockIdx.x] = t;
+    loss_part[slot] = t;
   }
   // ---- backward ----------------------------------------------------------
-  float* wpart = partials + (int64_t)blockIdx.x * (sp.theta_len - sp.grid_len);
+  float* wpart = partials + slot * (sp.theta_len - sp.grid_len);
   float dX[kDX];
   for (int l = NL - 1; l >= 0; --l) {
     {  // a_prev of layer l -> staging (relu(z_{l-1}) or the encoded input)
@@ -339,6 +352,8 @@ __global__ void __launch_bounds__(kTT, 1)
                     make_float2(__fmul_rn(w, d0), __fmul_rn(w, d1)));
       }
     }
+  }
+  __syncthreads();  // the next item reuses the staging arrays
   }
   tc::fence_before();
   __syncthreads();
