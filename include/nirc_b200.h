@@ -139,7 +139,11 @@ int nirc_encode(const nirc_spec_t* spec, const float* theta,
                 const double* rough, const double* dirs, int64_t n,
                 float* X, int64_t* entries, float* weights, void* stream);
 
-/* scatter_grid_grad (encoding.py:160-167): grad[slot*F+f] += w * dX[:, l*F+f]. */
+/* scatter_grid_grad (encoding.py:160-167): grad[slot*F+f] += w * dX[:, l*F+f]
+ * with np.add.at's semantics: each slot sums its contributions in entry order
+ * ((row, level, corner) row-major) from its current value -- a stable radix
+ * sort of (slot, entry) then one sequential sum per slot.  Deterministic, and
+ * bit-identical to the reference for identical weights and dX. */
 int nirc_scatter_grid_grad(const nirc_spec_t* spec, float* grad,
                            const int64_t* entries, const float* weights,
                            const float* dX, int64_t n, int64_t dx_stride,
@@ -226,11 +230,24 @@ typedef struct nirc_records {
   int64_t n;
 } nirc_records_t;
 
+/* Optimizer / reproducibility options of the training entries (NULL = the
+ * reference defaults: beta1 0.9, beta2 0.99, eps 1e-8 from AdamState,
+ * adam.py:8-17; atomic grid scatter).  deterministic != 0: the hash-grid
+ * gradient is summed by the ordered scatter (nirc_scatter_grid_grad's
+ * np.add.at order) instead of atomics, so repeated runs give bit-identical
+ * theta (the reference's test_training_is_bit_reproducible contract). */
+typedef struct nirc_train_opts {
+  double beta1, beta2, eps;
+  int32_t deterministic;
+  int32_t reserved;
+} nirc_train_opts_t;
+
 int nirc_train_step(const nirc_spec_t* spec, float* theta, float* m, float* v,
                     int64_t* t, int64_t* skipped, const nirc_records_t* rec,
                     uint64_t seed, int64_t frame, int32_t step,
                     int32_t batch_cap, int32_t loss_kind, double loss_eps,
-                    double lr, double* running_mean, double* loss_out,
+                    double lr, const nirc_train_opts_t* opts,
+                    double* running_mean, double* loss_out,
                     int32_t* status_flags, int64_t* batch_idx_out,
                     void* workspace, int64_t workspace_bytes, void* stream);
 int64_t nirc_train_workspace_bytes(const nirc_spec_t* spec, int64_t n_records,
@@ -246,7 +263,8 @@ int nirc_train_frame(const nirc_spec_t* spec, float* theta, float* m, float* v,
                      int64_t* t, int64_t* skipped, const nirc_records_t* rec,
                      uint64_t seed, int64_t frame, int32_t steps,
                      int32_t batch_cap, int32_t loss_kind, double loss_eps,
-                     double lr, double* running_mean, double* loss_out,
+                     double lr, const nirc_train_opts_t* opts,
+                     double* running_mean, double* loss_out,
                      int32_t* status_flags, void* workspace,
                      int64_t workspace_bytes, void* stream);
 int64_t nirc_train_frame_workspace_bytes(const nirc_spec_t* spec,
@@ -267,7 +285,8 @@ int64_t nirc_train_tiles(int64_t n_records, int32_t batch_cap);
 int nirc_train_grad(const nirc_spec_t* spec, const float* theta,
                     const nirc_records_t* rec, uint64_t seed, int64_t frame,
                     int32_t step, int32_t batch_cap, int32_t loss_kind,
-                    double loss_eps, int64_t tile_begin, int64_t tile_end,
+                    double loss_eps, const nirc_train_opts_t* opts,
+                    int64_t tile_begin, int64_t tile_end,
                     float* grad, double* aux, int32_t* status_flags,
                     int64_t* batch_idx_out, void* workspace,
                     int64_t workspace_bytes, void* stream);
@@ -276,7 +295,8 @@ int nirc_train_grad(const nirc_spec_t* spec, const float* theta,
  * status flags.  scratch: >= 4 bytes of device memory. */
 int nirc_train_apply(const nirc_spec_t* spec, float* theta, float* m, float* v,
                      int64_t* t, int64_t* skipped, const float* grad,
-                     const double* aux, int64_t batch, double lr, double* loss_out,
+                     const double* aux, int64_t batch, double lr,
+                     const nirc_train_opts_t* opts, double* loss_out,
                      int32_t* status_flags, int32_t* scratch, void* stream);
 
 /* ---- rendering (pkg/src/nirclab/kernels.py:451-759) --------------------- */

@@ -56,6 +56,17 @@ class NircRecords(C.Structure):
         ("n", C.c_int64)]
 
 
+class NircTrainOpts(C.Structure):
+    """nirc_train_opts_t: Adam hyper-parameters + the deterministic switch."""
+    _fields_ = [("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("deterministic", C.c_int32), ("reserved", C.c_int32)]
+
+
+def train_opts(adam, deterministic=False):
+    return NircTrainOpts(float(adam.beta1), float(adam.beta2), float(adam.eps),
+                         1 if deterministic else 0, 0)
+
+
 class NircRecordsOut(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in
                 ("pos", "ns", "alb", "rough", "dirs", "target", "pdf")] + [
@@ -118,15 +129,18 @@ SIGNATURES = {
     "nirc_loss": (I32, [I32, P, P, P, P, F64, I64, P, P, P, P, P]),
     "nirc_adam_step": (I32, [P, P, P, P, I64, P, P, F64, F64, F64, F64, P, P, P]),
     "nirc_train_step": (I32, [SPEC, P, P, P, P, P, C.POINTER(NircRecords), U64, I64, I32,
-                              I32, I32, F64, F64, P, P, P, P, P, I64, P]),
+                              I32, I32, F64, F64, C.POINTER(NircTrainOpts), P, P, P, P, P,
+                              I64, P]),
     "nirc_train_workspace_bytes": (I64, [SPEC, I64, I32]),
     "nirc_train_frame": (I32, [SPEC, P, P, P, P, P, C.POINTER(NircRecords), U64, I64, I32,
-                               I32, I32, F64, F64, P, P, P, P, I64, P]),
+                               I32, I32, F64, F64, C.POINTER(NircTrainOpts), P, P, P, P, I64,
+                               P]),
     "nirc_train_frame_workspace_bytes": (I64, [SPEC, I64, I32, I32]),
     "nirc_train_tiles": (I64, [I64, I32]),
     "nirc_train_grad": (I32, [SPEC, P, C.POINTER(NircRecords), U64, I64, I32, I32, I32, F64,
-                              I64, I64, P, P, P, P, P, I64, P]),
-    "nirc_train_apply": (I32, [SPEC, P, P, P, P, P, P, P, I64, F64, P, P, P, P]),
+                              C.POINTER(NircTrainOpts), I64, I64, P, P, P, P, P, I64, P]),
+    "nirc_train_apply": (I32, [SPEC, P, P, P, P, P, P, P, I64, F64, C.POINTER(NircTrainOpts),
+                               P, P, P, P]),
     "nirc_render": (I32, [C.POINTER(NircScene), P, C.POINTER(NircRenderCfg), SPEC, P, P, P,
                           P, P, P, I64, P]),
     "nirc_render_workspace_bytes": (I64, [C.POINTER(NircRenderCfg)]),

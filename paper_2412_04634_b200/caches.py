@@ -11,6 +11,7 @@ status flags.
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 import os
 import tempfile
@@ -98,7 +99,7 @@ class TrainResult:
 
 
 def _launch_steps(spec, theta, adam, records, seed, frame, steps, batch, loss_kind, loss_eps,
-                  running_mean, ws, return_idx=False):
+                  running_mean, ws, return_idx=False, deterministic=False):
     n = len(records)
     if n == 0:
         raise ValueError("cannot train on an empty record set")
@@ -111,6 +112,7 @@ def _launch_steps(spec, theta, adam, records, seed, frame, steps, batch, loss_ki
     B = min(cap, n)
     losses = _dev.zeros((steps,), torch.float64)
     flags = _dev.zeros((1,), torch.int32)
+    opts = C.byref(_lib.train_opts(adam, deterministic))
     idx = None
     if not return_idx:
         # one C call: batches of all steps selected at once, then the steps
@@ -119,7 +121,7 @@ def _launch_steps(spec, theta, adam, records, seed, frame, steps, batch, loss_ki
         _lib.check(lib.nirc_train_frame(
             cs, _dev.ptr(theta), _dev.ptr(adam.m), _dev.ptr(adam.v), _dev.ptr(adam._t),
             _dev.ptr(adam._skipped), rec, int(seed), int(frame), int(steps), cap,
-            LOSS_KINDS.index(loss_kind), float(loss_eps), float(adam.lr),
+            LOSS_KINDS.index(loss_kind), float(loss_eps), float(adam.lr), opts,
             _dev.ptr(running_mean), _dev.ptr(losses), _dev.ptr(flags), _dev.ptr(buf),
             int(buf.numel()), _dev.stream()), "nirc_train_frame")
     else:
@@ -130,7 +132,7 @@ def _launch_steps(spec, theta, adam, records, seed, frame, steps, batch, loss_ki
             _lib.check(lib.nirc_train_step(
                 cs, _dev.ptr(theta), _dev.ptr(adam.m), _dev.ptr(adam.v), _dev.ptr(adam._t),
                 _dev.ptr(adam._skipped), rec, int(seed), int(frame), s, cap,
-                LOSS_KINDS.index(loss_kind), float(loss_eps), float(adam.lr),
+                LOSS_KINDS.index(loss_kind), float(loss_eps), float(adam.lr), opts,
                 _dev.ptr(running_mean), _dev.ptr(losses[s:s + 1]), _dev.ptr(flags),
                 _dev.ptr(idx[s]), _dev.ptr(buf), int(buf.numel()), _dev.stream()),
                 "nirc_train_step")
@@ -174,14 +176,16 @@ def sample_incident_targets(scene, origin, direction, seed, count, prev_pdf=-1.0
 
 
 def train_frame_device(spec, theta, records, seed, frame, steps=4, batch=None, adam=None,
-                       loss_kind="relative_l2", loss_eps=0.01, return_idx=False):
+                       loss_kind="relative_l2", loss_eps=0.01, return_idx=False,
+                       deterministic=False):
     """Device training on a bare (spec, theta) pair -- the batch form of
-    train_frame used by tests and the benchmark."""
+    train_frame used by tests and the benchmark.  ``deterministic`` sums the
+    hash-grid gradient in np.add.at's order (bit-reproducible runs)."""
     if adam is None:
         adam = AdamState(theta)
     rm = _dev.zeros((3,), torch.float64)
     return _launch_steps(spec, theta, adam, records, seed, frame, steps, batch, loss_kind,
-                         loss_eps, rm, _Workspace(), return_idx)
+                         loss_eps, rm, _Workspace(), return_idx, deterministic)
 
 
 class Cache:
@@ -203,6 +207,10 @@ class Cache:
         self.snapshot_dir = None
         self.has_env = scene.pack.env_kind != 0
         self._ws = _Workspace()
+        # bit-reproducible training (ordered grid-gradient scatter) -- the
+        # reference's contract; NIRC_DETERMINISTIC=0 trades it
+        # for the atomic scatter
+        self.deterministic = os.environ.get("NIRC_DETERMINISTIC", "1") != "0"
 
     @property
     def running_mean(self):
@@ -346,7 +354,7 @@ def train_frame(cache, records, steps=4, batch=None):
         raise ValueError("cannot train on an empty record set")
     res = _launch_steps(cache.spec, cache.theta, cache.adam, records, cache.seed, cache.frame,
                         steps, batch, cache.loss_kind, cache.loss_eps, cache._running_mean,
-                        cache._ws)
+                        cache._ws, deterministic=getattr(cache, "deterministic", False))
     if res.flags & 1:
         raise InvalidSampleError("sample pdf must be positive")
     if res.flags & 2:

@@ -312,6 +312,12 @@ int check_cuda(cudaError_t e, const char* what);
 
 // Stream-ordered temporary: cudaFreeAsync on every exit path of the entry
 // point that allocated it (early error returns included).
+// Row stride (floats) of the training kernels' per-tile MLP-gradient
+// partials: the MLP block of theta padded to 16 bytes (vector reduction).
+NIRC_HD int64_t part_stride(const nirc_spec_t& sp) {
+  return (sp.theta_len - sp.grid_len + 3) & ~(int64_t)3;
+}
+
 struct AsyncBuf {
   void* p = nullptr;
   cudaStream_t s = nullptr;

@@ -467,12 +467,15 @@ __global__ void k_adam_apply4(float* __restrict__ theta, float* __restrict__ m,
                               float* __restrict__ v, const float* __restrict__ g, int64_t n,
                               int64_t* __restrict__ t, int64_t* __restrict__ skipped, float lr,
                               double b1, double b2, float eps, const int32_t* __restrict__ bad,
-                              const int32_t* __restrict__ gate) {
+                              const int32_t* __restrict__ gate, const float* __restrict__ bc_in) {
   if (gate && gate[0]) return;
   if (bad[0]) {
     if (blockIdx.x == 0 && threadIdx.x == 0) skipped[0] += 1;
     return;
   }
+  // bias corrections precomputed (k_reduce_grad): no block reads t, so
+  // block 0 advances it here (no k_adam_tick launch)
+  if (bc_in != nullptr && blockIdx.x == 0 && threadIdx.x == 0) t[0] += 1;
   const float c1 = (float)(1.0 - b1);
   const float c2 = (float)(1.0 - b2);
   const int64_t n4 = n >> 2;
@@ -490,13 +493,18 @@ __global__ void k_adam_apply4(float* __restrict__ theta, float* __restrict__ m,
     gi = reinterpret_cast<const float4*>(g)[tid];
   }
   float bc1 = 0.0f, bc2 = 0.0f;
-  if ((threadIdx.x & 31) == 0) {
-    const int64_t tn = t[0] + 1;
-    bc1 = (float)(1.0 - pow(b1, (double)tn));
-    bc2 = (float)(1.0 - pow(b2, (double)tn));
+  if (bc_in != nullptr) {
+    bc1 = bc_in[0];
+    bc2 = bc_in[1];
+  } else {
+    if ((threadIdx.x & 31) == 0) {
+      const int64_t tn = t[0] + 1;
+      bc1 = (float)(1.0 - pow(b1, (double)tn));
+      bc2 = (float)(1.0 - pow(b2, (double)tn));
+    }
+    bc1 = __shfl_sync(0xffffffffu, bc1, 0);
+    bc2 = __shfl_sync(0xffffffffu, bc2, 0);
   }
-  bc1 = __shfl_sync(0xffffffffu, bc1, 0);
-  bc2 = __shfl_sync(0xffffffffu, bc2, 0);
   for (int64_t i = tid; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     if (i != tid) {
       th = reinterpret_cast<float4*>(theta)[i];
@@ -585,13 +593,19 @@ __global__ void k_sel_scan(int64_t n, int B, SelWs w, const int32_t* __restrict_
   uint32_t* boff = w.boff + (int64_t)sy * (kSelBins + 1);
   uint32_t* fill = w.fill + (int64_t)sy * kSelBins;
   int32_t* bstar = w.bstar + 2 * sy;
-  const int t = threadIdx.x;  // 1024 threads x 16 bins
+  const int t = threadIdx.x;  // 1024 threads x 16 consecutive bins (4 x 16-byte loads)
   constexpr int kPer = kSelBins / 1024;
   uint32_t v[kPer], s = 0;
-  for (int q = 0; q < kPer; ++q) {
-    v[q] = hist[t * kPer + q];
-    s += v[q];
+#pragma unroll
+  for (int q = 0; q < kPer; q += 4) {
+    const uint4 x = reinterpret_cast<const uint4*>(hist + t * kPer)[q / 4];
+    v[q] = x.x;
+    v[q + 1] = x.y;
+    v[q + 2] = x.z;
+    v[q + 3] = x.w;
   }
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) s += v[q];
   // block-wide inclusive scan of the per-thread sums (warp shuffles)
   const int lane = t & 31, wid = t >> 5;
   uint32_t x = s;
@@ -613,17 +627,23 @@ __global__ void k_sel_scan(int64_t n, int B, SelWs w, const int32_t* __restrict_
   }
   __syncthreads();
   uint32_t run = x - s + (wid > 0 ? part[wid - 1] : 0u);
+  uint32_t o[kPer];
+#pragma unroll
   for (int q = 0; q < kPer; ++q) {
-    const int b = t * kPer + q;
-    boff[b] = run;
-    fill[b] = 0;
+    o[q] = run;
     // the bucket containing rank B-1 (or the last bucket when n <= B)
     if (run < (uint32_t)B && run + v[q] >= (uint32_t)B) {
-      bstar[0] = b;
+      bstar[0] = t * kPer + q;
       bstar[1] = (int32_t)(run + v[q]);
     }
     run += v[q];
   }
+  // boff is kSelBins + 1 long: 4-byte stores; fill via 16-byte stores
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) boff[t * kPer + q] = o[q];
+#pragma unroll
+  for (int q = 0; q < kPer; q += 4)
+    reinterpret_cast<uint4*>(fill + t * kPer)[q / 4] = make_uint4(0u, 0u, 0u, 0u);
   if (t == 1023) boff[kSelBins] = run;
   if (n <= B && t == 0) {
     bstar[0] = kSelBins - 1;
@@ -661,6 +681,33 @@ __global__ void k_sel_sort(int64_t n, SelWs w, const int32_t* __restrict__ flags
   uint64_t* skey = w.skey + (int64_t)s * n;
   int64_t* sidx = w.sidx + (int64_t)s * n;
   const uint32_t lo = boff[b], hi = boff[b + 1];
+  constexpr uint32_t kLocal = 32;
+  if (hi - lo <= kLocal) {  // small bucket (the common case): sort in registers / L1
+    uint64_t k[kLocal];
+    int64_t x[kLocal];
+    const uint32_t nb = hi - lo;
+    for (uint32_t i = 0; i < nb; ++i) {
+      k[i] = skey[lo + i];
+      x[i] = sidx[lo + i];
+    }
+    for (uint32_t i = 1; i < nb; ++i) {  // insertion sort by (key, index)
+      const uint64_t kk = k[i];
+      const int64_t xx = x[i];
+      uint32_t j = i;
+      while (j > 0 && (k[j - 1] > kk || (k[j - 1] == kk && x[j - 1] > xx))) {
+        k[j] = k[j - 1];
+        x[j] = x[j - 1];
+        --j;
+      }
+      k[j] = kk;
+      x[j] = xx;
+    }
+    for (uint32_t i = 0; i < nb; ++i) {
+      skey[lo + i] = k[i];
+      sidx[lo + i] = x[i];
+    }
+    return;
+  }
   for (uint32_t i = lo + 1; i < hi; ++i) {  // insertion sort by (key, index)
     const uint64_t k = skey[i];
     const int64_t x = sidx[i];
@@ -744,7 +791,12 @@ int launch_fused_train(const nirc_spec_t& sp, const float* theta, const nirc_rec
                        const int64_t* idx, int64_t B, int loss_kind, double loss_eps,
                        float* grad, float* partials, double* loss_part, double* loss_out,
                        int32_t* flags, int32_t* adam_bad, cudaStream_t s, int64_t tile0,
-                       int64_t tile1, int mode, const float* rstat);
+                       int64_t tile1, int mode, const float* rstat, bool deterministic,
+                       const int64_t* t, float* bc, double b1, double b2);
+template <typename T>
+int ordered_scatter(const nirc_spec_t& sp, T* grad, const int64_t* entries, const float* weights,
+                    const T* dX, int64_t n, int64_t stride, const double* pos, const int64_t* idx,
+                    int64_t r0, cudaStream_t s);
 int64_t train_static_bytes(int64_t n);
 int launch_record_static(const nirc_spec_t& sp, const nirc_records_t& rec, float* out,
                          cudaStream_t s);
@@ -813,12 +865,9 @@ extern "C" int nirc_scatter_grid_grad(const nirc_spec_t* spec, float* grad,
                                       void* stream) {
   int st = check_spec(spec);
   if (st) return st;
-  const int64_t total = n * spec->levels * 8;
-  if (total <= 0) return NIRC_OK;
-  k_scatter<<<blocks_for(total, 256), 256, 0, S(stream)>>>(*spec, grad, entries, weights, dX, n,
-                                                          dx_stride);
-  NIRC_LAUNCH_CHECK("k_scatter");
-  return NIRC_OK;
+  if (n <= 0) return NIRC_OK;
+  return ordered_scatter<float>(*spec, grad, entries, weights, dX, n, dx_stride, nullptr, nullptr,
+                                0, S(stream));
 }
 
 extern "C" int nirc_mlp_forward(const nirc_spec_t* spec, const float* theta, const float* X,
@@ -867,11 +916,16 @@ extern "C" int nirc_loss(int32_t kind, const float* Y, const double* target, con
   return NIRC_OK;
 }
 
+static nirc_train_opts_t opts_or_default(const nirc_train_opts_t* o) {
+  nirc_train_opts_t d{0.9, 0.99, 1e-8, 0, 0};  // AdamState defaults (adam.py:8-17)
+  return o != nullptr ? *o : d;
+}
+
 // Dense Adam apply + tick; the non-finite check already ran (adam_bad).
 static int launch_adam(float* theta, float* m, float* v, const float* grad, int64_t n,
                        int64_t* t, int64_t* skipped, float lr, const int32_t* bad,
                        const int32_t* gate, cudaStream_t s, double b1 = 0.9, double b2 = 0.99,
-                       double eps = 1e-8) {
+                       double eps = 1e-8, const float* bc = nullptr) {
   const bool aligned = ((reinterpret_cast<uintptr_t>(theta) | reinterpret_cast<uintptr_t>(m) |
                          reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(grad)) &
                         15u) == 0;
@@ -879,7 +933,11 @@ static int launch_adam(float* theta, float* m, float* v, const float* grad, int6
     const int64_t n4 = (n >> 2) > 0 ? (n >> 2) : 1;
     const int nb = (int)((n4 + 255) / 256 < 148 * 8 ? (n4 + 255) / 256 : 148 * 8);
     k_adam_apply4<<<nb, 256, 0, s>>>(theta, m, v, grad, n, t, skipped, lr, b1, b2, (float)eps,
-                                     bad, gate);
+                                     bad, gate, bc);
+    if (bc != nullptr) {  // t advanced by k_adam_apply4
+      NIRC_LAUNCH_CHECK("k_adam_apply4");
+      return NIRC_OK;
+    }
   } else {
     k_adam_apply<<<148 * 4, 256, 0, s>>>(theta, m, v, grad, n, t, skipped, lr, b1, b2,
                                          (float)eps, bad, gate);
@@ -948,7 +1006,7 @@ TrainWs carve_train(const nirc_spec_t& sp, int64_t n, int64_t B, int steps, void
   // with 4k, 2k <= the SM count (train_fused.cu tile_rows_for)
   const int64_t ntiles = (B + kFusedTileRows - 1) / kFusedTileRows;
   const int64_t slots = ntiles > 256 ? ntiles : 256;
-  w.fpart = (float*)take(slots * (sp.theta_len - sp.grid_len) * 4);
+  w.fpart = (float*)take(slots * part_stride(sp) * 4);
   w.floss = (double*)take(slots * 8);
   w.rstat = (float*)take(train_static_bytes(n));
   w.bytes = off;
@@ -1009,19 +1067,21 @@ static bool use_fused(const nirc_spec_t& sp, int loss_kind) {
 static int step_body(const nirc_spec_t* spec, float* theta, float* m, float* v, int64_t* t,
                      int64_t* skipped, const nirc_records_t* rec, const int64_t* idx,
                      int64_t B, int32_t loss_kind, double loss_eps, double lr,
-                     double* running_mean, double* loss_out, int32_t* status_flags,
-                     const TrainWs& w, void* stream, const float* rstat) {
+                     const nirc_train_opts_t& o, double* running_mean, double* loss_out,
+                     int32_t* status_flags, const TrainWs& w, void* stream, const float* rstat) {
   cudaStream_t s = S(stream);
   int st;
   if (use_fused(*spec, loss_kind)) {
     // one fused kernel per step: encode, forward, loss, backward, scatter
     const int64_t ntiles = (B + kFusedTileRows - 1) / kFusedTileRows;
+    float* bc = reinterpret_cast<float*>(w.adam_bad + 2);  // [bad | pad | bc1 | bc2]
     if ((st = launch_fused_train(*spec, theta, *rec, idx, B, loss_kind, loss_eps, w.grad,
                                  w.fpart, w.floss, loss_out, status_flags, w.adam_bad, s, 0,
-                                 ntiles, 0, rstat)))
+                                 ntiles, 0, rstat, o.deterministic != 0, t, bc, o.beta1,
+                                 o.beta2)))
       return st;
     return launch_adam(theta, m, v, w.grad, spec->theta_len, t, skipped, (float)lr, w.adam_bad,
-                       status_flags, s);
+                       status_flags, s, o.beta1, o.beta2, o.eps, bc);
   }
   const size_t sm = simt_smem_bytes(*spec);
   if ((st = set_smem((const void*)k_train_forward, sm))) return st;
@@ -1047,18 +1107,25 @@ static int step_body(const nirc_spec_t* spec, float* theta, float* m, float* v, 
   dim3 g(blocks_for(B, kDwRows), spec->n_layers, dw_zsplit(*spec));
   k_weight_grad<<<g, kDwThreads, 0, s>>>(*spec, w.X, w.zs, w.dzs, B, w.grad, status_flags);
   NIRC_LAUNCH_CHECK("k_weight_grad");
-  k_train_scatter<<<blocks_for(B * spec->levels, 256), 256, 0, s>>>(*spec, *rec, idx, B, w.dX,
-                                                                   w.grad, status_flags);
-  NIRC_LAUNCH_CHECK("k_train_scatter");
-  return nirc_adam_step(theta, m, v, w.grad, spec->theta_len, t, skipped, lr, 0.9, 0.99, 1e-8,
-                        status_flags, w.adam_bad, stream);
+  if (o.deterministic) {
+    if ((st = ordered_scatter<float>(*spec, w.grad, nullptr, nullptr, w.dX, B, spec->in_dim,
+                                     rec->pos, idx, 0, s)))
+      return st;
+  } else {
+    k_train_scatter<<<blocks_for(B * spec->levels, 256), 256, 0, s>>>(*spec, *rec, idx, B, w.dX,
+                                                                     w.grad, status_flags);
+    NIRC_LAUNCH_CHECK("k_train_scatter");
+  }
+  return nirc_adam_step(theta, m, v, w.grad, spec->theta_len, t, skipped, lr, o.beta1, o.beta2,
+                        o.eps, status_flags, w.adam_bad, stream);
 }
 
 extern "C" int nirc_train_step(const nirc_spec_t* spec, float* theta, float* m, float* v,
                                int64_t* t, int64_t* skipped, const nirc_records_t* rec,
                                uint64_t seed, int64_t frame, int32_t step, int32_t batch_cap,
                                int32_t loss_kind, double loss_eps, double lr,
-                               double* running_mean, double* loss_out, int32_t* status_flags,
+                               const nirc_train_opts_t* opts, double* running_mean,
+                               double* loss_out, int32_t* status_flags,
                                int64_t* batch_idx_out, void* workspace,
                                int64_t workspace_bytes, void* stream) {
   int st = train_args_ok(spec, rec, batch_cap);
@@ -1076,15 +1143,17 @@ extern "C" int nirc_train_step(const nirc_spec_t* spec, float* theta, float* m, 
   if (batch_idx_out)
     NIRC_CUDA_TRY(cudaMemcpyAsync(batch_idx_out, w.sel.sidx, B * 8, cudaMemcpyDeviceToDevice, s));
   return step_body(spec, theta, m, v, t, skipped, rec, w.sel.sidx, B, loss_kind, loss_eps, lr,
-                   running_mean, loss_out, status_flags, w, stream, nullptr);
+                   opts_or_default(opts), running_mean, loss_out, status_flags, w, stream,
+                   nullptr);
 }
 
 extern "C" int nirc_train_frame(const nirc_spec_t* spec, float* theta, float* m, float* v,
                                 int64_t* t, int64_t* skipped, const nirc_records_t* rec,
                                 uint64_t seed, int64_t frame, int32_t steps, int32_t batch_cap,
                                 int32_t loss_kind, double loss_eps, double lr,
-                                double* running_mean, double* loss_out, int32_t* status_flags,
-                                void* workspace, int64_t workspace_bytes, void* stream) {
+                                const nirc_train_opts_t* opts, double* running_mean,
+                                double* loss_out, int32_t* status_flags, void* workspace,
+                                int64_t workspace_bytes, void* stream) {
   int st = train_args_ok(spec, rec, batch_cap);
   if (st) return st;
   if (steps < 1) { set_last_error("steps must be positive"); return NIRC_E_CONFIG; }
@@ -1104,8 +1173,8 @@ extern "C" int nirc_train_frame(const nirc_spec_t* spec, float* theta, float* m,
   }
   for (int k = 0; k < steps; ++k)
     if ((st = step_body(spec, theta, m, v, t, skipped, rec, w.sel.sidx + (int64_t)k * n, B,
-                        loss_kind, loss_eps, lr, running_mean, loss_out + k, status_flags, w,
-                        stream, rstat)))
+                        loss_kind, loss_eps, lr, opts_or_default(opts), running_mean,
+                        loss_out + k, status_flags, w, stream, rstat)))
       return st;
   return NIRC_OK;
 }
@@ -1120,7 +1189,8 @@ extern "C" int64_t nirc_train_tiles(int64_t n_records, int32_t batch_cap) {
 extern "C" int nirc_train_grad(const nirc_spec_t* spec, const float* theta,
                                const nirc_records_t* rec, uint64_t seed, int64_t frame,
                                int32_t step, int32_t batch_cap, int32_t loss_kind,
-                               double loss_eps, int64_t tile_begin, int64_t tile_end,
+                               double loss_eps, const nirc_train_opts_t* opts,
+                               int64_t tile_begin, int64_t tile_end,
                                float* grad, double* aux, int32_t* status_flags,
                                int64_t* batch_idx_out, void* workspace, int64_t workspace_bytes,
                                void* stream) {
@@ -1150,7 +1220,8 @@ extern "C" int nirc_train_grad(const nirc_spec_t* spec, const float* theta,
     NIRC_CUDA_TRY(cudaMemcpyAsync(batch_idx_out, w.sel.sidx, B * 8, cudaMemcpyDeviceToDevice, s));
   return launch_fused_train(*spec, theta, *rec, w.sel.sidx, B, loss_kind, loss_eps, grad, w.fpart,
                             w.floss, aux, status_flags, nullptr, s, tile_begin, tile_end, 1,
-                            nullptr);
+                            nullptr, opts_or_default(opts).deterministic != 0, nullptr, nullptr,
+                            0.9, 0.99);
 }
 
 namespace nirc {
@@ -1168,13 +1239,15 @@ __global__ void k_train_fold(const double* __restrict__ aux, int64_t B,
 
 extern "C" int nirc_train_apply(const nirc_spec_t* spec, float* theta, float* m, float* v,
                                 int64_t* t, int64_t* skipped, const float* grad,
-                                const double* aux, int64_t batch, double lr, double* loss_out,
+                                const double* aux, int64_t batch, double lr,
+                                const nirc_train_opts_t* opts, double* loss_out,
                                 int32_t* status_flags, int32_t* scratch, void* stream) {
   int st = check_spec(spec);
   if (st) return st;
   if (batch < 1) { set_last_error("batch must be positive"); return NIRC_E_CONFIG; }
   k_train_fold<<<1, 1, 0, S(stream)>>>(aux, batch, loss_out, status_flags);
   NIRC_LAUNCH_CHECK("k_train_fold");
-  return nirc_adam_step(theta, m, v, grad, spec->theta_len, t, skipped, lr, 0.9, 0.99, 1e-8,
-                        status_flags, scratch, stream);
+  const nirc_train_opts_t o = opts_or_default(opts);
+  return nirc_adam_step(theta, m, v, grad, spec->theta_len, t, skipped, lr, o.beta1, o.beta2,
+                        o.eps, status_flags, scratch, stream);
 }

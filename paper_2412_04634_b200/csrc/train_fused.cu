@@ -147,70 +147,128 @@ inline int tile_rows_for(int64_t ntiles) {
 
 // grad[mlp] = sum over tiles (tile order) of the partials.
 // mode 0 (whole batch on this GPU): loss = mean; flags: 2 = non-finite loss
-//   (stop), adam_bad = any non-finite gradient.
+//   (stop), adam_bad = any non-finite gradient; bc (when given) = the Adam
+//   bias corrections of the coming step, f32(1 - b^(t+1)) computed in f64
+//   (the reference's python-float arithmetic, adam.py:30-31).
 // mode 1 (one shard of a multi-GPU batch): aux[0] = this shard's raw loss
 //   sum, aux[1] = 1 if a row of this shard had pdf <= 0; the finiteness
 //   checks run after the cross-GPU sum (nirc_train_apply).
-__global__ void k_reduce_grad(nirc_spec_t sp, const float* __restrict__ partials, int ntiles,
-                              const double* __restrict__ loss_part, int64_t B,
-                              float* __restrict__ grad, double* __restrict__ loss_out,
-                              int32_t* __restrict__ flags, int32_t* __restrict__ adam_bad,
-                              int mode) {
+// Blocks [0, nb_mlp): 32 float4 columns of the MLP block each, warp w sums
+// the tiles of chunk w (8 chunks) -- the chunk sums are added in warp order
+// (deterministic); the remaining blocks check the grid gradient.
+constexpr int kRedMlpCols = 32;
+__global__ void __launch_bounds__(256) k_reduce_grad(
+    nirc_spec_t sp, const float* __restrict__ partials, int ntiles,
+    const double* __restrict__ loss_part, int64_t B, float* __restrict__ grad,
+    double* __restrict__ loss_out, int32_t* __restrict__ flags, int32_t* __restrict__ adam_bad,
+    int mode, int nb_mlp, const int64_t* __restrict__ t, float* __restrict__ bc, double b1,
+    double b2) {
   if (mode == 0 && (flags[0] & 3)) return;
-  // block = 8 warps x 32 consecutive parameters; warp w sums a contiguous
-  // chunk of tiles, the 8 chunk sums are added in warp order (deterministic)
-  __shared__ float part[8][33];
   const int np = (int)(sp.theta_len - sp.grid_len);
+  const int64_t ps = part_stride(sp);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int per = (ntiles + 7) / 8;
-  const int t0 = wid * per, t1 = min(ntiles, t0 + per);
   int bad = 0;
-  for (int pb = blockIdx.x * 32; pb < np; pb += gridDim.x * 32) {
-    const int p = pb + lane;
-    float s = 0.0f;
-    if (p < np) {
-#pragma unroll 8
-      for (int t = t0; t < t1; ++t) s += partials[(int64_t)t * np + p];
+  if ((int)blockIdx.x < nb_mlp) {
+    __shared__ float4 part[8][kRedMlpCols];
+    const int c4 = blockIdx.x * kRedMlpCols + lane;  // float4 column
+    const int per = (ntiles + 7) / 8;
+    const int t0 = wid * per, t1 = min(ntiles, t0 + per);
+    float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (4 * c4 < ps) {
+      const float4* src = reinterpret_cast<const float4*>(partials) + c4;
+      int tt = t0;
+      for (; tt + 8 <= t1; tt += 8) {  // 8 independent 16-byte loads in flight
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = src[(int64_t)(tt + u) * (ps / 4)];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          s4.x += v[u].x;
+          s4.y += v[u].y;
+          s4.z += v[u].z;
+          s4.w += v[u].w;
+        }
+      }
+      for (; tt < t1; ++tt) {
+        const float4 v = src[(int64_t)tt * (ps / 4)];
+        s4.x += v.x;
+        s4.y += v.y;
+        s4.z += v.z;
+        s4.w += v.w;
+      }
     }
-    part[wid][lane] = s;
+    part[wid][lane] = s4;
     __syncthreads();
-    if (wid == 0 && p < np) {
-      float tot = part[0][lane];
-      for (int w = 1; w < 8; ++w) tot += part[w][lane];
-      grad[sp.grid_len + p] = tot;
-      bad |= !isfinite(tot);
+    if (wid == 0 && 4 * c4 < np) {
+      float4 tot = part[0][lane];
+      for (int w = 1; w < 8; ++w) {
+        tot.x += part[w][lane].x;
+        tot.y += part[w][lane].y;
+        tot.z += part[w][lane].z;
+        tot.w += part[w][lane].w;
+      }
+      const float vv[4] = {tot.x, tot.y, tot.z, tot.w};
+      for (int k = 0; k < 4 && 4 * c4 + k < np; ++k) {
+        grad[sp.grid_len + 4 * c4 + k] = vv[k];
+        bad |= !isfinite(vv[k]);
+      }
     }
-    __syncthreads();
+  } else if (mode == 0) {  // the grid gradient's finiteness (float4 sweeps)
+    const int64_t n4 = sp.grid_len / 4;
+    const float4* g4 = reinterpret_cast<const float4*>(grad);
+    for (int64_t i = (int64_t)(blockIdx.x - nb_mlp) * blockDim.x + threadIdx.x; i < n4;
+         i += (int64_t)(gridDim.x - nb_mlp) * blockDim.x) {
+      const float4 v = g4[i];
+      bad |= !isfinite(v.x) | !isfinite(v.y) | !isfinite(v.z) | !isfinite(v.w);
+    }
   }
+  // the tiles' loss partials: 32 lanes sum contiguous chunks, then a fixed
+  // shuffle tree (deterministic, no serial 128-long load chain)
+  auto loss_sum = [&]() -> double {
+    const int per = (ntiles + 31) / 32;
+    double s = 0.0;
+    for (int k = lane * per; k < min(ntiles, lane * per + per); ++k) s += loss_part[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    return s;
+  };
   if (mode == 1) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      double s = 0.0;
-      for (int t = 0; t < ntiles; ++t) s += loss_part[t];
-      loss_out[0] = s;
-      loss_out[1] = (flags[0] & 1) ? 1.0 : 0.0;
+    if (blockIdx.x == 0 && wid == 0) {
+      const double s = loss_sum();
+      if (lane == 0) {
+        loss_out[0] = s;
+        loss_out[1] = (flags[0] & 1) ? 1.0 : 0.0;
+      }
     }
     return;
   }
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sp.grid_len;
-       i += (int64_t)gridDim.x * blockDim.x)
-    bad |= !isfinite(grad[i]);
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(adam_bad, 1);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double s = 0.0;
-    for (int t = 0; t < ntiles; ++t) s += loss_part[t];
+  if (blockIdx.x == gridDim.x - 1 && wid == 0) {
+    const double s = loss_sum();
+    if (lane != 0) return;
     const double v = s / (double)(B * 3);
     loss_out[0] = v;
     if (!isfinite(v)) atomicOr(flags, 2);
+    if (bc != nullptr) {
+      const double tn = (double)(t[0] + 1);
+      bc[0] = (float)(1.0 - pow(b1, tn));
+      bc[1] = (float)(1.0 - pow(b2, tn));
+    }
   }
 }
 
+inline int reduce_blocks_mlp(const nirc_spec_t& sp) {
+  const int64_t c4 = part_stride(sp) / 4;
+  return (int)((c4 + kRedMlpCols - 1) / kRedMlpCols);
+}
 
 bool train_tc_supported(const nirc_spec_t& sp);
 int launch_train_tc(const nirc_spec_t& sp, const float* theta, const float* rstat,
                     const nirc_records_t& rec, const int64_t* idx, int64_t B, int loss_kind,
                     double loss_eps, float* grad, float* partials, double* loss_part,
                     int32_t* flags, cudaStream_t s, int64_t tile0, int64_t tile1, int32_t* fix,
-                    float* dx_out);
+                    float* dx_out, uint32_t* lvlmax, void* zero_b, int64_t zero_b_bytes,
+                    int32_t* adam_bad);
 int64_t train_static_bytes(int64_t n);
 int launch_record_static(const nirc_spec_t& sp, const nirc_records_t& rec, float* out,
                          cudaStream_t s);
@@ -219,21 +277,50 @@ int launch_record_static(const nirc_spec_t& sp, const nirc_records_t& rec, float
 // per GPU in the multi-GPU frame, mode 1).  The default layout trains on
 // tcgen05 (train_tc.cu) with the fp32 SIMT kernel as the fp16-range fix-up;
 // other layouts (or NIRC_TRAIN_SIMT=1) run the SIMT kernel throughout.
+int fixed_scatter_rows(const nirc_spec_t& sp, float* grad, const float* dX, int64_t nrows,
+                       const uint32_t* lvlmax, const double* pos, const int64_t* idx, int64_t r0,
+                       int64_t batch_rows, unsigned long long* acc, cudaStream_t s);
+
 int launch_fused_train(const nirc_spec_t& sp, const float* theta, const nirc_records_t& rec,
                        const int64_t* idx, int64_t B, int loss_kind, double loss_eps,
                        float* grad, float* partials, double* loss_part, double* loss_out,
                        int32_t* flags, int32_t* adam_bad, cudaStream_t s, int64_t tile0,
-                       int64_t tile1, int mode, const float* rstat) {
+                       int64_t tile1, int mode, const float* rstat, bool deterministic,
+                       const int64_t* t, float* bc, double b1, double b2) {
   const int ntiles = (int)(tile1 > tile0 ? tile1 - tile0 : 0);
   const bool force_simt = getenv("NIRC_TRAIN_SIMT") != nullptr;  // read per call (tests switch it)
-  if (!force_simt && train_tc_supported(sp)) {
-    NIRC_CUDA_TRY(cudaMemsetAsync(grad, 0, sp.grid_len * 4, s));
-    if (adam_bad) NIRC_CUDA_TRY(cudaMemsetAsync(adam_bad, 0, 4, s));
+  // deterministic mode: the tile kernels write the rows' grid gradients (and
+  // each level's max |dX|); the 64-bit fixed-point scatter sums them
+  // order-independently (scatter.cu)
+  AsyncBuf dxb(s);
+  float* dx_out = nullptr;
+  uint32_t* lvlmax = nullptr;
+  unsigned long long* acc = nullptr;
+  const int64_t r0 = tile0 * kTileRows, r1 = tile1 * kTileRows < B ? tile1 * kTileRows : B;
+  if (deterministic && ntiles > 0) {
+    const size_t dxbytes = ((size_t)B * 24 * 4 + 255) & ~(size_t)255;
+    NIRC_CUDA_TRY(dxb.alloc(dxbytes + 256 + (size_t)sp.grid_len * 8));
+    dx_out = static_cast<float*>(dxb.p);
+    lvlmax = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(dxb.p) + dxbytes);
+    acc = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(dxb.p) + dxbytes + 256);
+  }
+  const bool tc_path = !force_simt && train_tc_supported(sp);
+  if (lvlmax != nullptr && !(tc_path && ntiles > 0))  // the tc path zeroes them in its prepare
+    NIRC_CUDA_TRY(cudaMemsetAsync(lvlmax, 0, 256 + (size_t)sp.grid_len * 8, s));
+  auto det_scatter = [&]() -> int {
+    if (!dx_out || r1 <= r0) return NIRC_OK;
+    return fixed_scatter_rows(sp, grad, dx_out + r0 * 24, r1 - r0, lvlmax, rec.pos, idx, r0, B,
+                              acc, s);
+  };
+  if (tc_path) {
+    if (ntiles == 0) {
+      NIRC_CUDA_TRY(cudaMemsetAsync(grad, 0, sp.grid_len * 4, s));
+      if (adam_bad) NIRC_CUDA_TRY(cudaMemsetAsync(adam_bad, 0, 4, s));
+    }
     if (ntiles > 0) {
       AsyncBuf fb(s), img(s), sb(s);
       NIRC_CUDA_TRY(fb.alloc((size_t)(ntiles + 1) * 4));
-      int32_t* fix = static_cast<int32_t*>(fb.p);
-      NIRC_CUDA_TRY(cudaMemsetAsync(fix, 0, 4, s));
+      int32_t* fix = static_cast<int32_t*>(fb.p);  // zeroed by k_train_prepare
       if (rstat == nullptr) {  // per-record static encoding (train_frame computes it once)
         NIRC_CUDA_TRY(sb.alloc((size_t)train_static_bytes(rec.n)));
         int st = launch_record_static(sp, rec, static_cast<float*>(sb.p), s);
@@ -241,7 +328,8 @@ int launch_fused_train(const nirc_spec_t& sp, const float* theta, const nirc_rec
         rstat = static_cast<const float*>(sb.p);
       }
       int st = launch_train_tc(sp, theta, rstat, rec, idx, B, loss_kind, loss_eps, grad, partials,
-                               loss_part, flags, s, tile0, tile1, fix, nullptr);
+                               loss_part, flags, s, tile0, tile1, fix, dx_out, lvlmax, lvlmax,
+                               lvlmax ? 256 + (int64_t)sp.grid_len * 8 : 0, adam_bad);
       if (st) return st;
       // fp32 fix-up of the tiles beyond the fp16 range (CTAs past the list exit)
       const FusedLayout L = fused_layout(sp, kTileRows);
@@ -254,12 +342,14 @@ int launch_fused_train(const nirc_spec_t& sp, const float* theta, const nirc_rec
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       t128::k_train_tile<<<ntiles < 32 ? ntiles : 32, kTT, sm, s>>>(
           sp, L, theta, static_cast<const float*>(img.p), rec, idx, B, loss_kind, loss_eps, grad,
-          partials, loss_part, flags, tile0, fix);
+          partials, loss_part, flags, tile0, fix, dx_out, lvlmax);
       NIRC_LAUNCH_CHECK("k_train_tile(fix)");
+      if ((st = det_scatter())) return st;
     }
-    const int np = (int)(sp.theta_len - sp.grid_len);
-    k_reduce_grad<<<(np + 31) / 32, 256, 0, s>>>(sp, partials, ntiles, loss_part, B, grad,
-                                                 loss_out, flags, adam_bad, mode);
+    const int nbm = reduce_blocks_mlp(sp);
+    k_reduce_grad<<<nbm + (mode == 0 ? 64 : 0), 256, 0, s>>>(
+        sp, partials, ntiles, loss_part, B, grad, loss_out, flags, adam_bad, mode, nbm, t, bc,
+        b1, b2);
     NIRC_LAUNCH_CHECK("k_reduce_grad");
     return NIRC_OK;
   }
@@ -280,17 +370,19 @@ int launch_fused_train(const nirc_spec_t& sp, const float* theta, const nirc_rec
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       kern<<<ntiles * nsub, kTT, sm, s>>>(sp, L, theta, static_cast<const float*>(img.p), rec,
                                           idx, B, loss_kind, loss_eps, grad, partials, loss_part,
-                                          flags, tile0, nullptr);
+                                          flags, tile0, nullptr, dx_out, lvlmax);
       return NIRC_OK;
     };
     int st = tr == 32 ? launch(t32::k_train_tile)
                       : tr == 64 ? launch(t64::k_train_tile) : launch(t128::k_train_tile);
     if (st) return st;
     NIRC_LAUNCH_CHECK("k_train_tile");
+    if ((st = det_scatter())) return st;
   }
-  const int np = (int)(sp.theta_len - sp.grid_len);
-  k_reduce_grad<<<(np + 31) / 32, 256, 0, s>>>(sp, partials, ntiles * nsub, loss_part, B, grad,
-                                               loss_out, flags, adam_bad, mode);
+  const int nbm = reduce_blocks_mlp(sp);
+  k_reduce_grad<<<nbm + (mode == 0 ? 64 : 0), 256, 0, s>>>(sp, partials, ntiles * nsub, loss_part,
+                                                           B, grad, loss_out, flags, adam_bad,
+                                                           mode, nbm, t, bc, b1, b2);
   NIRC_LAUNCH_CHECK("k_reduce_grad");
   return NIRC_OK;
 }

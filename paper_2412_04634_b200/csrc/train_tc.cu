@@ -304,7 +304,22 @@ __global__ void k_record_static(nirc_spec_t sp, nirc_records_t rec, float4* __re
 __global__ void k_train_prepare(nirc_spec_t sp, TcNet net, DenseLevels dl,
                                 const float* __restrict__ theta, uint8_t* __restrict__ img,
                                 float* __restrict__ bias, int32_t* __restrict__ unsafe,
-                                float2* __restrict__ dense, uint32_t* __restrict__ dslot) {
+                                float2* __restrict__ dense, uint32_t* __restrict__ dslot,
+                                float4* __restrict__ zero_a, int64_t n_zero_a,
+                                float4* __restrict__ zero_b, int64_t n_zero_b,
+                                int32_t* __restrict__ zero_c, int32_t* __restrict__ zero_d) {
+  // the step's zero-initialised buffers (grid gradient, fixed-point
+  // accumulators, fix-up count, Adam's bad flag): no separate memsets
+  {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = g; i < n_zero_a; i += stride) zero_a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t i = g; i < n_zero_b; i += stride) zero_b[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (g == 0) {
+      if (zero_c) *zero_c = 0;
+      if (zero_d) *zero_d = 0;
+    }
+  }
   int nw = 0;
   for (int l = 0; l < net.nl; ++l) nw += net.N[l] * net.K[l];
   const int nb = net.nl * 64, nd = dl.off[dl.n];
@@ -351,7 +366,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                const int64_t* __restrict__ idx, int64_t B, int loss_kind, double loss_eps,
                float* __restrict__ grad, float* __restrict__ partials,
                double* __restrict__ loss_part, int32_t* __restrict__ flags, int64_t tile0,
-               int32_t* __restrict__ fix, float* __restrict__ dx_out, float* __restrict__ dbg,
+               int32_t* __restrict__ fix, float* __restrict__ dx_out,
+               uint32_t* __restrict__ lvlmax, float* __restrict__ dbg,
                long long* __restrict__ prof) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t s_rmax[kSplit][kR];
@@ -613,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // all belong to h = 0).  Per layer: maxima -> scales -> operands -> MMAs
   // (dA and dW committed separately: the dW MMA runs under the dA epilogue
   // and the next layer's maxima) -> staged, coalesced dW / db partials.
-  float* wpart = partials + (int64_t)blockIdx.x * (sp.theta_len - sp.grid_len);
+  float* wpart = partials + (int64_t)blockIdx.x * part_stride(sp);
   float dz[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) dz[j] = 0.0f;
@@ -772,12 +788,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       dbg[row * kDbgStride + 312 + 2 * (h + 4 * k) + 1] = dxv[2 * k + 1];
     }
   // ---- hash-grid scatter (encoding.py:160-167): levels h, h + 4, h + 8 ------
-  if (dx_out != nullptr) {  // deterministic mode: the rows' grid gradients
-    if (live)
-      for (int k = 0; k < 3; ++k) {
+  if (dx_out != nullptr) {  // deterministic mode: the rows' grid gradients + level maxima
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (live) {
         dx_out[row * 24 + 2 * (h + 4 * k)] = dxv[2 * k];
         dx_out[row * 24 + 2 * (h + 4 * k) + 1] = dxv[2 * k + 1];
       }
+      const uint32_t m = __reduce_max_sync(
+          0xffffffffu, max(__float_as_uint(fabsf(dxv[2 * k])), __float_as_uint(fabsf(dxv[2 * k + 1]))));
+      if (lane == 0) atomicMax(lvlmax + h + 4 * k, m);
+    }
   } else if (live) {
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -863,7 +884,8 @@ int launch_train_tc(const nirc_spec_t& sp, const float* theta, const float* rsta
                     const nirc_records_t& rec, const int64_t* idx, int64_t B, int loss_kind,
                     double loss_eps, float* grad, float* partials, double* loss_part,
                     int32_t* flags, cudaStream_t s, int64_t tile0, int64_t tile1, int32_t* fix,
-                    float* dx_out) {
+                    float* dx_out, uint32_t* lvlmax, void* zero_b, int64_t zero_b_bytes,
+                    int32_t* adam_bad) {
   tc::TcNet net;
   if (!tc::tc_net_for(sp, &net, tc::PrecF16x2::kId)) return NIRC_E_UNSUPPORTED;
   const ttc::Plan P = ttc::plan_for(sp, net);
@@ -881,16 +903,21 @@ int launch_train_tc(const nirc_spec_t& sp, const float* theta, const float* rsta
   NIRC_CUDA_TRY(cudaMemsetAsync(unsafe, 0, 4, s));
   int total = P.dl.off[P.dl.n] + net.nl * 64;
   for (int l = 0; l < net.nl; ++l) total += net.N[l] * net.K[l];
-  ttc::k_train_prepare<<<(total + 255) / 256, 256, 0, s>>>(sp, net, P.dl, theta, img, bias, unsafe,
-                                                           dense, dslot);
+  // grad's grid part is zeroed by the prepare kernel (atomic scatter target)
+  const int64_t nza = sp.grid_len / 4, nzb = zero_b_bytes / 16;
+  int64_t blocks = (total + 255) / 256;
+  blocks = blocks < 4 * 148 ? 4 * 148 : blocks;
+  ttc::k_train_prepare<<<(unsigned)blocks, 256, 0, s>>>(
+      sp, net, P.dl, theta, img, bias, unsafe, dense, dslot, reinterpret_cast<float4*>(grad), nza,
+      reinterpret_cast<float4*>(zero_b), nzb, fix, adam_bad);
   NIRC_LAUNCH_CHECK("k_train_prepare");
   NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)ttc::k_train_tc,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.total));
   ttc::k_train_tc<<<ntiles, ttc::kThreads, P.total, s>>>(
       sp, net, P, img, bias, unsafe, dense, dslot, theta, reinterpret_cast<const float4*>(rstat),
       rec, idx,
-      B, loss_kind, loss_eps, grad, partials, loss_part, flags, tile0, fix, dx_out, g_train_dbg,
-      g_train_prof);
+      B, loss_kind, loss_eps, grad, partials, loss_part, flags, tile0, fix, dx_out, lvlmax,
+      g_train_dbg, g_train_prof);
   NIRC_LAUNCH_CHECK("k_train_tc");
   return NIRC_OK;
 }

@@ -154,7 +154,8 @@ __global__ void __launch_bounds__(kTT, 1)
                  const int64_t* __restrict__ idx, int64_t B, int loss_kind, double loss_eps,
                  float* __restrict__ grad, float* __restrict__ partials,
                  double* __restrict__ loss_part, int32_t* __restrict__ flags, int64_t tile0,
-                 const int32_t* __restrict__ tile_list) {
+                 const int32_t* __restrict__ tile_list, float* __restrict__ dx_out,
+                 uint32_t* __restrict__ lvlmax) {
   extern __shared__ __align__(16) float fsm[];
   __shared__ uint32_t tmem_holder;
   __shared__ __align__(8) uint64_t wbar;
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(kTT, 1)
     loss_part[slot] = t;
   }
   // ---- backward ----------------------------------------------------------
-  float* wpart = partials + slot * (sp.theta_len - sp.grid_len);
+  float* wpart = partials + slot * part_stride(sp);
   float dX[kDX];
   for (int l = NL - 1; l >= 0; --l) {
     {  // a_prev of layer l -> staging (relu(z_{l-1}) or the encoded input)
@@ -340,9 +341,15 @@ __global__ void __launch_bounds__(kTT, 1)
     for (int q = 0; q < kLvl; ++q) {
       const int lvl = kLvl * h + q;
       if (lvl >= sp.levels) continue;
+      const float d0 = dX[2 * q], d1 = dX[2 * q + 1];
+      if (dx_out != nullptr) {  // deterministic mode: rows for the ordered scatter
+        dx_out[row * 24 + 2 * lvl] = d0;
+        dx_out[row * 24 + 2 * lvl + 1] = d1;
+        atomicMax(lvlmax + lvl, max(__float_as_uint(fabsf(d0)), __float_as_uint(fabsf(d1))));
+        continue;
+      }
       const LevelCell c = level_cell(ux, uy, uz, sp.res[lvl]);
       float* gl = grad + (size_t)lvl * T * 2;
-      const float d0 = dX[2 * q], d1 = dX[2 * q + 1];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const float w = corner_weight(c, k);

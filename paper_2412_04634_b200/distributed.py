@@ -181,6 +181,7 @@ class DeviceOps:
         _lib.check(self.lib.nirc_train_grad(
             cs, _dev.ptr(cache.theta), rec, int(cache.seed), int(cache.frame), int(step),
             int(batch_cap), LOSS_KINDS.index(cache.loss_kind), float(cache.loss_eps),
+            C.byref(_lib.train_opts(cache.adam, getattr(cache, "deterministic", False))),
             int(tile_begin), int(tile_end), _dev.ptr(grad), _dev.ptr(aux), _dev.ptr(flags),
             None, _dev.ptr(ws), int(ws.numel()), _dev.stream()), "nirc_train_grad")
 
@@ -192,7 +193,8 @@ class DeviceOps:
         _lib.check(self.lib.nirc_train_apply(
             cs, _dev.ptr(cache.theta), _dev.ptr(st.m), _dev.ptr(st.v), _dev.ptr(st._t),
             _dev.ptr(st._skipped), _dev.ptr(grad), _dev.ptr(aux), int(batch), float(st.lr),
-            _dev.ptr(loss_out), _dev.ptr(flags), _dev.ptr(st._scratch), _dev.stream()),
+            C.byref(_lib.train_opts(st)), _dev.ptr(loss_out), _dev.ptr(flags),
+            _dev.ptr(st._scratch), _dev.stream()),
             "nirc_train_apply")
 
     def train_full(self, cache, records, steps, batch):

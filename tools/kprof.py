@@ -26,7 +26,9 @@ def train_job():
                   **{k: torch.as_tensor(v).cuda() for k, v in r.items()})
     theta = torch.from_numpy(init_theta(spec, seed=1, out_scale=0.1)).cuda()
     adam = AdamState(theta)
-    return lambda: train_frame_device(spec, theta, rec, seed=0, frame=0, steps=4, adam=adam)
+    det = os.environ.get("DET", "0") == "1"
+    return lambda: train_frame_device(spec, theta, rec, seed=0, frame=0, steps=4, adam=adam,
+                                      deterministic=det)
 
 
 def frame_job():

@@ -75,7 +75,7 @@ flags = torch.zeros(1, dtype=torch.int32, device="cuda")
 need = lib.nirc_train_workspace_bytes(cs, n, 16384)
 ws = torch.empty(need, dtype=torch.uint8, device="cuda")
 _lib.check(lib.nirc_train_grad(cs, _dev.ptr(theta0 := torch.from_numpy(th.copy()).cuda()), r_c, 7,
-                               2, 0, 16384, 1, 0.01, 0, ntiles, _dev.ptr(grad), _dev.ptr(aux),
+                               2, 0, 16384, 1, 0.01, None, 0, ntiles, _dev.ptr(grad), _dev.ptr(aux),
                                _dev.ptr(flags), None, _dev.ptr(ws), int(ws.numel()),
                                _dev.stream()), "nirc_train_grad")
 got = grad.cpu().numpy().astype(np.float64)

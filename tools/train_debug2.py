@@ -51,7 +51,7 @@ S = 336
 dbg = torch.zeros((n, S), dtype=torch.float32, device="cuda")
 lib.nirc_debug_train_probe.argtypes = [C.c_void_p]
 lib.nirc_debug_train_probe(C.c_void_p(dbg.data_ptr()))
-_lib.check(lib.nirc_train_grad(cs, _dev.ptr(thD), r_c, 7, 2, 1, 16384, 1, 0.01, 0,
+_lib.check(lib.nirc_train_grad(cs, _dev.ptr(thD), r_c, 7, 2, 1, 16384, 1, 0.01, None, 0,
                                lib.nirc_train_tiles(n, 16384), _dev.ptr(grad), _dev.ptr(aux),
                                _dev.ptr(flags), None, _dev.ptr(ws), int(ws.numel()),
                                _dev.stream()), "nirc_train_grad")
