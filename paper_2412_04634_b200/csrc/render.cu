@@ -17,6 +17,7 @@
 //                     deterministic order (cache_lc_s, kernels.py:424-448).
 //   k_accumulate      per pixel: r = PT sum + cache terms; img += r,
 //                     img2 += r*r, term += vertices (render_kernel :753-759).
+#include <cstdlib>
 #include <type_traits>
 #include "common.cuh"
 #include "pt_common.cuh"
@@ -1455,6 +1456,7 @@ static int render_impl(const nirc_scene_t* scene, const double* cam, const nirc_
     const uint32_t extra =
         (uint32_t)(128 * 3 * 8 + a.verts_per_tile * 24 * 4 + 16 + a.verts_per_tile * sizeof(CacheVertex));
     const int ng = tc_ok ? tc_groups_for(net, extra) : 0;
+
     AsyncBuf wbuf(s);
     if (ng > 0) {
       PackedNet pn;

@@ -316,15 +316,17 @@ __device__ __forceinline__ void write_a_row_ts(uint32_t a_hi, uint32_t a_lo, con
   }
 }
 
+// acc0 = 1: the accumulator was pre-filled (with the layer's bias).
 __device__ __forceinline__ void issue_layer_ts(const TcNet& net, int l, uint32_t w_base,
-                                               uint32_t a_hi, uint32_t a_lo, uint32_t tmem_d) {
+                                               uint32_t a_hi, uint32_t a_lo, uint32_t tmem_d,
+                                               uint32_t acc0 = 0) {
   const int K = net.K[l], N = net.N[l];
   const uint32_t idesc =
       PrecF16x2::kIdescFmt | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTileRows >> 4) << 24);
   const uint32_t w_hi = w_base + net.woff[l];
   const uint32_t w_lo = w_hi + (uint32_t)(N * K * 2);
   const uint32_t w_lbo = (uint32_t)N * 16;
-  uint32_t acc = 0;
+  uint32_t acc = acc0;
 #pragma unroll
   for (int term = 0; term < 3; ++term) {  // hi*lo, lo*hi, then hi*hi
     const uint32_t A = term == 1 ? a_lo : a_hi;
@@ -341,22 +343,39 @@ __device__ __forceinline__ void issue_layer_ts(const TcNet& net, int l, uint32_t
   }
 }
 
+// This thread's lane of a layer's accumulator <- the layer's bias (N columns,
+// 16 or 64): the MMAs then accumulate on top of it, so no epilogue adds it.
+__device__ __forceinline__ void prefill_bias_ts(const float* __restrict__ b, int N,
+                                                uint32_t taddr) {
+  for (int q = 0; q < N / 16; ++q) {
+    float bq[16];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      *reinterpret_cast<float4*>(bq + 4 * j) = *reinterpret_cast<const float4*>(b + 16 * q + 4 * j);
+    tmem_st16(taddr + 16 * q, bq);
+  }
+}
+
 // Runs the network for the group's tile; precondition: this thread wrote its
-// layer-0 row with write_a_row_ts and waited (tcgen05.wait::st).
-// `unsafe` accumulates the fp16 range guard over every hidden activation.
+// layer-0 row with write_a_row_ts.  Every layer's accumulator starts from
+// its bias (prefill_bias_ts); the epilogue is ReLU + fp16 hi/lo split.
+// `unsafe` accumulates the fp16 range guard over every hidden activation
+// (an fp16 hi part that rounded to inf; activations are >= 0 after ReLU, so
+// their fp16 bit patterns order like their values).
 __device__ __forceinline__ void run_chain_ts(const TcNet& net, uint32_t w_base,
                                              const float* __restrict__ s_bias, int group, int tg,
                                              uint32_t tmem_grp, uint32_t mbar, uint32_t& phase,
                                              float* y, bool& unsafe) {
   const uint32_t lane_off = (uint32_t)((tg >> 5) * 32) << 16;
   const uint32_t tmem_d = tmem_grp, a_hi = tmem_grp + 64, a_lo = tmem_grp + 96;
+  prefill_bias_ts(s_bias, net.N[0], tmem_d + lane_off);
   tmem_wait_st();
   fence_before();
   named_bar_sync(1 + group, kGroupThreads);
   if ((tg >> 5) == 0) {
     fence_after();
     if (elect_one()) {
-      issue_layer_ts(net, 0, w_base, a_hi, a_lo, tmem_d);
+      issue_layer_ts(net, 0, w_base, a_hi, a_lo, tmem_d, 1u);
       mma_commit(mbar);
     }
     __syncwarp();
@@ -366,38 +385,32 @@ __device__ __forceinline__ void run_chain_ts(const TcNet& net, uint32_t w_base,
     phase ^= 1u;
     fence_after();
     if (l < net.nl - 1) {
-      const float* b = s_bias + l * 64;
+      uint32_t hmax = 0u;
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         float h[32];
         tmem_ld32(tmem_d + lane_off + half * 32, h);
-        float bq[32];
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          *reinterpret_cast<float4*>(bq + 4 * j) =
-              *reinterpret_cast<const float4*>(b + half * 32 + 4 * j);
         tmem_wait_ld();
-        float hm = 0.0f;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float z = h[j] + bq[j];
-          h[j] = z > 0.0f ? z : 0.0f;
-          hm = fmaxf(hm, h[j]);
-        }
-        unsafe |= !(hm < kF16Max);
+        for (int j = 0; j < 32; ++j) h[j] = fmaxf(h[j], 0.0f);
         uint32_t hh[16], ll[16];
 #pragma unroll
         for (int c = 0; c < 4; ++c) PrecF16x2::split8(h + 8 * c, hh + 4 * c, ll + 4 * c);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) hmax = __vmaxu2(hmax, hh[c]);
         tmem_st16u(a_hi + lane_off + half * 16, hh);
         tmem_st16u(a_lo + lane_off + half * 16, ll);
       }
+      unsafe |= (hmax & 0xffffu) > 0x7bffu || (hmax >> 16) > 0x7bffu;
+      // the accumulator was read: pre-fill it with the next layer's bias
+      prefill_bias_ts(s_bias + (l + 1) * 64, net.N[l + 1], tmem_d + lane_off);
       tmem_wait_st();
       fence_before();
       named_bar_sync(1 + group, kGroupThreads);
       if ((tg >> 5) == 0) {
         fence_after();
         if (elect_one()) {
-          issue_layer_ts(net, l + 1, w_base, a_hi, a_lo, tmem_d);
+          issue_layer_ts(net, l + 1, w_base, a_hi, a_lo, tmem_d, 1u);
           mma_commit(mbar);
         }
         __syncwarp();
@@ -408,7 +421,7 @@ __device__ __forceinline__ void run_chain_ts(const TcNet& net, uint32_t w_base,
       tmem_wait_ld();
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const float z = o[j] + s_bias[l * 64 + j];
+        const float z = o[j];
         y[j] = net.out_act == 0 ? (z > 0.0f ? z : 0.0f) : 1.0f / (1.0f + expf(-z));
       }
     }
