@@ -195,6 +195,41 @@ int nirc_query(const nirc_spec_t* spec, const float* theta, const double* surf,
                int64_t n_dirs, float* Y, int32_t precision, int32_t* status_flags,
                void* stream);
 
+/* ---- the reference's 64-bit shadow mode -------------------
+ * init_theta(dtype=float64) networks: the same entries on f64 theta / rows
+ * (fp64 SIMT; every reduction over rows in a fixed order).  encode: X f64
+ * (features sum w * theta in f64, SH and aux unrounded), entries/weights as
+ * nirc_encode (encoding.py:111-157); forward/backward as mlp.py:102-154
+ * (zs, scratch: (n, sum(dims[1:])) f64; grad accumulates); scatter as
+ * nirc_scatter_grid_grad (np.add.at order); loss: every operation f64,
+ * frozen_denom (n,3, nullable) = loss_relative_l2's frozen denominator
+ * (losses.py:33-42); adam: f64 m / v (adam.py:20-33), skip + skipped++ on a
+ * non-finite gradient.  scratch: >= 4 bytes of device memory. */
+int nirc_encode_f64(const nirc_spec_t* spec, const double* theta,
+                    const double* pos, const double* normal,
+                    const double* albedo, const double* rough,
+                    const double* dirs, int64_t n, double* X, int64_t* entries,
+                    float* weights, void* stream);
+int nirc_mlp_forward_f64(const nirc_spec_t* spec, const double* theta,
+                         const double* X, int64_t n, double* Y, double* zs,
+                         int32_t* nonfinite_flag, void* stream);
+int nirc_mlp_backward_f64(const nirc_spec_t* spec, const double* theta,
+                          const double* X, const double* zs, const double* dY,
+                          int64_t n, double* grad, double* dX, double* scratch,
+                          void* stream);
+int nirc_scatter_grid_grad_f64(const nirc_spec_t* spec, double* grad,
+                               const int64_t* entries, const float* weights,
+                               const double* dX, int64_t n, int64_t dx_stride,
+                               void* stream);
+int nirc_loss_f64(int32_t kind, const double* Y, const double* target,
+                  const double* pdf, const double* running_mean,
+                  const double* frozen_denom, double eps, int64_t n, double* dY,
+                  double* loss_out, int32_t* status_flags, void* stream);
+int nirc_adam_step_f64(double* theta, double* m, double* v, const double* grad,
+                       int64_t n, int64_t* t, int64_t* skipped, double lr,
+                       double beta1, double beta2, double eps, int32_t* scratch,
+                       void* stream);
+
 /* ---- losses (pkg/src/nirclab/losses.py) --------------------------------- */
 /* kind: 0 l2, 1 relative_l2, 2 variance, 3 bce.  Y (n,3) f32, target (n,3)
  * f64, pdf (n,) f64 (unused for bce), running_mean (3,) f64 (variance).

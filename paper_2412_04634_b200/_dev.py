@@ -69,3 +69,10 @@ def empty(shape, dtype):
 def zeros(shape, dtype):
     require_cuda()
     return torch.zeros(shape, dtype=dtype, device="cuda")
+
+
+def is_f64(x):
+    """True for float64 arrays / tensors (the reference's 64-bit shadow mode)."""
+    if isinstance(x, torch.Tensor):
+        return x.dtype == torch.float64
+    return getattr(x, "dtype", None) == np.float64

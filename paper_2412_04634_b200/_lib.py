@@ -127,6 +127,12 @@ SIGNATURES = {
     "nirc_mlp_backward": (I32, [SPEC, P, P, P, P, I64, P, P, P, P]),
     "nirc_full_forward": (I32, [SPEC, P, P, P, P, P, P, I64, P, I32, P, P]),
     "nirc_loss": (I32, [I32, P, P, P, P, F64, I64, P, P, P, P, P]),
+    "nirc_encode_f64": (I32, [SPEC, P, P, P, P, P, P, I64, P, P, P, P]),
+    "nirc_mlp_forward_f64": (I32, [SPEC, P, P, I64, P, P, P, P]),
+    "nirc_mlp_backward_f64": (I32, [SPEC, P, P, P, P, I64, P, P, P, P]),
+    "nirc_scatter_grid_grad_f64": (I32, [SPEC, P, P, P, P, I64, I64, P]),
+    "nirc_loss_f64": (I32, [I32, P, P, P, P, P, F64, I64, P, P, P, P]),
+    "nirc_adam_step_f64": (I32, [P, P, P, P, I64, P, P, F64, F64, F64, F64, P, P]),
     "nirc_adam_step": (I32, [P, P, P, P, I64, P, P, F64, F64, F64, F64, P, P, P]),
     "nirc_train_step": (I32, [SPEC, P, P, P, P, P, C.POINTER(NircRecords), U64, I64, I32,
                               I32, I32, F64, F64, C.POINTER(NircTrainOpts), P, P, P, P, P,

@@ -41,11 +41,16 @@ def _c_spec(spec):
 def encode_batch(spec, theta, pos, normal, albedo, rough, dirs, dtype=None):
     """Returns (X, entries, weights) like encoding.py:111-157.
 
-    X is (B, in_dim) float32, entries (B, levels, 8) int64 feature-table
-    slots, weights (B, levels, 8) float32.
-    """
-    if dtype not in (None, np.float32, torch.float32):
-        raise NotImplementedError("the device encoder produces float32 rows")
+    X is (B, in_dim) in ``dtype`` (default: theta's dtype, as the
+    reference), entries (B, levels, 8) int64 feature-table slots, weights
+    (B, levels, 8) float32.  float64 = the reference's shadow mode: the
+    features accumulate in f64, SH and aux are not rounded to f32."""
+    if dtype is None:
+        dtype = np.float64 if _dev.is_f64(theta) else np.float32
+    if dtype in (np.float64, torch.float64):
+        return _encode_batch_f64(spec, theta, pos, normal, albedo, rough, dirs)
+    if dtype not in (np.float32, torch.float32):
+        raise NotImplementedError(f"encode_batch dtype {dtype}")
     host = _dev.is_host(pos)
     B = int(pos.shape[0])
     th = _dev.dev(theta, torch.float32)
@@ -61,8 +66,40 @@ def encode_batch(spec, theta, pos, normal, albedo, rough, dirs, dtype=None):
     return _dev.out(X, host), _dev.out(ent, host), _dev.out(wts, host)
 
 
+def _encode_batch_f64(spec, theta, pos, normal, albedo, rough, dirs):
+    host = _dev.is_host(pos)
+    B = int(pos.shape[0])
+    th = _dev.dev(theta, torch.float64)
+    args = [_dev.dev(a, torch.float64) for a in (pos, normal, albedo, rough, dirs)]
+    X = _dev.empty((B, spec.in_dim), torch.float64)
+    ent = _dev.empty((B, spec.levels, 8), torch.int64)
+    wts = _dev.empty((B, spec.levels, 8), torch.float32)
+    lib = _lib.load()
+    _lib.check(lib.nirc_encode_f64(_c_spec(spec), _dev.ptr(th), *[_dev.ptr(a) for a in args], B,
+                                   _dev.ptr(X), _dev.ptr(ent), _dev.ptr(wts), _dev.stream()),
+               "nirc_encode_f64")
+    return _dev.out(X, host), _dev.out(ent, host), _dev.out(wts, host)
+
+
 def scatter_grid_grad(spec, grad_theta, entries, weights, dX):
-    """grad[slot*F + f] += w * dX[:, l*F + f] (encoding.py:160-167), in place."""
+    """grad[slot*F + f] += w * dX[:, l*F + f] (encoding.py:160-167), in place,
+    in np.add.at's order (bit-identical given identical inputs)."""
+    if _dev.is_f64(grad_theta):
+        host = _dev.is_host(grad_theta)
+        g = _dev.dev(grad_theta, torch.float64)
+        e = _dev.dev(entries, torch.int64)
+        w = _dev.dev(weights, torch.float32)
+        d = _dev.dev(dX, torch.float64)
+        lib = _lib.load()
+        _lib.check(lib.nirc_scatter_grid_grad_f64(_c_spec(spec), _dev.ptr(g), _dev.ptr(e),
+                                                  _dev.ptr(w), _dev.ptr(d), int(e.shape[0]),
+                                                  int(d.shape[1]), _dev.stream()),
+                   "nirc_scatter_grid_grad_f64")
+        if host:
+            grad_theta[...] = g.cpu().numpy()
+        elif g.data_ptr() != grad_theta.data_ptr():
+            grad_theta.copy_(g)
+        return grad_theta
     host = _dev.is_host(grad_theta)
     g = _dev.dev(grad_theta, torch.float32)
     e = _dev.dev(entries, torch.int64)

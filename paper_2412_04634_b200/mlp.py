@@ -96,10 +96,34 @@ def _zs_width(spec):
     return int(sum(int(d) for d in spec.dims[1:]))
 
 
+def _mlp_forward_f64(spec, theta, X, training):
+    host = _dev.is_host(X)
+    th = _dev.dev(theta, torch.float64)
+    x = _dev.dev(X, torch.float64)
+    if x.dim() == 1:
+        x = x.reshape(1, -1)
+    n = int(x.shape[0])
+    Y = _dev.empty((n, int(spec.dims[-1])), torch.float64)
+    zs = _dev.empty((n, _zs_width(spec)), torch.float64) if training else None
+    flag = _dev.zeros((1,), torch.int32)
+    lib = _lib.load()
+    _lib.check(lib.nirc_mlp_forward_f64(_lib.make_c_spec(spec), _dev.ptr(th), _dev.ptr(x), n,
+                                        _dev.ptr(Y), _dev.ptr(zs), _dev.ptr(flag),
+                                        _dev.stream()), "nirc_mlp_forward_f64")
+    if int(flag.item()) != 0:
+        raise DivergenceError("non-finite network parameter")
+    if training:
+        return _dev.out(Y, host), (x, zs)
+    return _dev.out(Y, host)
+
+
 def mlp_forward(spec, theta, X, training=False):
     """Batch forward (mlp.py:102-122).  Returns Y, or (Y, cache) when
     training; the cache holds X and every pre-activation for mlp_backward.
-    Raises DivergenceError if theta holds a non-finite value."""
+    Raises DivergenceError if theta holds a non-finite value.  A float64
+    theta runs the reference's 64-bit shadow mode (fp64 kernels)."""
+    if _dev.is_f64(theta):
+        return _mlp_forward_f64(spec, theta, X, training)
     host = _dev.is_host(X)
     th = _dev.dev(theta, torch.float32)
     x = _dev.dev(X, torch.float32)
@@ -121,9 +145,31 @@ def mlp_forward(spec, theta, X, training=False):
     return _dev.out(Y, host)
 
 
+def _mlp_backward_f64(spec, theta, cache, dY, entries, weights):
+    X, zs = cache
+    host = _dev.is_host(dY)
+    th = _dev.dev(theta, torch.float64)
+    dy = _dev.dev(dY, torch.float64)
+    n = int(X.shape[0])
+    g = _dev.zeros((spec.theta_len,), torch.float64)
+    dX = _dev.empty((n, spec.in_dim), torch.float64)
+    scratch = _dev.empty((n, _zs_width(spec)), torch.float64)
+    lib = _lib.load()
+    _lib.check(lib.nirc_mlp_backward_f64(_lib.make_c_spec(spec), _dev.ptr(th), _dev.ptr(X),
+                                         _dev.ptr(zs), _dev.ptr(dy), n, _dev.ptr(g),
+                                         _dev.ptr(dX), _dev.ptr(scratch), _dev.stream()),
+               "nirc_mlp_backward_f64")
+    if entries is not None:
+        scatter_grid_grad(spec, g, _dev.dev(entries, torch.int64),
+                          _dev.dev(weights, torch.float32), dX)
+    return _dev.out(g, host)
+
+
 def mlp_backward(spec, theta, cache, dY, entries=None, weights=None):
     """Reverse mode (mlp.py:125-154); ReLU' is (z >= 0) on every layer.
-    Returns a gradient congruent to theta."""
+    Returns a gradient congruent to theta (float64 in the shadow mode)."""
+    if _dev.is_f64(theta):
+        return _mlp_backward_f64(spec, theta, cache, dY, entries, weights)
     X, zs = cache
     host = _dev.is_host(dY)
     th = _dev.dev(theta, torch.float32)
@@ -259,8 +305,10 @@ def full_forward(spec, theta, pos, normal, albedo, rough, dirs, training=False,
     SIMT twin); pinned host tensors stream through a copy/compute/copy
     pipeline (into `out`, a pinned (n, 3) f32 tensor, when given); training
     returns the reference tuple via the SIMT path."""
-    if training:
+    if training or _dev.is_f64(theta):  # the batch pipeline (and the f64 shadow mode)
         X, entries, weights = encode_batch(spec, theta, pos, normal, albedo, rough, dirs)
+        if not training:
+            return mlp_forward(spec, theta, X)
         Y, cache = mlp_forward(spec, theta, X, training=True)
         return Y, cache, entries, weights
     host = _dev.is_host(pos)
@@ -301,3 +349,86 @@ def mlp_forward_s(spec, theta, xin, h1=None, h2=None):
     y = np.asarray(Y, np.float64).reshape(-1)
     out = [float(y[i]) if i < y.size else 0.0 for i in range(3)]
     return out[0], out[1], out[2]
+
+
+def forward_scalar_reference(spec, theta, xin):
+    """Naive per-neuron forward of one encoded input, the reference's test
+    oracle (mlp.py:195-213): python-float (f64) sums in (bias, i ascending)
+    order.  Host code by design -- it is the checker, not a kernel."""
+    theta = np.asarray(theta.cpu() if isinstance(theta, torch.Tensor) else theta)
+    cur = [float(v) for v in np.asarray(xin).ravel()]
+    for layer in range(spec.nl):
+        din = int(spec.dims[layer])
+        dout = int(spec.dims[layer + 1])
+        w = int(spec.w_off[layer])
+        b = int(spec.b_off[layer])
+        nxt = []
+        for j in range(dout):
+            acc = float(theta[b + j])
+            for i in range(din):
+                acc += cur[i] * float(theta[w + j * din + i])
+            if layer < spec.nl - 1 or spec.out_act == ACT_RELU:
+                nxt.append(max(acc, 0.0))
+            else:
+                nxt.append(1.0 / (1.0 + np.exp(-acc)))
+        cur = nxt
+    return np.array(cur)
+
+
+def gradient_check(spec, theta, surf, target, pdf, loss_kind="l2", h=1e-3, eps=0.01,
+                   running_mean=None, indices=None):
+    """Five-point central-difference check of the full reverse-mode gradient
+    (mlp.py:227-292): the device forward / losses / backward (+ grid
+    scatter) against finite differences of the device loss, in theta's
+    dtype (float64 = the shadow mode, where the 1e-5 bar is meaningful).
+    The relative-L2 denominator and the variance running mean are frozen
+    across the perturbed evaluations.  Returns the maximum relative error
+    over the checked indices (default: every parameter)."""
+    from . import losses
+
+    pos, normal, albedo, rough, dirs = surf
+    theta = np.asarray(theta)
+    if running_mean is None:
+        running_mean = np.array([0.3, 0.2, 0.1])
+    Y0, cache, entries, weights = full_forward(spec, theta, pos, normal, albedo, rough, dirs,
+                                               training=True)
+    frozen = losses.relative_l2_denom(np.asarray(Y0), eps)
+
+    def eval_loss(th, want_grad=False):
+        if want_grad:
+            Y, cc, en, we = full_forward(spec, th, pos, normal, albedo, rough, dirs,
+                                         training=True)
+        else:
+            Y = full_forward(spec, th, pos, normal, albedo, rough, dirs)
+        Y = np.asarray(Y)
+        if loss_kind == "l2":
+            val, dY = losses.loss_l2(Y, target, pdf)
+        elif loss_kind == "relative_l2":
+            val, dY = losses.loss_relative_l2(Y, target, pdf, eps, frozen_denom=frozen)
+        elif loss_kind == "variance":
+            val, dY = losses.loss_variance(Y, target, pdf, running_mean)
+        elif loss_kind == "bce":
+            val, dY = losses.loss_bce(Y, target)
+        else:
+            raise ValueError(loss_kind)
+        if want_grad:
+            return val, np.asarray(mlp_backward(spec, th, cc, dY, en, we))
+        return val
+
+    _, g = eval_loss(theta, want_grad=True)
+    if indices is None:
+        indices = range(spec.theta_len)
+    gscale = np.abs(g).max()
+    worst = 0.0
+    for i in indices:
+        keep = theta[i]
+        vals = []
+        for step in (h, -h, 2.0 * h, -2.0 * h):
+            theta[i] = keep + step
+            vals.append(eval_loss(theta))
+        theta[i] = keep
+        up, dn, up2, dn2 = vals
+        fd = (8.0 * (up - dn) - (up2 - dn2)) / (12.0 * h)
+        denom = max(abs(fd), abs(g[i]), 1e-4 * gscale, 1e-12)
+        worst = max(worst, abs(fd - g[i]) / denom)
+    return worst

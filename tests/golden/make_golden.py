@@ -143,6 +143,37 @@ def golden_train1():
     np.savez_compressed(os.path.join(HERE, "train1.npz"), **out)
 
 
+def golden_f64():
+    """The reference's 64-bit shadow mode (init_theta(dtype=float64)): the
+    default D = 2 layout (2^12-entry tables) on 500 queries -- encode_batch (f64 X), mlp_forward,
+    the relative-L2 loss, mlp_backward with the grid scatter -- and three
+    Adam steps on a tiny net (test_training_is_bit_reproducible's recipe)."""
+    from nirclab.adam import AdamState, adam_step
+    from nirclab.encoding import encode_batch
+    from nirclab.losses import loss_relative_l2
+    from nirclab.mlp import full_forward, init_theta, make_spec, mlp_backward, mlp_forward
+
+    out = {}
+    spec = make_spec(depth=2, table=2 ** 12)
+    theta = init_theta(spec, seed=4, dtype=np.float64, out_scale=0.3)
+    pos, nrm, alb, rough, dirs = measure_queries(500, seed=11)
+    X, ent, wts = encode_batch(spec, theta, pos, nrm, alb, rough, dirs)
+    Y, cache = mlp_forward(spec, theta, X, training=True)
+    tgt = np.abs(np.random.default_rng(3).normal(size=(500, 3)))
+    pdf = np.random.default_rng(4).uniform(0.3, 2.0, 500)
+    val, dY = loss_relative_l2(Y, tgt, pdf)
+    g = mlp_backward(spec, theta, cache, dY, ent, wts)
+    out.update(q=np.concatenate([pos, nrm, alb, rough[:, None], dirs], axis=1), X=X, Y=Y,
+               tgt=tgt, pdf=pdf, loss=np.float64(val), g=g, theta0=theta.copy())
+    st = AdamState(theta)
+    for _ in range(3):
+        Y, cache, e2, w2 = full_forward(spec, theta, pos, nrm, alb, rough, dirs, training=True)
+        _, dY = loss_relative_l2(Y, tgt, pdf)
+        adam_step(st, theta, mlp_backward(spec, theta, cache, dY, e2, w2))
+    out["theta3"] = theta
+    np.savez_compressed(os.path.join(HERE, "f64.npz"), **out)
+
+
 def golden_losses_adam():
     """Known-answer loss values and 20 Adam steps (incl. a skipped one)."""
     from nirclab.adam import AdamState, adam_step
@@ -537,6 +568,8 @@ if __name__ == "__main__" and len(sys.argv) > 1:
         golden_trained()
     if "train1" in sys.argv:
         golden_train1()
+    if "f64" in sys.argv:
+        golden_f64()
     if "big" in sys.argv:
         golden_big()
     if "baseline" in sys.argv:
