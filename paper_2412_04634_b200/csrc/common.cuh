@@ -110,7 +110,9 @@ NIRC_D void sh_eval(double x, double y, double z, int bands,
 }
 
 // Real SH (bands = 4), the scalar-path recurrences of sh.py:36-76 in fp32.
-NIRC_D void sh4_f32(float x, float y, float z, const double* sh_k, float* out) {
+// sh_k may be the spec's f64 table or its f32 rounding (the same values).
+template <class KT>
+NIRC_D void sh4_f32(float x, float y, float z, const KT* sh_k, float* out) {
   const float s = sqrtf(x * x + y * y);
   float cphi = 1.0f, sphi = 0.0f;
   if (s > 0.0f) {

@@ -788,38 +788,72 @@ __device__ inline void build_row(const nirc_spec_t& sp, const float* feat, const
 // directions feed only the network input (SH) and the Lambert weight
 // f*cos/pdf = albedo*cos/(cos/pi); fp32 changes either by ~1e-7 relative,
 // far inside the two-level image tolerance (tests/test_gpu_render.py).
-__device__ inline RowDir row_direction_fast(const CacheVertex& r, int k) {
-  if (r.mkind != pt::MAT_LAMBERT || k >= r.ncq) return row_direction(r, k);
-  RowDir o;
-  o.kind = 0;
-  o.wi = {0.0, 0.0, 1.0};
-  o.s = 0.0;
-  o.f = {0.0, 0.0, 0.0};
-  const double u1d = rand_uniform(r.key, r.base + OFF_CACHE + 2 * k);
-  const double u2d = rand_uniform(r.key, r.base + OFF_CACHE + 2 * k + 1);
+// Per-vertex part of the fp32 Lambert sampler: the ONB of the shading normal
+// (core.py:39-54 onb_s, Duff et al.) and the visibility of wo.
+struct LambertFrame {
+  float nx, ny, nz, tx, ty, tz, bx, by, bz;
+  bool co_pos;
+};
+__device__ inline LambertFrame lambert_frame(const CacheVertex& r) {
+  LambertFrame F;
+  F.nx = (float)r.ns[0];
+  F.ny = (float)r.ns[1];
+  F.nz = (float)r.ns[2];
+  const float sg = F.nz >= 0.0f ? 1.0f : -1.0f;
+  const float a = -1.0f / (sg + F.nz);
+  const float bb = F.nx * F.ny * a;
+  F.tx = 1.0f + sg * F.nx * F.nx * a;
+  F.ty = sg * bb;
+  F.tz = -sg * F.nx;
+  F.bx = bb;
+  F.by = sg + F.ny * F.ny * a;
+  F.bz = -F.ny;
+  const double co = r.ns[0] * r.wo[0] + r.ns[1] * r.wo[1] + r.ns[2] * r.wo[2];
+  F.co_pos = co > 0.0;
+  return F;
+}
+// Per-row part: cosine-weighted direction k (cosine_dir_s, core.py:57-65)
+// from the vertex's stream; kind 1 with s = cos/pdf, or kind 0 (rejected).
+__device__ inline void lambert_row(const LambertFrame& F, uint64_t key, int64_t base, int k,
+                                   float* w, double* s_out, int* kind) {
+  const double u1d = rand_uniform(key, base + OFF_CACHE + 2 * k);
+  const double u2d = rand_uniform(key, base + OFF_CACHE + 2 * k + 1);
   const float u1 = (float)u1d, u2 = (float)u2d;
-  const float nx = (float)r.ns[0], ny = (float)r.ns[1], nz = (float)r.ns[2];
-  const float sg = nz >= 0.0f ? 1.0f : -1.0f;
-  const float a = -1.0f / (sg + nz);
-  const float bb = nx * ny * a;
-  const float tx = 1.0f + sg * nx * nx * a, ty = sg * bb, tz = -sg * nx;
-  const float bx = bb, by = sg + ny * ny * a, bz = -ny;
   float sp, cp;
   sincospif(2.0f * u2, &sp, &cp);
   const float rr = sqrtf(u1);
   const float lx = rr * cp, ly = rr * sp;
   const float lz = sqrtf(fmaxf(0.0f, 1.0f - u1));
   const float pdf = lz * (float)pt::INV_PI;
-  const float wx = tx * lx + bx * ly + nx * lz;
-  const float wy = ty * lx + by * ly + ny * lz;
-  const float wz = tz * lx + bz * ly + nz * lz;
-  const double co = r.ns[0] * r.wo[0] + r.ns[1] * r.wo[1] + r.ns[2] * r.wo[2];
-  if (co <= 0.0 || pdf <= 0.0f) return o;
-  const float ci = wx * nx + wy * ny + wz * nz;
-  if (ci <= 0.0f) return o;
-  o.kind = 1;
-  o.wi = {wx, wy, wz};
-  o.s = (double)(ci / pdf);
+  w[0] = F.tx * lx + F.bx * ly + F.nx * lz;
+  w[1] = F.ty * lx + F.by * ly + F.ny * lz;
+  w[2] = F.tz * lx + F.bz * ly + F.nz * lz;
+  *kind = 0;
+  *s_out = 0.0;
+  if (!F.co_pos || pdf <= 0.0f) return;
+  const float ci = w[0] * F.nx + w[1] * F.ny + w[2] * F.nz;
+  if (ci <= 0.0f) return;
+  *kind = 1;
+  *s_out = (double)(ci / pdf);
+}
+
+// fp32 producer for the amortised inference rows (render path only; the
+// reference-exact f64 sampler above stays for non-Lambert lobes).  The
+// directions feed only the network input (SH) and the Lambert weight
+// f*cos/pdf = albedo*cos/(cos/pi); fp32 changes either by ~1e-7 relative,
+// far inside the two-level image tolerance (tests/test_gpu_render.py).
+__device__ inline RowDir row_direction_fast(const CacheVertex& r, int k) {
+  if (r.mkind != pt::MAT_LAMBERT || k >= r.ncq) return row_direction(r, k);
+  RowDir o;
+  o.f = {0.0, 0.0, 0.0};
+  const LambertFrame F = lambert_frame(r);
+  float w[3];
+  lambert_row(F, r.key, r.base, k, w, &o.s, &o.kind);
+  if (o.kind == 0) {
+    o.wi = {0.0, 0.0, 1.0};
+    return o;
+  }
+  o.wi = {w[0], w[1], w[2]};
   o.f = {r.alb[0] * pt::INV_PI, r.alb[1] * pt::INV_PI, r.alb[2] * pt::INV_PI};
   return o;
 }
@@ -849,6 +883,8 @@ struct InferArgs {
   long long* dbg;       // optional phase timestamps (CTA 0, group 0, thread 0)
   const int32_t* w_unsafe;  // F16x2: a weight outside the fp16 range (every tile flagged)
   int32_t* fix;             // F16x2 range guard: [count, tile ids...] for k_infer_fix
+  int ablate;               // tools only (NIRC_INFER_ABLATE): 1 = producers skip the
+                            // row work, 2 = chains skip MMAs + epilogues (wrong results)
 };
 
 // Deferred vertex term from its rows' contributions (row k at rows[3k]):
@@ -1007,6 +1043,8 @@ __global__ void __launch_bounds__(NG * 128, 1)
   }
   tc::tc_epilogue(tmem_base, NG, P::kId);
 }
+
+#include "infer_ws.cuh"
 
 // fp16 range fix-up of k_infer_tc<F16x2>: recomputes every vertex of the
 // flagged tiles (a.fix) with the fp32 twin -- same rows, same k-ordered
@@ -1448,7 +1486,8 @@ static int render_impl(const nirc_scene_t* scene, const double* cam, const nirc_
   if (tl) {
     if (!spec || !theta) return NIRC_E_CONFIG;
     const int R = rows_per_vertex(c);
-    InferArgs a{w.cv, w.counters, w.result, nullptr, R, 128 / R, g_infer_probe, nullptr, w.fix};
+    InferArgs a{w.cv, w.counters, w.result, nullptr, R, 128 / R, g_infer_probe, nullptr, w.fix, 0};
+    if (const char* e = getenv("NIRC_INFER_ABLATE")) a.ablate = atoi(e);
     const int prec = c.precision == 2 ? tc::PrecF16x2::kId : tc::PrecTF32x3::kId;
     tc::TcNet net;
     const bool tc_ok =
@@ -1475,7 +1514,45 @@ static int render_impl(const nirc_scene_t* scene, const double* cam, const nirc_
         kern<<<grid, threads, L.total, s>>>(*spec, net, L, theta, pn.img, pn.bias, a);
         return NIRC_OK;
       };
-      if (prec == tc::PrecF16x2::kId) {
+      // warp-specialised kernel (infer_ws.cuh) where its shared-memory plan fits
+      int np_ws = 2;
+      if (const char* e = getenv("NIRC_INFER_NP")) np_ws = atoi(e);  // 0 = k_infer_tc
+      if (np_ws > 2) np_ws = 2;
+      const ws::Layout WL = ws::layout(net, a.verts_per_tile, np_ws > 0 ? np_ws : 1);
+      bool ws_shape = net.K[0] == 48 && net.N[0] == 64 && net.N[net.nl - 1] == 16;
+      for (int l = 1; l < net.nl; ++l) ws_shape = ws_shape && net.K[l] == 64;
+      for (int l = 0; l < net.nl - 1; ++l) ws_shape = ws_shape && net.N[l] == 64;
+      const bool use_ws = prec == tc::PrecF16x2::kId && np_ws > 0 && ws_shape &&
+                          WL.total <= 227u * 1024u - 256u;
+      auto launch_ws = [&](auto kern, int threads, int chain_regs, int prod_regs) -> int {
+        // setmaxnreg only redistributes the registers the CTA was launched
+        // with: check the split against the compiled allocation
+        cudaFuncAttributes fa;
+        NIRC_CUDA_TRY(cudaFuncGetAttributes(&fa, (const void*)kern));
+        const int npw = threads / 128 - ws::kChainGroups;
+        if (chain_regs > 0 &&
+            fa.numRegs * threads < ws::kChainGroups * 128 * chain_regs + npw * 128 * prod_regs) {
+          set_last_error("k_infer_ws register split exceeds its allocation (%d x %d)",
+                         fa.numRegs, threads);
+          return NIRC_E_UNSUPPORTED;
+        }
+        NIRC_CUDA_TRY(cudaFuncSetAttribute((const void*)kern,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)WL.total));
+        kern<<<grid, threads, WL.total, s>>>(*spec, net, WL, theta, pn.img, pn.bias, a);
+        return NIRC_OK;
+      };
+#define NIRC_WS_LAUNCH(NPV, PROBE)                                                         \
+  launch_ws(k_infer_ws<NPV, PROBE>, (ws::kChainGroups + NPV) * 128, ws::kChainRegs<NPV>, \
+            ws::kProdRegs<NPV>)
+      if (use_ws && a.dbg) {  // phase stamps (tools/infer_ab.py)
+        if (np_ws == 1) st = NIRC_WS_LAUNCH(1, true);
+        else st = NIRC_WS_LAUNCH(2, true);
+      } else if (use_ws) {
+        if (np_ws == 1) st = NIRC_WS_LAUNCH(1, false);
+        else st = NIRC_WS_LAUNCH(2, false);
+#undef NIRC_WS_LAUNCH
+      } else if (prec == tc::PrecF16x2::kId) {
         if (ng == 4) st = launch(k_infer_tc<tc::PrecF16x2, 4>, 512);
         else if (ng == 3) st = launch(k_infer_tc<tc::PrecF16x2, 3>, 384);
         else if (ng == 2) st = launch(k_infer_tc<tc::PrecF16x2, 2>, 256);

@@ -174,7 +174,14 @@ __global__ void __launch_bounds__(256) k_reduce_grad(
     const int per = (ntiles + 7) / 8;
     const int t0 = wid * per, t1 = min(ntiles, t0 + per);
     float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (4 * c4 < ps) {
+    if (4 * c4 + 4 > np && 4 * c4 < np) {
+      // the column holding the last parameters: scalar loads, so the
+      // partials' padding past np (never written) is not read
+      const float* src = partials + 4 * c4;
+      float* acc = &s4.x;
+      for (int tt = t0; tt < t1; ++tt)
+        for (int k = 0; 4 * c4 + k < np; ++k) acc[k] += src[(int64_t)tt * ps + k];
+    } else if (4 * c4 < np) {
       const float4* src = reinterpret_cast<const float4*>(partials) + c4;
       int tt = t0;
       for (; tt + 8 <= t1; tt += 8) {  // 8 independent 16-byte loads in flight
