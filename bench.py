@@ -40,6 +40,46 @@ L2_GATHER_BYTES_PER_QUERY = 12 * 8 * 2 * 4            # 768
 PRECISION = int(os.environ.get("NIRC_BENCH_PRECISION", "2"))  # 2: tcgen05 2xFP16 split
 
 
+def cfg2_config(world):
+    """The workload dict both arms print (the driver compares them)."""
+    return {"workload": "cfg2 NIRC inference micro-bench: 2^22 random (pos,dir) queries per "
+                        "GPU, fused hash-grid+SH encode + 64-wide 2-hidden-layer MLP",
+            "model": "nirc 12x2^15x2 hash + SH4 + 64x2 MLP", "global_batch": world * N_QUERIES,
+            "seq_len": 1, "parallelism": f"dp{world} (independent query shards)",
+            "l2_flush": "inputs (436 MB/step) larger than L2; hash tables L2-resident"}
+
+
+def host_info():
+    """The CPU baseline's context: CPU model, threads, and the
+    numpy / numba / OpenBLAS versions of the reference's stack."""
+    info = {"cpu_model": None, "host_threads": os.cpu_count()}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        import numpy
+        info["numpy"] = numpy.__version__
+    except Exception:
+        info["numpy"] = None
+    try:
+        import numba
+        info["numba"] = numba.__version__
+    except Exception:
+        info["numba"] = None
+    try:
+        import threadpoolctl
+        blas = [d for d in threadpoolctl.threadpool_info() if d.get("user_api") == "blas"]
+        info["openblas"] = (blas[0].get("internal_api", "") + " " + blas[0].get("version", "")
+                            + " " + str(blas[0].get("architecture", ""))) if blas else None
+    except Exception:
+        info["openblas"] = None
+    return info
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -169,13 +209,12 @@ def run_reference(args, rank, world):
         "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "cfg2 NIRC inference micro-bench (2^22 random queries, D=2)",
-                   "model": "nirc 12x2^15x2 hash + SH4 + 64x2 MLP", "global_batch": N_QUERIES,
-                   "seq_len": 1, "parallelism": "cpu processes"},
+        "config": cfg2_config(args.gpus),
         "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "port",
-                         "sample": f"{cores} x 2^15 random queries per step through "
-                                   "oracle/nirc_oracle.full_forward (numpy restatement of "
-                                   "encode_batch + mlp_forward)"},
+                         "sample": f"{cores} x 2^15 random queries per step (one process per "
+                                   "core) through oracle/nirc_oracle.full_forward (numpy "
+                                   "restatement of encode_batch + mlp_forward)",
+                         "host": host_info()},
         "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -183,6 +222,29 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------- frame leg -------
+FLOPS_PER_QUERY_D4 = 2 * (47 * 64 + 3 * 64 * 64 + 64 * 3)  # 30,976: the frame caches' D = 4
+
+
+def infer_roofline(queries, infer_ms):
+    """The frame inference kernel against the tensor roofline: useful
+    (reference-arithmetic) FLOP per launch / its device time, over the
+    measured dense bf16 peak; the 2xFP16 split issues 3 MMAs per product."""
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("bf16_tflops", 1590.0))
+    tf = queries * FLOPS_PER_QUERY_D4 / (infer_ms * 1e-3) / 1e12
+    return {"bound": "tensor", "kernel": "k_infer_ws (fused encode + tcgen05 MLP + MLMC combine)",
+            "useful_flop_per_launch": queries * FLOPS_PER_QUERY_D4, "avg_launch_ms": infer_ms,
+            "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
+            "issued_frac": 3 * tf / peak,
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops" if peaks else "fallback",
+            "timing": "CUDA events on the render stream around the launch (C-ABI stage timer), "
+                      "sequential frame (no train-stream overlap), median over frames"}
+
+
 def frame_bench(frames, warmup, width=1920, height=1080, nc=(16,), comm=None, name="cfg3"):
     """BASELINE config 3: Cornell at 1920x1080, two-level with nc=(16,) at
     the first cache vertex, spp 1, D = 4 cache; then collect ceil(0.025 W H)
@@ -208,6 +270,15 @@ def frame_bench(frames, warmup, width=1920, height=1080, nc=(16,), comm=None, na
     count = default_train_count(scene)
     world = comm.world if comm is not None else 1
     ops = D.DeviceOps() if world > 1 else None
+    # per-stage device times of the render launch set (C-ABI stage events)
+    import ctypes
+
+    from paper_2412_04634_b200 import _lib
+
+    lib = _lib.load()
+    lib.nirc_stage_timing(1)
+    stage_buf = (ctypes.c_float * 3)()
+    stages = {"trace": [], "infer": [], "accumulate": []}
     for f in range(warmup + frames):
         if comm is not None:
             comm.barrier()
@@ -235,6 +306,9 @@ def frame_bench(frames, warmup, width=1920, height=1080, nc=(16,), comm=None, na
         ev[3].record(stream)
         torch.cuda.synchronize()
         if f >= warmup:
+            _lib.check(lib.nirc_stage_times(stage_buf, 3), "nirc_stage_times")
+            for k, v in zip(("trace", "infer", "accumulate"), stage_buf):
+                stages[k].append(float(v))
             t = torch.tensor([ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]),
                               ev[2].elapsed_time(ev[3]), ev[0].elapsed_time(ev[3])],
                              device="cuda")
@@ -248,11 +322,13 @@ def frame_bench(frames, warmup, width=1920, height=1080, nc=(16,), comm=None, na
                 comm.all_reduce_sum_(qt)
             queries.append(int(qt.item()))
             records.append(len(rec))
+    lib.nirc_stage_timing(0)
     if world > 1:
         same = D.replicas_identical(cache, comm)
     else:
         same = True
     med = {k: sorted(v)[len(v) // 2] for k, v in phases.items()}
+    smed = {k: sorted(v)[len(v) // 2] for k, v in stages.items()}
     return {
         "metric": f"ms_per_frame_{width}x{height}", "value": med["frame"], "unit": "ms/frame",
         "higher_is_better": False, "frames": frames, "warmup": warmup, "n_gpus": world,
@@ -262,6 +338,8 @@ def frame_bench(frames, warmup, width=1920, height=1080, nc=(16,), comm=None, na
         "train_paths_per_frame": count,
         "train_samples_per_sec": 4 * min(16384, records[-1]) / (med["train"] * 1e-3),
         "render_queries_per_sec": queries[-1] / (med["render"] * 1e-3),
+        "stage_ms": {k + "_ms": v for k, v in smed.items()},
+        "infer_roofline": infer_roofline(queries[-1] // world, smed["infer"]),
         "phases": "render_collect = one nirc_render_collect launch set (path tracer with the "
                   "training walks as its first work items, fused inference, accumulation, "
                   "record compaction); record_allgather = multi-GPU record exchange",
@@ -326,6 +404,65 @@ def frame_bench_overlap(frames, warmup, width=1920, height=1080, nc=(16,), name=
         "config": f"{name}: cornell {width}x{height}, two-level nc={tuple(nc)}, spp 1, D=4 "
                   f"cache, collect 0.025 W H paths, 4 x min(16384, records) train steps; "
                   "render(f) || train(f) (frame.FramePipeline)",
+        "reference_cpu_context": "SURVEY.md 6: 122.6 s/frame on 1 core (not re-timed here)",
+    }
+
+
+def frame_bench_sharded(frames, warmup, comm, width=1920, height=1080, nc=(16,), name="cfg3"):
+    """The sharded frame (N > 1) through distributed.ShardedFramePipeline:
+    render(f) of this rank's row band (+ its share of frame f+1's training
+    walks) on the render stream while the record all-gather and the
+    tile-sharded train(f) with one gradient all-reduce per step run on a
+    second stream.  Frame time per rank = device time from the frame's
+    start to the later stream's end; the max over ranks is reported."""
+    import torch
+
+    from paper_2412_04634_b200 import distributed as D
+    from paper_2412_04634_b200.caches import Cache
+    from paper_2412_04634_b200.frame import config3
+    from paper_2412_04634_b200.scene import load_builtin
+
+    scene = load_builtin("cornell").with_resolution(width, height)
+    cache = Cache.create("nirc", scene, seed=0, init="random")
+    pipe = D.ShardedFramePipeline(scene, cache, config3(nc), comm, seed=0)
+    frame_ms, render_ms, train_ms, queries, records = [], [], [], [], []
+    for f in range(warmup + frames):
+        comm.barrier()
+        torch.cuda.synchronize()
+        e0, er = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(pipe.s_render)
+        _, rows, st = pipe.step(f)
+        er.record(pipe.s_render)
+        torch.cuda.synchronize()
+        if f >= warmup:
+            t0, t1 = pipe.train_events
+            t = torch.tensor([max(e0.elapsed_time(er), e0.elapsed_time(t1)),
+                              e0.elapsed_time(er), t0.elapsed_time(t1)], device="cuda")
+            comm.all_reduce_max_(t)
+            q = st["queries"].clone()
+            comm.all_reduce_sum_(q)
+            a, b, c = t.tolist()
+            frame_ms.append(a)
+            render_ms.append(b)
+            train_ms.append(c)
+            queries.append(int(q.item()))
+            records.append(st.get("records", 0))
+    same = D.replicas_identical(cache, comm)
+    med = lambda v: sorted(v)[len(v) // 2]  # noqa: E731
+    return {
+        "metric": f"ms_per_frame_{width}x{height}", "value": med(frame_ms), "unit": "ms/frame",
+        "higher_is_better": False, "frames": frames, "warmup": warmup, "n_gpus": comm.world,
+        "render_collect_ms": med(render_ms), "train_stream_span_ms": med(train_ms),
+        "queries_per_frame": queries[-1], "records_per_frame": records[-1],
+        "render_queries_per_sec": queries[-1] / (med(render_ms) * 1e-3),
+        "replicas_identical": same, "overlap": True,
+        "phases": "per rank: render_collect = its row band + its share of the next frame's "
+                  "walks (render stream); train_stream_span = record all-gather + 4 sharded "
+                  "steps with one gradient all-reduce each (train stream); max over ranks",
+        "config": f"{name}: cornell {width}x{height}, two-level nc={tuple(nc)}, spp 1, D=4 "
+                  f"cache, collect 0.025 W H paths, 4 x min(16384, records) train steps; "
+                  f"sharded over {comm.world} GPUs (row bands, path shards, tile shards) with "
+                  "render(f) || train(f) (distributed.ShardedFramePipeline)",
         "reference_cpu_context": "SURVEY.md 6: 122.6 s/frame on 1 core (not re-timed here)",
     }
 
@@ -495,6 +632,24 @@ def run_b200(args, rank, world, local_rank):
     h2d = int(sum(h.numel() * h.element_size() for h in host))
     d2h = int(y_last[0].numel() * 4)
 
+    # ---- the same call as a numpy user makes it (the reference's types):
+    # numpy theta and numpy f64 rows in (pageable), numpy f32 rgb out; the
+    # call returns host results, so its wall time is the step time
+    host_np = [h.numpy() for h in host]
+    theta_np = theta.cpu().numpy()
+    full_forward(spec, theta_np, *host_np, precision=PRECISION)
+    np_steps = 5
+    barrier()
+    t0w = time.perf_counter()
+    for _ in range(np_steps):
+        y_np = full_forward(spec, theta_np, *host_np, precision=PRECISION)
+    np_s = time.perf_counter() - t0w
+    assert isinstance(y_np, np.ndarray)
+    e2e_numpy = {"value": world * n * np_steps / np_s, "unit": "queries/s", "steps": np_steps,
+                 "h2d_bytes_per_step": h2d + theta_np.nbytes, "d2h_bytes_per_step": d2h,
+                 "path": "paper_2412_04634_b200.mlp.full_forward on numpy arrays (pageable host "
+                         "memory, numpy theta), host wall clock per call"}
+
     fb = None
     if not args.no_frame:
         from paper_2412_04634_b200 import distributed as D
@@ -506,7 +661,8 @@ def run_b200(args, rank, world, local_rank):
             fb = frame_bench_overlap(args.frame_steps, 3)
             fb["sequential"] = frame_bench(args.frame_steps, 3)
         else:
-            fb = frame_bench(args.frame_steps, 3, comm=comm)
+            fb = frame_bench_sharded(args.frame_steps, 3, comm)
+            fb["sequential"] = frame_bench(args.frame_steps, 3, comm=comm)
         if not args.no_extra_frames:
             # BASELINE cfg5 (4K, 32 NIRC samples/pixel as nc=(16,16): the
             # reference caps N_c at 28 per vertex) and cfg1 (the reference's
@@ -517,10 +673,10 @@ def run_b200(args, rank, world, local_rank):
                 fb["cfg1_128"] = frame_bench_overlap(args.frame_steps, 3, 128, 128, (8,),
                                                      name="cfg1")
             else:
-                fb["cfg5_4k"] = frame_bench(max(3, args.frame_steps // 2), 2, 3840, 2160,
-                                            (16, 16), comm=comm, name="cfg5")
-                fb["cfg1_128"] = frame_bench(args.frame_steps, 3, 128, 128, (8,), comm=comm,
-                                             name="cfg1")
+                fb["cfg5_4k"] = frame_bench_sharded(max(3, args.frame_steps // 2), 2, comm, 3840,
+                                                    2160, (16, 16), name="cfg5")
+                fb["cfg1_128"] = frame_bench_sharded(args.frame_steps, 3, comm, 128, 128, (8,),
+                                                     name="cfg1")
             fb["cfg1_128"]["reference_cpu_context"] = (
                 "SURVEY.md 6: 1.28 s/frame for cfg1 on 1 core (render 1084 + collect 12 + "
                 "train 179 ms)")
@@ -566,12 +722,8 @@ def run_b200(args, rank, world, local_rank):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "cfg2 NIRC inference micro-bench: 2^22 random (pos,dir) queries "
-                               "per GPU, fused hash-grid+SH encode + 64-wide 2-hidden-layer MLP "
-                               f"(tcgen05 {'2xFP16-split' if PRECISION == 2 else '3xTF32'})",
-                   "model": "nirc 12x2^15x2 hash + SH4 + 64x2 MLP", "global_batch": world * n,
-                   "seq_len": 1, "parallelism": f"dp{world} (independent query shards)",
-                   "l2_flush": "inputs (436 MB/step) larger than L2; hash tables L2-resident"},
+        "config": cfg2_config(world),
+        "kernel_precision": f"tcgen05 {'2xFP16-split' if PRECISION == 2 else '3xTF32'}",
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved_gbs / hbm_peak, "traffic": traffic,
                      "kernel": "k_full_forward_tc (+ k_pack_weights)",
@@ -593,18 +745,28 @@ def run_b200(args, rank, world, local_rank):
                                  "rarely whole windows) of the host copies run slower, so "
                                  "the per-step median is given beside it",
                 "path": "paper_2412_04634_b200.mlp.full_forward on pinned host tensors (chunked "
-                        "H2D / fused kernel / D2H pipeline inside the call)"},
+                        "H2D / fused kernel / D2H pipeline inside the call)",
+                "numpy_caller": e2e_numpy},
         "gpu_launches": 2 * args.steps,
     }
     if fb is not None:
         line["frame_1080p"] = fb
+        seq = fb.get("sequential", fb)
+        line["frame_1080p_ms"] = fb["value"]
+        line["train_samples_per_sec"] = seq.get("train_samples_per_sec")
+        line["infer_roofline"] = seq.get("infer_roofline")
+        if "cfg5_4k" in fb:
+            line["frame_4k_ms"] = fb["cfg5_4k"]["value"]
+        if "cfg1_128" in fb:
+            line["frame_128_ms"] = fb["cfg1_128"]["value"]
     if world == 1 and not args.no_cpu_baseline:
         # ~10 s of single-core work: 64 chunks of 2^15 random cfg2 queries
         rate, nq = cpu_baseline(cores=1, chunks=64, chunk=1 << 15)
         line["cpu_baseline"] = {"value": rate, "unit": "queries/s", "cores": 1, "kind": "port",
                                 "sample": f"{nq} random cfg2 queries (64 chunks of 2^15) through "
                                           "oracle/nirc_oracle.full_forward (numpy "
-                                          "encode_batch + mlp_forward, OPENBLAS 1 thread)"}
+                                          "encode_batch + mlp_forward, OPENBLAS 1 thread)",
+                                "host": host_info()}
     print(json.dumps(line), flush=True)
 
 

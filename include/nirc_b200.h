@@ -130,6 +130,13 @@ typedef struct nirc_render_cfg {
 const char* nirc_version(void);
 int nirc_last_error(char* buf, int buflen);
 int nirc_device_sm_count(void);
+/* Measurement (bench.py): with stage timing on, every render records CUDA
+ * events on its stream around the tracer, the fused inference (+ fp16
+ * fix-up) and the accumulation; nirc_stage_times writes the last timed
+ * render's [trace, inference, accumulate] milliseconds (waits for it).
+ * Not part of the reference's interface. */
+int nirc_stage_timing(int32_t on);
+int nirc_stage_times(float* ms, int32_t n);
 
 /* ---- encoding (pkg/src/nirclab/encoding.py) ----------------------------- */
 /* encode_batch (encoding.py:111-157): X (n,in_dim) f32, entries (n,levels,8)

@@ -121,6 +121,8 @@ SIGNATURES = {
     "nirc_version": (C.c_char_p, []),
     "nirc_last_error": (I32, [C.c_char_p, I32]),
     "nirc_device_sm_count": (I32, []),
+    "nirc_stage_timing": (I32, [I32]),
+    "nirc_stage_times": (I32, [P, I32]),
     "nirc_encode": (I32, [SPEC, P, P, P, P, P, P, I64, P, P, P, P]),
     "nirc_scatter_grid_grad": (I32, [SPEC, P, P, P, P, I64, I64, P]),
     "nirc_mlp_forward": (I32, [SPEC, P, P, I64, P, P, P, P]),

@@ -51,6 +51,11 @@ NIRC_HD uint64_t rand_u64(uint64_t key, uint64_t dim) {
 NIRC_HD double rand_uniform(uint64_t key, uint64_t dim) {
   return (double)(rand_u64(key, dim) >> 11) * (1.0 / 9007199254740992.0);
 }
+// (float)rand_uniform(key, dim) in one conversion: rounding the 53-bit
+// integer to f32 and scaling by the power of two 2^-53 is the same rounding.
+NIRC_D float rand_uniform_f32(uint64_t key, uint64_t dim) {
+  return __ull2float_rn(rand_u64(key, dim) >> 11) * 0x1p-53f;
+}
 
 // ----------------------------------------------------- exact f64 helpers --
 NIRC_D double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -116,8 +121,9 @@ NIRC_D void sh4_f32(float x, float y, float z, const KT* sh_k, float* out) {
   const float s = sqrtf(x * x + y * y);
   float cphi = 1.0f, sphi = 0.0f;
   if (s > 0.0f) {
-    cphi = x / s;
-    sphi = y / s;
+    const float inv = 1.0f / s;
+    cphi = x * inv;
+    sphi = y * inv;
   }
   float cm = 1.0f, sm = 0.0f, pmm = 1.0f;
 #pragma unroll
@@ -135,7 +141,7 @@ NIRC_D void sh4_f32(float x, float y, float z, const KT* sh_k, float* out) {
       float p;
       if (l == m) p = pmm;
       else if (l == m + 1) p = z * (2.0f * m + 1.0f) * pmm;
-      else p = ((2.0f * l - 1.0f) * z * p1 - (l + m - 1.0f) * p2) / (float)(l - m);
+      else p = ((2.0f * l - 1.0f) * z * p1 - (l + m - 1.0f) * p2) * (1.0f / (float)(l - m));
       p2 = p1;
       p1 = p;
       const int base = l * l + l;

@@ -816,9 +816,8 @@ __device__ inline LambertFrame lambert_frame(const CacheVertex& r) {
 // from the vertex's stream; kind 1 with s = cos/pdf, or kind 0 (rejected).
 __device__ inline void lambert_row(const LambertFrame& F, uint64_t key, int64_t base, int k,
                                    float* w, double* s_out, int* kind) {
-  const double u1d = rand_uniform(key, base + OFF_CACHE + 2 * k);
-  const double u2d = rand_uniform(key, base + OFF_CACHE + 2 * k + 1);
-  const float u1 = (float)u1d, u2 = (float)u2d;
+  const float u1 = rand_uniform_f32(key, base + OFF_CACHE + 2 * k);
+  const float u2 = rand_uniform_f32(key, base + OFF_CACHE + 2 * k + 1);
   float sp, cp;
   sincospif(2.0f * u2, &sp, &cp);
   const float rr = sqrtf(u1);
@@ -1333,6 +1332,19 @@ __global__ void k_compact_records(Stage st, const int64_t* __restrict__ off,
 
 long long* g_infer_probe = nullptr;  // set by nirc_debug_infer_probe (tools only)
 
+// Optional per-stage timing of the render launch set (nirc_stage_timing):
+// CUDA events on the launch stream around the tracer, the fused inference
+// (+ its fp16 fix-up) and the accumulation of the last timed render.
+struct StageTimer {
+  bool on = false;
+  bool created = false;
+  cudaEvent_t ev[4];
+};
+StageTimer g_stage;
+static void stage_mark(int i, cudaStream_t s) {
+  if (g_stage.on) cudaEventRecord(g_stage.ev[i], s);
+}
+
 bool default_layout(const nirc_spec_t& sp) {
   return sp.levels == 12 && sp.feats == 2 && sp.bands == 4 && sp.in_dim == 47;
 }
@@ -1467,6 +1479,7 @@ static int render_impl(const nirc_scene_t* scene, const double* cam, const nirc_
     return NIRC_OK;
   };
   int tst;
+  stage_mark(0, s);
   constexpr int kS = NIRC_TRACE_MINB, kB = NIRC_TRACE_MINB_BVH;
   const bool bvh = scene->bvh_packed != nullptr;  // general scene: packed BVH traversal
   if (c.mode >= 2 && bvh)
@@ -1483,6 +1496,7 @@ static int render_impl(const nirc_scene_t* scene, const double* cam, const nirc_
                     : launch_trace(k_trace<false, false, kS>);
   if (tst) return tst;
   NIRC_LAUNCH_CHECK("k_trace");
+  stage_mark(1, s);
   if (tl) {
     if (!spec || !theta) return NIRC_E_CONFIG;
     const int R = rows_per_vertex(c);
@@ -1586,10 +1600,12 @@ static int render_impl(const nirc_scene_t* scene, const double* cam, const nirc_
       NIRC_LAUNCH_CHECK("k_combine_rows");
     }
   }
+  stage_mark(2, s);
   const int64_t npix = (int64_t)(c.row1 - c.row0) * c.width;
   k_accumulate<<<(int)((npix + 127) / 128), 128, 0, s>>>(c, w.acc, w.term, w.result, tl ? 1 : 0,
                                                         img, img2, term);
   NIRC_LAUNCH_CHECK("k_accumulate");
+  stage_mark(3, s);
   if (queries_out)
     NIRC_CUDA_TRY(cudaMemcpyAsync(queries_out, w.counters + 1, 8, cudaMemcpyDeviceToDevice, s));
   return NIRC_OK;
@@ -1709,6 +1725,26 @@ extern "C" int nirc_collect(const nirc_scene_t* scene, const double* cam, uint64
 // stamps of CTA 0 / group 0 of the next k_infer_tc launches into `buf`
 // (device, >= 64*8 int64), or disable with NULL.
 extern "C" void nirc_debug_infer_probe(long long* buf) { nirc::g_infer_probe = buf; }
+
+extern "C" int nirc_stage_timing(int32_t on) {
+  if (on && !g_stage.created) {
+    for (int i = 0; i < 4; ++i) NIRC_CUDA_TRY(cudaEventCreate(&g_stage.ev[i]));
+    g_stage.created = true;
+  }
+  g_stage.on = on != 0;
+  return NIRC_OK;
+}
+
+extern "C" int nirc_stage_times(float* ms, int32_t n) {
+  if (!g_stage.created) {
+    set_last_error("stage timing was never enabled");
+    return NIRC_E_CONFIG;
+  }
+  NIRC_CUDA_TRY(cudaEventSynchronize(g_stage.ev[3]));
+  for (int i = 0; i < 3 && i < n; ++i)
+    NIRC_CUDA_TRY(cudaEventElapsedTime(&ms[i], g_stage.ev[i], g_stage.ev[i + 1]));
+  return NIRC_OK;
+}
 
 // Tools/tests only (not part of include/nirc_b200.h): the fp32 pre-filtered
 // triangle scan against the plain f64 scan on n random rays through the

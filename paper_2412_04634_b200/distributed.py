@@ -113,7 +113,7 @@ class Comm:
         n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
         counts = [torch.zeros_like(n) for _ in range(self.world)]
         self.dist.all_gather(counts, n, group=self.group)
-        counts = [int(c.item()) for c in counts]
+        counts = torch.cat(counts).tolist()  # one host read for all ranks' counts
         mx = max(counts)
         if mx == 0:
             return t[:0]
@@ -246,14 +246,20 @@ def train_frame_sharded(cache, records, comm, steps=4, batch=None, ops=None):
     else:
         ntiles = ops.train_tiles(n, cap)
         t0, t1 = split_range(ntiles, comm.world, comm.rank)
-        grad = torch.empty_like(theta)
+        # ONE all-reduce per step: the flat gradient with [loss sum, bad-pdf
+        # count] appended as two more f32 (the loss sum rounds to f32 before
+        # the cross-GPU sum; every rank receives the same bits)
+        plen = int(theta.numel())
+        buf = torch.empty((plen + 2,), dtype=torch.float32, device=theta.device)
+        grad = buf[:plen]
         aux = torch.zeros((2,), dtype=torch.float64, device=theta.device)
         flags_t = torch.zeros((1,), dtype=torch.int32, device=theta.device)
         losses = torch.zeros((steps,), dtype=torch.float64, device=theta.device)
         for s in range(steps):
             ops.train_grad(cache, records, s, cap, t0, t1, grad, aux, flags_t)
-            comm.all_reduce_sum_(grad)
-            comm.all_reduce_sum_(aux)
+            buf[plen:].copy_(aux)
+            comm.all_reduce_sum_(buf)
+            aux.copy_(buf[plen:])
             ops.train_apply(cache, grad, aux, B, losses[s:s + 1], flags_t)
         trace = losses.cpu().numpy().tolist()
         flags = int(flags_t.item())
@@ -320,6 +326,93 @@ def run_frame_sharded(scene, cache, config, comm, seed, frame, spp=1, steps=4, b
     return (img, img2, term), rows, stats
 
 
+class ShardedFramePipeline:
+    """The sharded frame with rendering and training overlapped (SURVEY.md
+    8(e): "render(f) || collect + train(f) ... so the allreduce hides under
+    rendering"), the multi-GPU form of frame.FramePipeline:
+
+      frame f:  theta_r <- theta_f                                (render stream)
+                render this rank's row band with theta_r, walking this rank's
+                share of frame f+1's training paths in the same launch
+                all-gather records(f); tile-sharded train(f) with one
+                gradient all-reduce per step -> theta_{f+1}         (train stream)
+
+    The walks never read theta, so frame f+1's records collected during
+    frame f's launch are the ones run_frame_sharded collects at f+1; each
+    frame computes what run_frame_sharded computes, only overlapped.  The
+    record all-gather and the gradient all-reduces run on the train stream
+    (NCCL orders them after the stream's prior work), so they hide under the
+    render of the same frame.  Across an animation boundary the next records
+    are collected on their own at the next frame.
+    """
+
+    def __init__(self, scene, cache, config, comm, seed, spp=1, train_fraction=0.025, steps=4,
+                 batch=None, ops=None):
+        self.scene, self.cache, self.config, self.comm = scene, cache, config, comm
+        self.seed, self.spp, self.steps, self.batch = seed, spp, steps, batch
+        self.train_fraction = train_fraction
+        self.ops = ops or DeviceOps()
+        self.s_render = torch.cuda.current_stream()
+        self.s_train = torch.cuda.Stream()
+        self.theta_r = torch.empty_like(cache.theta)
+        self.pending = None  # (frame, callable -> this rank's Records of that frame)
+        self.train_events = None
+
+    def _count(self, scene):
+        from .caches import default_train_count
+
+        return default_train_count(scene, self.train_fraction)
+
+    def step(self, frame, out=None):
+        """Frame `frame` on this rank: ((img, img2, term) band sums, rows, stats)."""
+        from .estimators import render_and_collect, render_device
+
+        cache, comm = self.cache, self.comm
+        scene = self.scene = self.scene.at_frame(frame)
+        cache.scene = scene
+        same_geometry = not any((a.frame <= frame + 1) != (a.frame <= frame)
+                                for a in scene.desc.anims)
+        h = int(scene.camera[15])
+        rows = split_range(h, comm.world, comm.rank)
+        count = self._count(scene)
+        paths = split_range(count, comm.world, comm.rank)
+        if self.pending is not None and self.pending[0] == frame:
+            local = self.pending[1]()
+            packed = pack_records({k: getattr(local, k) for k, _ in REC_COLS})
+        else:
+            packed = self.ops.collect_range(scene, cache.seed, frame, paths[0],
+                                            paths[1] - paths[0], cache.record_kind)
+        self.pending = None
+        # theta_f snapshot for the render, after the previous training
+        self.s_render.wait_stream(self.s_train)
+        self.theta_r.copy_(cache.theta)
+        snap = torch.cuda.Event()
+        snap.record(self.s_render)
+        if same_geometry:
+            img, img2, term, q, nxt = render_and_collect(
+                scene, self.config, cache, self.seed, self.spp, frame, count=count,
+                train_frame=frame + 1, rows=rows, paths=paths, out=out, theta=self.theta_r,
+                defer=True)
+            self.pending = (frame + 1, nxt)
+        else:
+            img, img2, term, q = render_device(scene, self.config, cache, self.seed, self.spp,
+                                               frame, rows=rows, out=out, theta=self.theta_r)
+        stats = {"rows": rows, "queries": q}
+        self.train_events = None
+        self.s_train.wait_event(snap)  # theta_f copied; this frame's records complete
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(self.s_train):
+            t0.record(self.s_train)
+            rec = unpack_records(comm.all_gather_rows(packed), cache.record_kind, frame)
+            stats["records"] = len(rec)
+            if len(rec):
+                stats["trace"] = train_frame_sharded(cache, rec, comm, self.steps, self.batch,
+                                                     self.ops)
+            t1.record(self.s_train)
+        self.train_events = (t0, t1)
+        return (img, img2, term), rows, stats
+
+
 def broadcast_cache(cache, comm, src=0):
     """Make every replica equal to rank `src`'s cache state."""
     for t in (cache.theta, cache.adam.m, cache.adam.v, cache.adam._t, cache.adam._skipped):
@@ -339,5 +432,6 @@ def replicas_identical(cache, comm):
 
 
 __all__ = ["split_range", "Comm", "DeviceOps", "collect_sharded", "train_frame_sharded",
+           "ShardedFramePipeline",
            "render_band", "gather_image", "run_frame_sharded", "broadcast_cache",
            "replicas_identical", "pack_records", "unpack_records", "REC_COLS", "REC_WIDTH"]

@@ -181,3 +181,77 @@ def test_sharded_frame_two_ranks_one_gpu(lib):
         assert (d > 1e-5).mean() < 1e-2 and d.max() < 1e-2 and d.mean() < 1e-6, (
             d.max(), d.mean(), (d > 1e-5).mean())
     assert np.array_equal(res[0][1], res[1][1])
+
+
+def _pipeline_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2412_04634_b200 import distributed as D
+        from paper_2412_04634_b200.caches import Cache
+        from paper_2412_04634_b200.frame import config3
+
+        comm = D.Comm()
+        sc = _cornell(96)
+        outs = {}
+        for mode in ("sequential", "overlapped"):
+            cache = Cache.create("nirc", sc, seed=0, init="random")
+            pipe = D.ShardedFramePipeline(sc, cache, config3((8,)), comm, seed=0)
+            frames = []
+            for f in range(3):
+                if mode == "sequential":
+                    (img, _, term), rows, st = D.run_frame_sharded(sc, cache, config3((8,)),
+                                                                   comm, seed=0, frame=f)
+                else:
+                    (img, _, term), rows, st = pipe.step(f)
+                    torch.cuda.current_stream().wait_stream(pipe.s_train)
+                torch.cuda.synchronize()
+                frames.append((D.gather_image(img, rows, comm).cpu().numpy(),
+                               D.gather_image(term, rows, comm).cpu().numpy(),
+                               st.get("records"), st.get("trace")))
+            outs[mode] = (frames, cache.theta.cpu().numpy(), D.replicas_identical(cache, comm))
+        q.put((rank, outs))
+    except Exception:  # noqa: BLE001
+        import traceback
+
+        q.put((rank, "ERROR " + traceback.format_exc()))
+    finally:
+        import torch.distributed as dist
+
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_overlapped_sharded_frames_match_sequential(lib):
+    """ShardedFramePipeline (render(f) || all-gather + sharded train(f) on a
+    second stream, frame f+1's records walked in frame f's launch) against
+    run_frame_sharded on two ranks sharing one GPU: the same frames -- path
+    lengths, record counts, loss traces, images and the final theta (the
+    deterministic scatter makes the sums order-free) -- and identical
+    replicas."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pipeline_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=900) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+    for v in res.values():
+        assert not isinstance(v, str), v
+    for r in (0, 1):
+        seq, ovl = res[r]["sequential"], res[r]["overlapped"]
+        assert seq[2] and ovl[2]
+        for (i0, t0, n0, tr0), (i1, t1, n1, tr1) in zip(seq[0], ovl[0]):
+            assert np.array_equal(t0, t1)
+            assert n0 == n1
+            np.testing.assert_allclose(tr1, tr0, rtol=1e-6)
+            np.testing.assert_allclose(i1, i0, rtol=1e-6, atol=1e-9)
+        np.testing.assert_allclose(ovl[1], seq[1], rtol=1e-6, atol=1e-9)
+    np.testing.assert_array_equal(res[0]["overlapped"][1], res[1]["overlapped"][1])
