@@ -226,6 +226,39 @@ NIRC_D float2 level_features2(const float* __restrict__ table, const LevelCell& 
   return make_float2(x0, x1);
 }
 
+// The same features with paired gathers: corners (x, y, z) and (x+1, y, z)
+// hash to slots h and h ^ 1 when x is even (x + 1 = x ^ 1, the mask keeps
+// bit 0), i.e. one aligned 16-byte slot pair; so the x-even corner pairs take
+// one 16-byte load each and the x-odd ones a 16-byte plus an 8-byte load.
+// Measured on B200 (tools/l2_gather_peak.cu): a random 16-byte L2 gather
+// costs 1.25x an 8-byte one, so a level costs 5 (even x) or 9 (odd x) load
+// units instead of 8.  The table must be 16-byte aligned.  Same values, same
+// f32 accumulation order as level_features2.
+NIRC_D float2 level_features2_pairs(const float* __restrict__ table, const LevelCell& c,
+                                    uint32_t mask) {
+  const float4* t4 = reinterpret_cast<const float4*>(table);
+  const float2* t2 = reinterpret_cast<const float2*>(table);
+  const bool even = (c.ix & 1) == 0;
+  float2 g[8];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t h0 = corner_hash(c, 2 * q, mask);
+    const float4 A = __ldg(t4 + (h0 >> 1));
+    const bool hi = (h0 & 1u) != 0u;
+    g[2 * q] = hi ? make_float2(A.z, A.w) : make_float2(A.x, A.y);
+    if (even) g[2 * q + 1] = hi ? make_float2(A.x, A.y) : make_float2(A.z, A.w);
+    else g[2 * q + 1] = __ldg(t2 + corner_hash(c, 2 * q + 1, mask));
+  }
+  float x0 = 0.0f, x1 = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float w = corner_weight(c, k);
+    x0 = __fadd_rn(x0, __fmul_rn(w, g[k].x));
+    x1 = __fadd_rn(x1, __fmul_rn(w, g[k].y));
+  }
+  return make_float2(x0, x1);
+}
+
 // Dense shared-memory copies of the coarse levels (feats == 2).  Level l's
 // cell coordinates lie in [0, res_l] and its corners in [0, res_l + 1], so a
 // dense (res_l + 2)^3 array indexed by (z, y, x) holds every slot the level
@@ -233,6 +266,7 @@ NIRC_D float2 level_features2(const float* __restrict__ table, const LevelCell& 
 // values, gathered from shared memory instead of scattered L2 lines.
 struct DenseLevels {
   int n;                          // levels 0..n-1 are dense
+  int pairs;                      // sparse levels: paired 16-byte gathers (aligned table)
   int R[NIRC_MAX_LEVELS];         // res + 2
   int off[NIRC_MAX_LEVELS + 1];   // float2 offsets; off[n] = total entries
 };

@@ -56,6 +56,7 @@ __global__ void k_pack_weights(nirc_spec_t sp, TcNet net, const float* __restric
 constexpr int kL = 12, kF = 2, kBands = 4, kIn = 47, kK0 = 48;
 constexpr int kDenseLevels = 4;  // dense coarse levels of the cfg2 kernel (measured best)
 
+
 __host__ __device__ inline bool is_default_layout(const nirc_spec_t& sp) {
   return sp.levels == kL && sp.feats == kF && sp.bands == kBands && sp.in_dim == kIn &&
          sp.dims[0] == kIn;
@@ -68,7 +69,7 @@ __host__ __device__ inline bool is_default_layout(const nirc_spec_t& sp) {
 // 5e-7 abs in fp32 (F32SH = true).  Levels < ND are
 // gathered from the CTA's dense shared-memory copies, the rest from the
 // L2-resident tables.
-template <int ND, bool F32SH>
+template <int ND, bool F32SH, bool kPairs = false>
 __device__ __forceinline__ void encode_default(const nirc_spec_t& sp,
                                                const float* __restrict__ theta, const double* p,
                                                const double* nrm, const double* alb,
@@ -84,7 +85,8 @@ __device__ __forceinline__ void encode_default(const nirc_spec_t& sp,
     // ND is a compile-time count: the 12 levels stay straight-line code and
     // the gathers of all levels overlap in flight
     const float2 f = lvl < ND ? level_features2_dense(dense + dl.off[lvl], dl.R[lvl], c)
-                              : level_features2(theta + (size_t)lvl * T * kF, c, T - 1u);
+                     : (kPairs ? level_features2_pairs(theta + (size_t)lvl * T * kF, c, T - 1u)
+                               : level_features2(theta + (size_t)lvl * T * kF, c, T - 1u));
     x[2 * lvl] = f.x;
     x[2 * lvl + 1] = f.y;
   }
@@ -103,7 +105,7 @@ __device__ __forceinline__ void encode_default(const nirc_spec_t& sp,
   x[47] = 0.0f;
 }
 
-template <class P, int NG, int ND>
+template <class P, int NG, int ND, bool kPairs = false>
 __global__ void __launch_bounds__(NG * 128, 1)
     k_full_forward_tc(nirc_spec_t sp, tc::TcNet net, tc::TcSmem L,
                       const float* __restrict__ theta, const uint8_t* __restrict__ wimg,
@@ -137,8 +139,8 @@ __global__ void __launch_bounds__(NG * 128, 1)
     const int64_t row = tile * tc::kTileRows + tg;
     float x[kK0];
     if (row < n) {
-      encode_default<ND, false>(sp, theta, pos + 3 * row, nrm + 3 * row, alb + 3 * row,
-                                rough[row], dirs + 3 * row, x, dl, dense);
+      encode_default<ND, false, kPairs>(sp, theta, pos + 3 * row, nrm + 3 * row, alb + 3 * row,
+                                        rough[row], dirs + 3 * row, x, dl, dense);
     } else {
 #pragma unroll
       for (int k = 0; k < kK0; ++k) x[k] = 0.0f;
@@ -332,6 +334,9 @@ static int full_forward_impl(const nirc_spec_t* spec, const float* theta, const 
   const uint32_t base_total = tc::tc_smem_layout(net, ng, 0).total;
   DenseLevels dl = dense_levels_for(*spec, 227u * 1024u - 1024u - base_total, nd_want);
   if (dl.n != 0 && dl.n != 4 && dl.n != 5) dl = dense_levels_for(*spec, 0, 0);
+  // paired 16-byte gathers need 16-byte aligned level tables (NIRC_PAIRS=0: 8-byte only)
+  dl.pairs = (reinterpret_cast<uintptr_t>(theta) & 15u) == 0;
+  if (const char* e = getenv("NIRC_PAIRS")) dl.pairs = dl.pairs && atoi(e) != 0;
   const tc::TcSmem L = tc::tc_smem_layout(net, ng, (uint32_t)dl.off[dl.n] * 8u);
   const int64_t want = (ntiles + ng - 1) / ng;
   const int grid = (int)(want < sm_count() ? want : sm_count());
@@ -343,7 +348,9 @@ static int full_forward_impl(const nirc_spec_t* spec, const float* theta, const 
     return NIRC_OK;
   };
   if (prec == tc::PrecF16x2::kId) {
-    if (ng == 4 && dl.n == 5) st = launch(k_full_forward_tc<tc::PrecF16x2, 4, 5>, 512);
+    if (ng == 4 && dl.n == 4 && dl.pairs)
+      st = launch(k_full_forward_tc<tc::PrecF16x2, 4, 4, true>, 512);
+    else if (ng == 4 && dl.n == 5) st = launch(k_full_forward_tc<tc::PrecF16x2, 4, 5>, 512);
     else if (ng == 4 && dl.n == 4) st = launch(k_full_forward_tc<tc::PrecF16x2, 4, 4>, 512);
     else if (ng == 4) st = launch(k_full_forward_tc<tc::PrecF16x2, 4, 0>, 512);
     else if (ng == 3) st = launch(k_full_forward_tc<tc::PrecF16x2, 3, 0>, 384);

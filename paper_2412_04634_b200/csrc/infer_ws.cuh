@@ -307,6 +307,7 @@ __global__ void __launch_bounds__((ws::kChainGroups + NP) * 128, 1)
     if (tg < S) s_vf[tg].unsafe = 0;  // (ordered by the loop's first barrier)
     const uint32_t pbar = 1 + NG + p;
     const uint32_t T = 1u << sp.table_log2;
+    const bool pairs = (reinterpret_cast<uintptr_t>(theta) & 15u) == 0;  // 16-byte slot pairs
     const int j = tg / R, k = tg % R;
     // asynchronous copy of a tile's records (8-byte cp.async per word)
     auto fetch = [&](int64_t i, int buf) {
@@ -361,7 +362,8 @@ __global__ void __launch_bounds__((ws::kChainGroups + NP) * 128, 1)
         const float uy = norm_coord(r.pos[1], sp.bb_min[1], sp.bb_inv[1]);
         const float uz = norm_coord(r.pos[2], sp.bb_min[2], sp.bb_inv[2]);
         const LevelCell c = level_cell(ux, uy, uz, sp.res[lvl]);
-        const float2 f = level_features2(theta + (size_t)lvl * T * 2, c, T - 1u);
+        const float2 f = pairs ? level_features2_pairs(theta + (size_t)lvl * T * 2, c, T - 1u)
+                               : level_features2(theta + (size_t)lvl * T * 2, c, T - 1u);
         s_feat[jj * 24 + 2 * lvl] = f.x;
         s_feat[jj * 24 + 2 * lvl + 1] = f.y;
       }
