@@ -224,11 +224,13 @@ __device__ __forceinline__ void ws_wait_sleep(uint32_t mbar, uint32_t parity) {
   }
 }
 
-template <int NP, bool kProbe>
-__global__ void __launch_bounds__((ws::kChainGroups + NP) * 128, 1)
+// Four chain groups, one TMEM slot each.  (Measured alternative, not kept:
+// two groups alternating between two slots each, "ping-pong", 5.60 vs 5.31
+// ms per 1080p render.)
+template <int NP, bool kProbe, int NG = 4>
+__global__ void __launch_bounds__((NG + NP) * 128, 1)
     k_infer_ws(nirc_spec_t sp, tc::TcNet net, ws::Layout L, const float* __restrict__ theta,
                const uint8_t* __restrict__ wimg, const float* __restrict__ bias_g, InferArgs a) {
-  constexpr int NG = ws::kChainGroups;
   constexpr int NS = ws::kSlots;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t s0 = tc::smem_u32(smem);
@@ -292,7 +294,7 @@ __global__ void __launch_bounds__((ws::kChainGroups + NP) * 128, 1)
 
   if (role >= NG) {
     // ------------------------------------------------------- producer ---
-    if constexpr (ws::kProdRegs<NP> > 0)
+    if constexpr (NG == 4 && ws::kProdRegs<NP> > 0)
       asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(ws::kProdRegs<NP>));
     const int p = role - NG;
     uint8_t* pbase = smem + L.prod_off + p * L.prod_bytes;
@@ -512,8 +514,9 @@ __global__ void __launch_bounds__((ws::kChainGroups + NP) * 128, 1)
     asm volatile("cp.async.wait_group 0;" ::: "memory");
   } else {
     // ----------------------------------------------------------- chain ---
-    if constexpr (ws::kChainRegs<NP> > 0)
+    if constexpr (NG == 4 && ws::kChainRegs<NP> > 0)
       asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(ws::kChainRegs<NP>));
+    {
     const int g = role;  // = the group's TMEM slot
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     const uint32_t tmem_d = tmem_base + g * tc::kTsColsPerGroup;
@@ -693,6 +696,7 @@ __global__ void __launch_bounds__((ws::kChainGroups + NP) * 128, 1)
       ws::mbar_arrive(full + 8 * (2 + b));  // mempty[b]: every chain thread is done with it
       if (kProbe && pb) pb[8] = clock64();
     }
+  }
   }
   tc::fence_before();
   __syncthreads();
