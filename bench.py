@@ -717,6 +717,18 @@ def run_b200(args, rank, world, local_rank):
                    "peak_per_sm_cycle": pk, "frac": ach / pk,
                    "source": "profiles/full_forward_traffic.json (ncu) + live launch time "
                              "and SM clock"}
+    # the measured random-gather peak of this pool's B200s (tools/l2_gather_peak.cu):
+    # the hash-table slots levels 4-11 read from L2 per second against it
+    l2peak = prof.get("l2_gather_peak") or {}
+    l2_vs_peak = None
+    if l2peak.get("slots_per_s_8B"):
+        slots = n / (avg_launch_ms * 1e-3) * float(prof.get("l2_slots_per_query", 64))
+        l2_vs_peak = {"slots_per_s": slots, "peak_slots_per_s_8B": l2peak["slots_per_s_8B"],
+                      "frac": slots / l2peak["slots_per_s_8B"],
+                      "note": "x-even corner pairs share one 16-byte load (2 slots), so the "
+                              "kernel can exceed the 8-byte-gather peak; the paired-load peak "
+                              "is " + f"{l2peak.get('pairs_per_s_16B', 0):.3g} loads/s",
+                      "source": l2peak.get("source")}
     line = {
         "metric": "nirc_queries_per_sec", "value": value, "unit": "queries/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -733,7 +745,7 @@ def run_b200(args, rank, world, local_rank):
                      "tensor_frac": tflops / float(peaks.get("bf16_tflops", 1590.0)),
                      "l2_gather_gbs": l2_gbs,
                      "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
-                     "binding_resource": binding},
+                     "binding_resource": binding, "l2_gather_vs_measured_peak": l2_vs_peak},
         "clocks": csum,
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps,
