@@ -43,6 +43,7 @@ template <int NP> constexpr int kProdRegs = NP == 1 ? 128 : (NP == 2 ? 96 : 0);
 // Per-vertex data the combine needs (vertex_result), written by the producer.
 struct VMeta {
   double T[3], Tp[3];
+  double inv;  // 1 / ncq (the reference's 1.0 / N_c, computed once by the producer)
   int64_t slot;
   int32_t ncq, has_res, nrc, pad;
 };
@@ -499,6 +500,7 @@ __global__ void __launch_bounds__((NG + NP) * 128, 1)
         m.has_res = r.has_res;
         m.nrc = r.nrc;
         m.pad = 0;
+        m.inv = r.ncq > 0 ? 1.0 / r.ncq : 0.0;
         vm[tg] = m;
       }
       int* pflag = reinterpret_cast<int*>(meta + 128 * 32 + S * sizeof(ws::VMeta));
@@ -545,10 +547,14 @@ __global__ void __launch_bounds__((NG + NP) * 128, 1)
       if (warp == 0) {
         tc::fence_after();
         if (tc::elect_one()) {
+          long long* tl = (kProbe && blockIdx.x == 0 && n < 32) ? a.dbg + 4096 + g * 512 + n * 16
+                                                               : nullptr;
+          if (kProbe && tl) tl[0] = clock64();
           ws::mma_bias<64>(tmem_d, b_img, b_img + 4096);
           ws::issue_layer0_ss(w_base + s_woff[0], a_hi, a_hi + ws::kASlotBytes / 2, tmem_d);
           tc::mma_commit(mbar);
           tc::mma_commit(full + 8);  // aempty: the A slot is free once layer 0 completes
+          if (kProbe && tl) tl[1] = clock64();
         }
         __syncwarp();
       }
@@ -579,6 +585,9 @@ __global__ void __launch_bounds__((NG + NP) * 128, 1)
         // one warp observes the layer's completion, the barrier releases the group
         if (warp == 0) tc::mbar_wait(mbar, phase);
         phase ^= 1u;
+        long long* tl = (kProbe && blockIdx.x == 0 && n < 32) ? a.dbg + 4096 + g * 512 + n * 16
+                                                             : nullptr;
+        if (kProbe && tl && tg == 0) tl[2 + 3 * l] = clock64();
         tc::named_bar_sync(gbar, 128);
         tc::fence_after();
         if (kProbe && pb) pb[2 + l] = clock64();
@@ -605,6 +614,7 @@ __global__ void __launch_bounds__((NG + NP) * 128, 1)
           if (warp == 0) {
             tc::fence_after();
             if (tc::elect_one()) {
+              if (kProbe && tl) tl[3 + 3 * l] = clock64();
               const uint32_t wl = w_base + s_woff[l + 1];
               const uint32_t bl = b_img + 4096 + 2048u * (uint32_t)(l + 1);
               if (l + 1 == nl - 1) {
@@ -615,6 +625,7 @@ __global__ void __launch_bounds__((NG + NP) * 128, 1)
                 ws::issue_layer_ts<64, 64>(wl, tmem_d + 64, tmem_d + 96, tmem_d);
               }
               tc::mma_commit(mbar);
+              if (kProbe && tl) tl[4 + 3 * l] = clock64();
             }
             __syncwarp();
           }
@@ -657,34 +668,23 @@ __global__ void __launch_bounds__((NG + NP) * 128, 1)
       const int64_t v0 = tile * S;
       const int nv = (int)((nverts - v0) < S ? (nverts - v0) : S);
       const ws::VMeta* vm = reinterpret_cast<const ws::VMeta*>(meta + 128 * 32);
-      if (tg < nv && a.ablate == 0) {
-        const ws::VMeta& r = vm[tg];
-        const double* rows = reinterpret_cast<const double*>(meta) + 4 * (tg * R);
-        double o[3];
+      // (vertex, channel) items on warps 1-3 (warp 0 goes on to the next
+      // layer-0 completion): the k-ordered f64 sum of cache_lc_s per channel
+      const double* md = reinterpret_cast<const double*>(meta);
+      for (int ct = tg - 32; ct >= 0 && ct < 3 * nv && a.ablate == 0; ct += 96) {
+        const int v = ct / 3, ch = ct - 3 * v;
+        const ws::VMeta& r = vm[v];
+        const double* rows = md + 4 * (v * R) + ch;
+        double o;
         if (r.nrc) {
-          o[0] = r.T[0] * rows[0];
-          o[1] = r.T[1] * rows[1];
-          o[2] = r.T[2] * rows[2];
+          o = r.T[ch] * rows[0];
         } else {
-          double sr = 0.0, sg = 0.0, sb = 0.0;
-          for (int c = 0; c < r.ncq; ++c) {
-            sr += rows[4 * c];
-            sg += rows[4 * c + 1];
-            sb += rows[4 * c + 2];
-          }
-          const double inv = 1.0 / r.ncq;
-          o[0] = r.T[0] * (sr * inv);
-          o[1] = r.T[1] * (sg * inv);
-          o[2] = r.T[2] * (sb * inv);
-          if (r.has_res) {
-            o[0] -= r.Tp[0] * rows[4 * r.ncq];
-            o[1] -= r.Tp[1] * rows[4 * r.ncq + 1];
-            o[2] -= r.Tp[2] * rows[4 * r.ncq + 2];
-          }
+          double acc = 0.0;
+          for (int c = 0; c < r.ncq; ++c) acc += rows[4 * c];
+          o = r.T[ch] * (acc * r.inv);
+          if (r.has_res) o -= r.Tp[ch] * rows[4 * r.ncq];
         }
-        a.result[3 * r.slot] = o[0];
-        a.result[3 * r.slot + 1] = o[1];
-        a.result[3 * r.slot + 2] = o[2];
+        a.result[3 * r.slot + ch] = o;
       }
       if (tg == 0 && a.ablate == 0) {
         const int* pflag = reinterpret_cast<const int*>(meta + 128 * 32 + S * sizeof(ws::VMeta));
