@@ -267,6 +267,91 @@ def _full_forward_pipelined(spec, th, host, precision, out=None, chunk=None):
     return y_host
 
 
+_NP_STAGING = {}
+
+
+def _np_staging(m, dout):
+    """Two pinned staging sets (5 input columns + outputs) of m rows, reused."""
+    key = (m, dout)
+    st = _NP_STAGING.get(key)
+    if st is None:
+        widths = [3, 3, 3, 1, 3]
+        inp = [[torch.empty((m, w) if w > 1 else (m,), dtype=torch.float64, pin_memory=True)
+                for w in widths] for _ in range(2)]
+        ys = [torch.empty((m, dout), dtype=torch.float32, pin_memory=True) for _ in range(2)]
+        st = (inp, ys)
+        _NP_STAGING[key] = st
+    return st
+
+
+def _full_forward_numpy(spec, th, rows, precision, chunk=None):
+    """numpy (pageable) query rows, the reference's types: each chunk is
+    copied into a pinned staging buffer on the host (multi-threaded torch
+    copy) while the previous chunk's H2D copy, kernel and D2H copy run; the
+    outputs drain from pinned staging into the numpy result the same way.
+    Returns a fresh numpy (n, dout) f32 array."""
+    n = int(rows[0].shape[0])
+    dout = int(spec.dims[-1])
+    m = min(chunk or _PIPE_CHUNK, n)
+    inp, ys = _np_staging(m, dout)
+    y = np.empty((n, dout), np.float32)
+    cur = torch.cuda.current_stream()
+    s_in, s_out = _pipe_streams()
+    widths = [3, 3, 3, 1, 3]
+    dbuf = [[_dev.empty((m, w) if w > 1 else (m,), torch.float64) for w in widths]
+            for _ in range(2)]
+    ybuf = [_dev.empty((m, dout), torch.float32) for _ in range(2)]
+    ev_h2d = [torch.cuda.Event() for _ in range(2)]
+    ev_comp = [torch.cuda.Event() for _ in range(2)]
+    ev_d2h = [torch.cuda.Event() for _ in range(2)]
+    lib = _lib.load()
+    cs = _lib.make_c_spec(spec)
+    flags = _dev.zeros((1,), torch.int32)
+    s_in.wait_stream(cur)
+    pending = None  # (buffer, lo, hi) of the chunk whose outputs drain next
+    for k, lo in enumerate(range(0, n, m)):
+        hi = min(n, lo + m)
+        c = hi - lo
+        b = k % 2
+        if k >= 2:
+            ev_h2d[b].synchronize()  # the H2D copy of chunk k-2 has read staging b
+        for t, a in zip(inp[b], rows):
+            t[:c].copy_(torch.from_numpy(a[lo:hi]))
+        with torch.cuda.stream(s_in):
+            if k >= 2:
+                s_in.wait_event(ev_comp[b])  # the kernel of chunk k-2 read dbuf[b]
+            for d, t in zip(dbuf[b], inp[b]):
+                d[:c].copy_(t[:c], non_blocking=True)
+            ev_h2d[b].record(s_in)
+        cur.wait_event(ev_h2d[b])
+        if k >= 2:
+            cur.wait_event(ev_d2h[b])  # chunk k-2's outputs left ybuf[b]
+        st = lib.nirc_full_forward(cs, _dev.ptr(th), *[_dev.ptr(d) for d in dbuf[b]], c,
+                                   _dev.ptr(ybuf[b]), int(precision),
+                                   _dev.ptr(flags) if k == 0 else _dev.ptr(None), _dev.stream())
+        _lib.check(st, "nirc_full_forward")
+        ev_comp[b].record(cur)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(ev_comp[b])
+            ys[b][:c].copy_(ybuf[b][:c], non_blocking=True)
+            ev_d2h[b].record(s_out)
+        if pending is not None:  # drain the previous chunk while this one runs
+            pb, plo, phi = pending
+            ev_d2h[pb].synchronize()
+            y[plo:phi] = ys[pb][: phi - plo].numpy()
+        pending = (b, lo, hi)
+    pb, plo, phi = pending
+    ev_d2h[pb].synchronize()
+    y[plo:phi] = ys[pb][: phi - plo].numpy()
+    for b in range(2):
+        for d in dbuf[b]:
+            d.record_stream(s_in)
+        ybuf[b].record_stream(s_out)
+    cur.wait_stream(s_out)
+    _lib.check_flags(flags, "full_forward")
+    return y
+
+
 def query(spec, theta, surf, dirs, dir_to_surf, precision=PRECISION_F16X2):
     """Directions against shared surfaces (Cache._query, caches.py:211-233,
     batched): surf (n_s, 10) rows pos.xyz | ns.xyz | albedo.rgb | roughness,
@@ -321,6 +406,13 @@ def full_forward(spec, theta, pos, normal, albedo, rough, dirs, training=False,
         if is_default_layout(spec):
             return _full_forward_pipelined(spec, th, [r.contiguous() for r in rows], precision,
                                            out)
+    if (out is None and all(isinstance(r, np.ndarray) and r.dtype == np.float64 for r in rows)
+            and int(pos.shape[0]) >= (1 << 18)):
+        from .encoding import is_default_layout
+
+        if is_default_layout(spec):  # large numpy batches: staged, overlapped copies
+            return _full_forward_numpy(spec, th, [np.ascontiguousarray(r) for r in rows],
+                                       precision)
     args = [_dev.dev(a, torch.float64) for a in rows]
     n = int(args[0].shape[0])
     Y = _dev.empty((n, int(spec.dims[-1])), torch.float32)

@@ -147,6 +147,26 @@ def test_pinned_pipeline_matches_device_path(nb):
     assert np.array_equal(y_host, y_dev)
 
 
+def test_numpy_staged_path_matches_device_path(nb):
+    """Large numpy batches (the reference's types) stream through pinned
+    staging with overlapped copies: a fresh numpy result equal to the
+    device-resident call, over several chunks and a ragged tail."""
+    from paper_2412_04634_b200 import mlp
+
+    spec = mlp.make_spec(depth=2)
+    th_np = mlp.init_theta(spec, seed=1, out_scale=0.1)
+    n = 3 * (1 << 18) + 555
+    q = [np.ascontiguousarray(a) for a in O.measure_queries(n, seed=4)]
+    y_np = mlp.full_forward(spec, th_np, *q)  # >= 2^18 rows: the staged path
+    assert isinstance(y_np, np.ndarray) and y_np.shape == (n, 3)
+    th = torch.from_numpy(th_np).cuda()
+    dev = [torch.from_numpy(a).cuda() for a in q]
+    y_dev = mlp.full_forward(spec, th, *dev).cpu().numpy()
+    assert np.array_equal(y_np, y_dev)
+    y_small = mlp._full_forward_numpy(spec, th, q, 2, chunk=1 << 16)  # many chunks
+    assert np.array_equal(y_small, y_dev)
+
+
 def test_query_amortised_bad_index_async(nb):
     """nirc_query encodes each surface once; a bad surface index is reported
     through the device status word (ConfigError at the result read) and the
