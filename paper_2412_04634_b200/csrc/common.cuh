@@ -116,44 +116,39 @@ NIRC_D void sh_eval(double x, double y, double z, int bands,
 
 // Real SH (bands = 4), the scalar-path recurrences of sh.py:36-76 in fp32.
 // sh_k may be the spec's f64 table or its f32 rounding (the same values).
+// Closed form of the scalar-path recurrences (sh.py:36-76, no Condon-Shortley
+// phase): out[l^2 + l +- m] = K_lm * Pt_lm(z) * Re / Im (x + i y)^m with
+// Pt_lm = P_lm / s^m the polynomial the recurrence builds -- no sqrt or
+// division; within an ulp or two of the fp32 recurrence.
 template <class KT>
 NIRC_D void sh4_f32(float x, float y, float z, const KT* sh_k, float* out) {
-  const float s = sqrtf(x * x + y * y);
-  float cphi = 1.0f, sphi = 0.0f;
-  if (s > 0.0f) {
-    const float inv = 1.0f / s;
-    cphi = x * inv;
-    sphi = y * inv;
-  }
-  float cm = 1.0f, sm = 0.0f, pmm = 1.0f;
-#pragma unroll
-  for (int m = 0; m < 4; ++m) {
-    if (m > 0) {
-      pmm = pmm * ((2.0f * m - 1.0f) * s);
-      const float cn = cm * cphi - sm * sphi;
-      const float sn = sm * cphi + cm * sphi;
-      cm = cn;
-      sm = sn;
-    }
-    float p2 = 0.0f, p1 = 0.0f;
-#pragma unroll
-    for (int l = m; l < 4; ++l) {
-      float p;
-      if (l == m) p = pmm;
-      else if (l == m + 1) p = z * (2.0f * m + 1.0f) * pmm;
-      else p = ((2.0f * l - 1.0f) * z * p1 - (l + m - 1.0f) * p2) * (1.0f / (float)(l - m));
-      p2 = p1;
-      p1 = p;
-      const int base = l * l + l;
-      if (m == 0) {
-        out[base] = (float)sh_k[l * 8] * p;
-      } else {
-        const float kk = (float)sh_k[l * 8 + m] * p;
-        out[base + m] = kk * cm;
-        out[base - m] = kk * sm;
-      }
-    }
-  }
+  const float z2 = z * z;
+  const float c2 = x * x - y * y, s2 = 2.0f * x * y;     // (x + i y)^2
+  const float c3 = x * c2 - y * s2, s3 = x * s2 + y * c2;  // (x + i y)^3
+  const float p20 = 1.5f * z2 - 0.5f;
+  const float p30 = z * (2.5f * z2 - 1.5f);
+  const float p31 = 7.5f * z2 - 1.5f;
+  out[0] = (float)sh_k[0];
+  out[2] = (float)sh_k[8] * z;
+  out[3] = (float)sh_k[9] * x;
+  out[1] = (float)sh_k[9] * y;
+  out[6] = (float)sh_k[16] * p20;
+  const float k21 = (float)sh_k[17] * (3.0f * z);
+  out[7] = k21 * x;
+  out[5] = k21 * y;
+  const float k22 = (float)sh_k[18] * 3.0f;
+  out[8] = k22 * c2;
+  out[4] = k22 * s2;
+  out[12] = (float)sh_k[24] * p30;
+  const float k31 = (float)sh_k[25] * p31;
+  out[13] = k31 * x;
+  out[11] = k31 * y;
+  const float k32 = (float)sh_k[26] * (15.0f * z);
+  out[14] = k32 * c2;
+  out[10] = k32 * s2;
+  const float k33 = (float)sh_k[27] * 15.0f;
+  out[15] = k33 * c3;
+  out[9] = k33 * s3;
 }
 
 // ----------------------------------------------------------- hash grid ---
