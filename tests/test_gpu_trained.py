@@ -219,7 +219,8 @@ def test_two_level_render_trained_cache(nb, golden, tag, depth):
         np.testing.assert_allclose(r.image, ref, rtol=1e-3, atol=1e-4 * max(1.0, ref.max() / 17))
 
 
-def test_render_fp16_range_guard(nb, golden):
+@pytest.mark.parametrize("nc", [8, 16])  # nc = 16: the warp-specialised kernel (k_infer_ws)
+def test_render_fp16_range_guard(nb, golden, nc):
     """The range-stress net in the two-level frame: the 2xFP16 inference
     kernel flags the tiles and k_infer_fix recomputes them; the image
     equals the 3xTF32 render (fp32 range) to the network tolerance."""
@@ -238,14 +239,15 @@ def test_render_fp16_range_guard(nb, golden):
     th[int(spec.w_off[0]): int(spec.b_off[0]) + int(spec.dims[1])] *= s
     th[int(spec.w_off[-1]):] *= np.float32(1.0) / s
     cache.theta.copy_(torch.from_numpy(th))
-    cfg = EstimatorConfig(mode="two-level", nc=(8,), max_cache_vertices=1)
+    cfg = EstimatorConfig(mode="two-level", nc=(nc,), max_cache_vertices=1)
     r2 = render(sc, cfg, cache=cache, seed=3, spp=1, precision=2)
     r0 = render(sc, cfg, cache=cache, seed=3, spp=1, precision=0)
     assert np.all(np.isfinite(r2.image))
     np.testing.assert_allclose(r2.image, r0.image, rtol=1e-3, atol=1e-4)
 
 
-def test_concurrent_renders_on_two_streams(nb):
+@pytest.mark.parametrize("nc", [8, 16])
+def test_concurrent_renders_on_two_streams(nb, nc):
     """parameters are read-only snapshots, callable
     concurrently: two caches with different theta render (and run the fused
     forward) at the same time on two streams, device-resident, no host sync
@@ -260,7 +262,7 @@ def test_concurrent_renders_on_two_streams(nb):
     c1 = Cache.create("nirc", sc, seed=1, init="random")
     c2 = Cache.create("nirc", sc, seed=2, init="random")
     c2.theta.mul_(1.5)
-    cfg = EstimatorConfig(mode="two-level", nc=(8,), max_cache_vertices=1)
+    cfg = EstimatorConfig(mode="two-level", nc=(nc,), max_cache_vertices=1)
     q = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in O.measure_queries(1 << 16, 5)]
 
     def run(c):
@@ -279,3 +281,24 @@ def test_concurrent_renders_on_two_streams(nb):
         for got, want in ((r1, ser[0]), (r2, ser[1])):
             for a, b in zip(got, want):
                 assert np.array_equal(a.cpu().numpy(), b), rep
+
+
+@pytest.mark.parametrize("depth", [2, 4])
+def test_warp_specialised_inference_matches_grouped_kernel(nb, depth, monkeypatch):
+    """k_infer_ws (producer warpgroups + four chain groups, the default for
+    nc >= 8 where its shared-memory plan fits) against the grouped k_infer_tc
+    (NIRC_INFER_NP=0) on the same frame: same walks, the same deferred
+    vertices and pixels within the two splits' rounding."""
+    from paper_2412_04634_b200.caches import Cache
+    from paper_2412_04634_b200.estimators import EstimatorConfig, render
+
+    sc = __import__("paper_2412_04634_b200.scene", fromlist=["load_builtin"]).load_builtin(
+        "cornell").with_resolution(128, 96)
+    cache = Cache.create("nirc", sc, seed=7, init="random", depth=depth)
+    cfg = EstimatorConfig(mode="two-level", nc=(16,), max_cache_vertices=1)
+    ws = render(sc, cfg, cache=cache, seed=2, spp=2, precision=2)
+    monkeypatch.setenv("NIRC_INFER_NP", "0")
+    grouped = render(sc, cfg, cache=cache, seed=2, spp=2, precision=2)
+    assert np.array_equal(ws.path_length, grouped.path_length)
+    assert ws.queries == grouped.queries > 0
+    np.testing.assert_allclose(ws.image, grouped.image, rtol=1e-5, atol=1e-7)
