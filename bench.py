@@ -645,6 +645,33 @@ def run_b200(args, rank, world, local_rank):
         y_np = full_forward(spec, theta_np, *host_np, precision=PRECISION)
     np_s = time.perf_counter() - t0w
     assert isinstance(y_np, np.ndarray)
+    # the PCIe roofline of the pinned e2e path: the same bytes as plain pinned
+    # copies (H2D of the five input columns while D2H of the outputs runs on
+    # a second stream), CUDA events, best of 3
+    pcie_ms = []
+    d_in = [torch.empty_like(h, device="cuda") for h in host]
+    d_out = torch.empty((n, 3), dtype=torch.float32, device="cuda")
+    s_d2h = torch.cuda.Stream()
+    for _ in range(3):
+        barrier()
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        s_d2h.wait_stream(stream)
+        with torch.cuda.stream(s_d2h):
+            y_host.copy_(d_out, non_blocking=True)
+        for d, h in zip(d_in, host):
+            d.copy_(h, non_blocking=True)
+        stream.wait_stream(s_d2h)
+        p1.record(stream)
+        torch.cuda.synchronize()
+        pcie_ms.append(p0.elapsed_time(p1))
+    del d_in, d_out
+    pcie_best = min(pcie_ms)
+    e2e_pcie = {"copy_only_ms": pcie_best,
+                "h2d_gbs": h2d / (pcie_best * 1e-3) / 1e9,
+                "e2e_frac_of_copy_only": (pcie_best * 1e-3) / (float(e_ms.item()) * 1e-3
+                                                               / e2e_steps),
+                "note": "the pinned e2e step against copying the same bytes alone: its bound"}
     e2e_numpy = {"value": world * n * np_steps / np_s, "unit": "queries/s", "steps": np_steps,
                  "h2d_bytes_per_step": h2d + theta_np.nbytes, "d2h_bytes_per_step": d2h,
                  "path": "paper_2412_04634_b200.mlp.full_forward on numpy arrays (pageable host "
@@ -758,7 +785,7 @@ def run_b200(args, rank, world, local_rank):
                                  "the per-step median is given beside it",
                 "path": "paper_2412_04634_b200.mlp.full_forward on pinned host tensors (chunked "
                         "H2D / fused kernel / D2H pipeline inside the call)",
-                "numpy_caller": e2e_numpy},
+                "numpy_caller": e2e_numpy, "pcie_roofline": e2e_pcie},
         "gpu_launches": 2 * args.steps,
     }
     if fb is not None:
