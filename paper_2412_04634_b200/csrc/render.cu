@@ -818,8 +818,10 @@ __device__ inline void lambert_row(const LambertFrame& F, uint64_t key, int64_t 
                                    float* w, double* s_out, int* kind) {
   const float u1 = rand_uniform_f32(key, base + OFF_CACHE + 2 * k);
   const float u2 = rand_uniform_f32(key, base + OFF_CACHE + 2 * k + 1);
+  // fast-math sampler: the directions feed the network input and the
+  // Lambert weight only (hardware sin / cos of 2 pi u2 to ~1e-6 absolute)
   float sp, cp;
-  sincospif(2.0f * u2, &sp, &cp);
+  __sincosf(6.28318530717958647692f * u2, &sp, &cp);
   const float rr = sqrtf(u1);
   const float lx = rr * cp, ly = rr * sp;
   const float lz = sqrtf(fmaxf(0.0f, 1.0f - u1));
@@ -833,7 +835,7 @@ __device__ inline void lambert_row(const LambertFrame& F, uint64_t key, int64_t 
   const float ci = w[0] * F.nx + w[1] * F.ny + w[2] * F.nz;
   if (ci <= 0.0f) return;
   *kind = 1;
-  *s_out = (double)(ci / pdf);
+  *s_out = (double)__fdividef(ci, pdf);
 }
 
 // fp32 producer for the amortised inference rows (render path only; the
