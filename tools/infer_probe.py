@@ -3,6 +3,8 @@ import ctypes as C
 import os
 import sys
 
+os.environ.setdefault("NIRC_INFER_NP", "0")  # these stamps are k_infer_tc's (grouped kernel)
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
