@@ -188,3 +188,37 @@ def test_query_zero_cache_and_amortization(box):
     singles = np.vstack([cache.nirc_query(it, d[None, :]) for d in dirs])
     assert np.array_equal(batch, singles)
     assert np.array_equal(cache.nrc_query(it, dirs[0]), batch[0])
+
+
+def test_render_stage_timer():
+    """nirc_stage_timing / nirc_stage_times (the bench's per-stage device
+    times): after a timed render the three stages are positive and add up to
+    about the launch set's duration."""
+    import ctypes
+
+    import torch
+
+    from paper_2412_04634_b200 import _lib
+    from paper_2412_04634_b200.caches import Cache
+    from paper_2412_04634_b200.estimators import EstimatorConfig, render_device
+    from paper_2412_04634_b200.scene import load_builtin
+
+    lib = _lib.load()
+    sc = load_builtin("cornell").with_resolution(128, 96)
+    cache = Cache.create("nirc", sc, seed=1, init="random")
+    cfg = EstimatorConfig(mode="two-level", nc=(16,), max_cache_vertices=1)
+    render_device(sc, cfg, cache, seed=1)
+    _lib.check(lib.nirc_stage_timing(1), "nirc_stage_timing")
+    try:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        render_device(sc, cfg, cache, seed=1)
+        e1.record()
+        torch.cuda.synchronize()
+        buf = (ctypes.c_float * 3)()
+        _lib.check(lib.nirc_stage_times(buf, 3), "nirc_stage_times")
+    finally:
+        lib.nirc_stage_timing(0)
+    ms = list(buf)
+    assert all(v > 0.0 for v in ms), ms
+    assert sum(ms) <= e0.elapsed_time(e1) * 1.05 + 0.05
