@@ -357,6 +357,9 @@ class ShardedFramePipeline:
         self.theta_r = torch.empty_like(cache.theta)
         self.pending = None  # (frame, callable -> this rank's Records of that frame)
         self.train_events = None
+        from .frame import ZeroWatch
+
+        self.zero = ZeroWatch(cache)
 
     def _count(self, scene):
         from .caches import default_train_count
@@ -388,15 +391,17 @@ class ShardedFramePipeline:
         self.theta_r.copy_(cache.theta)
         snap = torch.cuda.Event()
         snap.record(self.s_render)
+        zero = self.zero.get()
         if same_geometry:
             img, img2, term, q, nxt = render_and_collect(
                 scene, self.config, cache, self.seed, self.spp, frame, count=count,
                 train_frame=frame + 1, rows=rows, paths=paths, out=out, theta=self.theta_r,
-                defer=True)
+                defer=True, zero=zero)
             self.pending = (frame + 1, nxt)
         else:
             img, img2, term, q = render_device(scene, self.config, cache, self.seed, self.spp,
-                                               frame, rows=rows, out=out, theta=self.theta_r)
+                                               frame, rows=rows, out=out, theta=self.theta_r,
+                                               zero=zero)
         stats = {"rows": rows, "queries": q}
         self.train_events = None
         self.s_train.wait_event(snap)  # theta_f copied; this frame's records complete
@@ -409,6 +414,7 @@ class ShardedFramePipeline:
                 stats["trace"] = train_frame_sharded(cache, rec, comm, self.steps, self.batch,
                                                      self.ops)
             t1.record(self.s_train)
+            self.zero.after_update(self.s_train)
         self.train_events = (t0, t1)
         return (img, img2, term), rows, stats
 

@@ -140,7 +140,7 @@ def _v1_device(v1_map, w, h):
 
 
 def render_device(scene, config=None, cache=None, seed=0, spp=1, frame=0, force_cache=False,
-                  rows=None, out=None, precision=None, v1_map=None, theta=None):
+                  rows=None, out=None, precision=None, v1_map=None, theta=None, zero=None):
     """Device-resident render: returns (img, img2, term, queries) CUDA
     tensors of sums (callers divide by spp).  ``rows`` renders a band of
     pixel rows (multi-GPU tiles); ``out`` accumulates into given buffers;
@@ -152,7 +152,8 @@ def render_device(scene, config=None, cache=None, seed=0, spp=1, frame=0, force_
     mode = MODES[config.mode]
     w, h = int(scene.camera[14]), int(scene.camera[15])
     cache_on = 0
-    if mode >= 1 and cache is not None and (force_cache or not _is_zero(cache, theta)):
+    if mode >= 1 and cache is not None and (
+            force_cache or not (zero if zero is not None else _is_zero(cache, theta))):
         cache_on = 1
     v1 = _v1_device(v1_map, w, h) if mode in (3, 4) else None
     cfg = _c_cfg(config, scene, spp, seed, frame, cache_on, rows, precision, v1)
@@ -179,7 +180,7 @@ def render_device(scene, config=None, cache=None, seed=0, spp=1, frame=0, force_
 
 def render_and_collect(scene, config, cache, seed=0, spp=1, frame=0, count=None,
                        train_frame=None, rows=None, paths=None, out=None, precision=None,
-                       theta=None, defer=False):
+                       theta=None, defer=False, zero=None):
     """render_device + cache.collect of the same frame in ONE device pass
     (C ABI nirc_render_collect: the training walks are the first work items
     of the persistent path tracer).  Equivalent to calling render_device and
@@ -202,7 +203,11 @@ def render_and_collect(scene, config, cache, seed=0, spp=1, frame=0, count=None,
         train_frame = frame
     p0, p1 = (0, int(count)) if paths is None else (int(paths[0]), int(paths[1]))
     w, h = int(scene.camera[14]), int(scene.camera[15])
-    cache_on = 1 if (mode >= 1 and not _is_zero(cache, theta)) else 0
+    # ``zero``: the caller already knows Cache.is_zero of the parameters
+    # (the frame pipelines read it asynchronously after training)
+    if zero is None:
+        zero = _is_zero(cache, theta)
+    cache_on = 1 if (mode >= 1 and not zero) else 0
     cfg = _c_cfg(config, scene, spp, seed, frame, cache_on, rows, precision)
     lib = _lib.load()
     ds = scene.device()

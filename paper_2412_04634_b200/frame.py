@@ -50,6 +50,32 @@ def config3(nc=(16,)):
     return EstimatorConfig(mode="two-level", nc=tuple(nc), max_cache_vertices=len(nc))
 
 
+class ZeroWatch:
+    """Cache.is_zero (caches.py:206-209) of a cache whose parameters change
+    only through the pipeline's training: after each update the check runs on
+    the device and lands in pinned memory asynchronously, so the next frame
+    reads it without a host sync (None -> the caller checks synchronously)."""
+
+    def __init__(self, cache):
+        self.cache = cache
+        self.host = torch.zeros((1,), dtype=torch.bool).pin_memory()
+        self.ev = None
+        self.value = None
+
+    def after_update(self, stream):
+        lo = int(self.cache.spec.w_off[-1])
+        nz = torch.any(self.cache.theta[lo:] != 0)
+        self.host.copy_(nz.reshape(1), non_blocking=True)
+        self.ev = torch.cuda.Event()
+        self.ev.record(stream)
+        self.value = None
+
+    def get(self):
+        if self.value is None and self.ev is not None and self.ev.query():
+            self.value = not bool(self.host[0])
+        return self.value
+
+
 class FramePipeline:
     """The same frame loop with rendering and training overlapped (SURVEY.md
     8(e) "render(f) || collect + train(f) on separate streams, double-buffered
@@ -78,6 +104,7 @@ class FramePipeline:
         self.s_train = torch.cuda.Stream()
         self.theta_r = torch.empty_like(cache.theta)
         self.pending = None  # (frame, Records or callable) for the next train
+        self.zero = ZeroWatch(cache)
 
     def _count(self, scene):
         return default_train_count(scene, self.train_fraction)
@@ -102,16 +129,17 @@ class FramePipeline:
         self.theta_r.copy_(cache.theta)
         snap = torch.cuda.Event()
         snap.record(self.s_render)
+        zero = self.zero.get()
         if same_geometry:
             img, img2, term, queries, nxt_rec = render_and_collect(
                 scene, self.config, cache, self.seed, self.spp, frame,
                 count=self._count(scene), train_frame=frame + 1, out=out, theta=self.theta_r,
-                defer=True)
+                defer=True, zero=zero)
             self.pending = (frame + 1, nxt_rec)
         else:
             img, img2, term, queries = render_device(scene, self.config, cache, self.seed,
                                                      self.spp, frame, out=out,
-                                                     theta=self.theta_r)
+                                                     theta=self.theta_r, zero=zero)
         loss = math.nan
         self.train_events = None
         if len(rec):
@@ -121,6 +149,7 @@ class FramePipeline:
                 t0.record(self.s_train)
                 trace = train_frame(cache, rec, steps=self.steps, batch=self.batch)
                 t1.record(self.s_train)
+                self.zero.after_update(self.s_train)
             self.train_events = (t0, t1)
             loss = trace[-1]
         return (img, img2, term), FrameStats(int(queries.item()), len(rec), loss)
