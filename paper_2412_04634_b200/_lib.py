@@ -197,7 +197,8 @@ def load():
             _build.build(force=os.environ.get("NIRC_REBUILD") == "1")
         if not os.path.exists(LIB_PATH):
             raise RuntimeError(f"CUDA extension missing: {LIB_PATH}")
-        lib = C.CDLL(LIB_PATH)
+        # NIRC_LIB_PATH: another in-tree build of the same library (tools' A/B runs)
+        lib = C.CDLL(os.environ.get("NIRC_LIB_PATH", LIB_PATH))
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res
