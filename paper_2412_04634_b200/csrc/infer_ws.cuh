@@ -122,6 +122,21 @@ __device__ __forceinline__ void relu_split16(const float* h, uint32_t* hi, uint3
   }
 }
 
+// 2 layer-0 inputs (any sign) -> fp16x2 hi (the truncation) and lo =
+// fp16_rn(x - hi), as split8 below for one word.
+__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  asm("cvt.rz.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(x1), "f"(x0));
+  float l0, l1;
+  asm("{\n\t.reg .b16 h0, h1, m1;\n\t"
+      "mov.b32 {h0, h1}, %2;\n\t"
+      "mov.b16 m1, 0xBC00;\n\t"
+      "fma.rn.f32.f16 %0, h0, m1, %3;\n\t"
+      "fma.rn.f32.f16 %1, h1, m1, %4;\n\t}"
+      : "=f"(l0), "=f"(l1)
+      : "r"(hi), "f"(x0), "f"(x1));
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(l1), "f"(l0));
+}
+
 // 8 layer-0 inputs (any sign) -> one 16-byte chunk each of fp16 hi (the
 // truncation) and lo = fp16_rn(x - hi), as relu_split16 without the ReLU.
 __device__ __forceinline__ void split8(const float* x, uint4& hi4, uint4& lo4) {
@@ -301,7 +316,8 @@ __global__ void __launch_bounds__((NG + NP) * 128, 1)
     uint8_t* pbase = smem + L.prod_off + p * L.prod_bytes;
     const uint32_t cv_bytes = (uint32_t)(2 * S * (int)sizeof(CacheVertex) + 15) & ~15u;
     CacheVertex* s_cvb = reinterpret_cast<CacheVertex*>(pbase);
-    float* s_feat = reinterpret_cast<float*>(pbase + cv_bytes);
+    // (the S x 24 floats after the records are unused since the features
+    // are split into s_vx as they are computed)
     uint4* s_vx = reinterpret_cast<uint4*>(pbase + cv_bytes + (uint32_t)(S * 24 * 4 + 15) / 16 * 16);
     ws::VFrame* s_vf = reinterpret_cast<ws::VFrame*>(reinterpret_cast<uint8_t*>(s_vx) + S * 128);
     float* s_shk = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(s_vf) +
@@ -355,58 +371,90 @@ __global__ void __launch_bounds__((NG + NP) * 128, 1)
       // last reader was the tile before this one, ordered by its barriers)
       fetch(i + NP, (it + 1) & 1);
       asm volatile("cp.async.wait_group 1;" ::: "memory");
+      // the slot's meta buffer b is free once the combine of its tile n-2
+      // is done (checked here: the per-vertex meta is written below)
+      const int b = (int)(n & 1);
+      if (warp == 0 && n >= 2)
+        ws_wait_sleep(bar0 + 8 * (5 * slot + 2 + b), (uint32_t)(((n >> 1) - 1) & 1));
       tc::named_bar_sync(pbar, 128);
       if (kProbe && pb) pb[1] = clock64();
-      // shared surface encoding: one thread per (vertex, level)
-      for (int item = tg; item < nv * 12; item += 128) {
-        const int jj = item / 12, lvl = item % 12;
-        const CacheVertex& r = s_cv[jj];
-        const float ux = norm_coord(r.pos[0], sp.bb_min[0], sp.bb_inv[0]);
-        const float uy = norm_coord(r.pos[1], sp.bb_min[1], sp.bb_inv[1]);
-        const float uz = norm_coord(r.pos[2], sp.bb_min[2], sp.bb_inv[2]);
-        const LevelCell c = level_cell(ux, uy, uz, sp.res[lvl]);
-        const float2 f = pairs ? level_features2_pairs(theta + (size_t)lvl * T * 2, c, T - 1u)
-                               : level_features2(theta + (size_t)lvl * T * 2, c, T - 1u);
-        s_feat[jj * 24 + 2 * lvl] = f.x;
-        s_feat[jj * 24 + 2 * lvl + 1] = f.y;
-      }
-      tc::named_bar_sync(pbar, 128);
-      if (kProbe && pb) pb[2] = clock64();
-      // per-vertex operand chunks (features 0-2 and the aux block, shared by
-      // the vertex's rows) and the Lambert frame: items (vertex, part)
-      for (int item = tg; item < nv * 5; item += 128) {
-        const int jj = item / 5, part = item % 5;
-        const CacheVertex& r = s_cv[jj];
-        if (part < 4) {
-          float v[8];
-          if (part < 3) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) v[q] = s_feat[jj * 24 + 8 * part + q];
-          } else {
-            v[0] = (float)((r.ns[0] + 1.0) * 0.5);
-            v[1] = (float)((r.ns[1] + 1.0) * 0.5);
-            v[2] = (float)((r.ns[2] + 1.0) * 0.5);
-            v[3] = (float)r.alb[0];
-            v[4] = (float)r.alb[1];
-            v[5] = (float)r.alb[2];
-            v[6] = (float)r.rough;
-            v[7] = 0.0f;
+      uint8_t* meta = smem + L.meta_off + (slot * 2 + b) * L.meta_bytes;
+      ws::VMeta* vm = reinterpret_cast<ws::VMeta*>(meta + 128 * 32);
+      // one pass: the shared surface encoding, one thread per (vertex, level),
+      // each splitting its two features straight into the vertex's fp16
+      // hi / lo operand chunks (features 8 c .. 8 c + 7 in chunk c); then,
+      // from the next warp boundary on, the per-vertex items (aux chunk,
+      // Lambert frame, combine meta), which need no encoding
+      {
+        const int ne = nv * 12;
+        const int b2 = (ne + 31) & ~31;
+        uint32_t* s_vw = reinterpret_cast<uint32_t*>(s_vx);
+        for (int item = tg; item < b2 + 3 * nv; item += 128) {
+          if (item < ne) {
+            const int jj = item / 12, lvl = item % 12;
+            const CacheVertex& r = s_cv[jj];
+            const float ux = norm_coord(r.pos[0], sp.bb_min[0], sp.bb_inv[0]);
+            const float uy = norm_coord(r.pos[1], sp.bb_min[1], sp.bb_inv[1]);
+            const float uz = norm_coord(r.pos[2], sp.bb_min[2], sp.bb_inv[2]);
+            const LevelCell c = level_cell(ux, uy, uz, sp.res[lvl]);
+            const float2 f = pairs ? level_features2_pairs(theta + (size_t)lvl * T * 2, c, T - 1u)
+                                   : level_features2(theta + (size_t)lvl * T * 2, c, T - 1u);
+            uint32_t hw, lw;
+            ws::split2(f.x, f.y, hw, lw);
+            const int wi = (jj * 8 + (lvl >> 2)) * 4 + (lvl & 3);
+            s_vw[wi] = hw;
+            s_vw[wi + 16] = lw;
+            if (!(fabsf(f.x) < tc::kF16Max) || !(fabsf(f.y) < tc::kF16Max))
+              atomicOr(&s_vf[jj].unsafe, 1);
+          } else if (item >= b2) {
+            const int q = item - b2, jj = q % nv, what = q / nv;
+            const CacheVertex& r = s_cv[jj];
+            if (what == 0) {  // aux chunk: (n + 1) / 2, albedo, roughness
+              float v[8];
+              v[0] = (float)((r.ns[0] + 1.0) * 0.5);
+              v[1] = (float)((r.ns[1] + 1.0) * 0.5);
+              v[2] = (float)((r.ns[2] + 1.0) * 0.5);
+              v[3] = (float)r.alb[0];
+              v[4] = (float)r.alb[1];
+              v[5] = (float)r.alb[2];
+              v[6] = (float)r.rough;
+              v[7] = 0.0f;
+              uint4 hi, lo;
+              ws::split8(v, hi, lo);
+              s_vx[jj * 8 + 3] = hi;
+              s_vx[jj * 8 + 7] = lo;
+              if (tc::f16_unsafe(v, 8)) atomicOr(&s_vf[jj].unsafe, 1);
+            } else if (what == 1) {
+              ws::VFrame& vf = s_vf[jj];
+              vf.F = lambert_frame(r);
+              vf.lambert = r.mkind == pt::MAT_LAMBERT;
+              vf.f[0] = r.alb[0] * pt::INV_PI;
+              vf.f[1] = r.alb[1] * pt::INV_PI;
+              vf.f[2] = r.alb[2] * pt::INV_PI;
+            } else {
+              ws::VMeta m;
+              m.T[0] = r.T[0];
+              m.T[1] = r.T[1];
+              m.T[2] = r.T[2];
+              m.Tp[0] = r.Tp[0];
+              m.Tp[1] = r.Tp[1];
+              m.Tp[2] = r.Tp[2];
+              m.slot = r.slot;
+              m.ncq = r.ncq;
+              m.has_res = r.has_res;
+              m.nrc = r.nrc;
+              m.pad = 0;
+              m.inv = r.ncq > 0 ? 1.0 / r.ncq : 0.0;
+              vm[jj] = m;
+            }
           }
-          uint4 hi, lo;
-          ws::split8(v, hi, lo);
-          s_vx[jj * 8 + part] = hi;
-          s_vx[jj * 8 + 4 + part] = lo;
-          if (tc::f16_unsafe(v, 8)) atomicOr(&s_vf[jj].unsafe, 1);
-        } else {
-          ws::VFrame& vf = s_vf[jj];
-          vf.F = lambert_frame(r);
-          vf.lambert = r.mkind == pt::MAT_LAMBERT;
-          vf.f[0] = r.alb[0] * pt::INV_PI;
-          vf.f[1] = r.alb[1] * pt::INV_PI;
-          vf.f[2] = r.alb[2] * pt::INV_PI;
         }
       }
       tc::named_bar_sync(pbar, 128);
+      if (kProbe && pb) {
+        pb[2] = clock64();
+        pb[5] = pb[2];
+      }
       // per row: the direction, its SH block and the combine weights
       int kind = 0;
       double sw = 0.0, f0 = 0.0, f1 = 0.0, f2 = 0.0;
@@ -442,13 +490,10 @@ __global__ void __launch_bounds__((NG + NP) * 128, 1)
       ws::split8(sh, shi0, slo0);
       ws::split8(sh + 8, shi1, slo1);
       const bool unsafe = kind != 0 && s_vf[j < nv ? j : 0].unsafe != 0;
+      if (kProbe && pb) pb[6] = clock64();
       // one warp waits for the slot's A image (layer 0 of its previous tile
-      // complete) and meta buffer (combine of its tile n-2 done)
-      const int b = (int)(n & 1);
-      if (warp == 0) {
-        if (n >= 1) ws_wait_sleep(bar0 + 8 * (5 * slot + 1), (uint32_t)((n - 1) & 1));
-        if (n >= 2) ws_wait_sleep(bar0 + 8 * (5 * slot + 2 + b), (uint32_t)(((n >> 1) - 1) & 1));
-      }
+      // complete)
+      if (warp == 0 && n >= 1) ws_wait_sleep(bar0 + 8 * (5 * slot + 1), (uint32_t)((n - 1) & 1));
       tc::named_bar_sync(pbar, 128);
       if (kProbe && pb) pb[3] = clock64();
       // layer-0 row: chunks 0-2 features, 3-4 SH, 5 aux (K-major, 16-byte chunks)
@@ -471,7 +516,6 @@ __global__ void __launch_bounds__((NG + NP) * 128, 1)
         ws::sts128(a_hi + 5 * 2048 + ro, live ? s_vx[jv * 8 + 3] : z4);
         ws::sts128(a_lo + 5 * 2048 + ro, live ? s_vx[jv * 8 + 7] : z4);
       }
-      uint8_t* meta = smem + L.meta_off + (slot * 2 + b) * L.meta_bytes;
       double* mrow = reinterpret_cast<double*>(meta) + 4 * tg;
       if (kind == 1) {
         mrow[0] = f0;
@@ -484,24 +528,6 @@ __global__ void __launch_bounds__((NG + NP) * 128, 1)
         mrow[1] = v;
         mrow[2] = v;
         mrow[3] = kind >= 2 ? -1.0 : 0.0;  // < 0: unit weight, no ci/pdf factor
-      }
-      ws::VMeta* vm = reinterpret_cast<ws::VMeta*>(meta + 128 * 32);
-      if (tg < nv) {
-        const CacheVertex& r = s_cv[tg];
-        ws::VMeta m;
-        m.T[0] = r.T[0];
-        m.T[1] = r.T[1];
-        m.T[2] = r.T[2];
-        m.Tp[0] = r.Tp[0];
-        m.Tp[1] = r.Tp[1];
-        m.Tp[2] = r.Tp[2];
-        m.slot = r.slot;
-        m.ncq = r.ncq;
-        m.has_res = r.has_res;
-        m.nrc = r.nrc;
-        m.pad = 0;
-        m.inv = r.ncq > 0 ? 1.0 / r.ncq : 0.0;
-        vm[tg] = m;
       }
       int* pflag = reinterpret_cast<int*>(meta + 128 * 32 + S * sizeof(ws::VMeta));
       const bool wu = __any_sync(0xffffffffu, unsafe);

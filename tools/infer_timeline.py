@@ -60,3 +60,14 @@ print(f"span {tot:.0f} cycles; fraction of time with k groups' MMAs outstanding:
       {k: round(v / tot, 3) for k, v in busy.items()})
 g0 = a[0, 8]
 print("group 0 tile 8 (relative cycles):", [int(x - g0[0]) if x else None for x in g0[:15]])
+# producer 0 of CTA 0: per tile [start, records ready, encoding done, rows
+# built + slot free, arrive] (infer_ws.cuh probes pb[0..4])
+pr = buf.cpu().numpy()[2048:2048 + 32 * 8].reshape(32, 8).astype(np.float64)
+ok = [t for t in pr[2:] if t[0] and t[4]]
+if ok:
+    d = np.array([[t[1] - t[0], t[2] - t[1], t[5] - t[2], t[6] - t[5], t[3] - t[6], t[4] - t[3]]
+                  for t in ok])
+    per = np.diff([t[0] for t in ok])
+    print("producer 0 phases (median cycles): records %.0f, encoding %.0f, vertex chunks %.0f, "
+          "rows %.0f, slot wait %.0f, stores + meta %.0f; tile interval %.0f"
+          % (*np.median(d, axis=0), np.median(per)))

@@ -1,18 +1,21 @@
 """Executed warp instructions and stall samples per source line, with the
 opcode mix of each line, from an ncu report (read here, no GPU):
 
-    python tools/ncu_lines.py report.ncu-rep [top]
+    [NCU_KERNEL=regex:name] python tools/ncu_lines.py report.ncu-rep [top]
 Joins `--page source --print-source=sass` (per-instruction counts) with the
 `cuda,sass` view (address -> source line)."""
 import collections
 import csv
+import os
 import subprocess
 import sys
 
 
 def export(rep, view):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv",
-                          "--print-source=" + view], capture_output=True, text=True).stdout
+    cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=" + view]
+    if os.environ.get("NCU_KERNEL"):  # e.g. NCU_KERNEL=regex:k_trace for multi-kernel reports
+        cmd += ["-k", os.environ["NCU_KERNEL"]]
+    out = subprocess.run(cmd, capture_output=True, text=True).stdout
     return list(csv.reader(out.splitlines()))
 
 
