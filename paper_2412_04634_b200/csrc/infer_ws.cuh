@@ -370,6 +370,7 @@ __global__ void __launch_bounds__((NG + NP) * 128, 1)
       // the next tile's records load while this one is built (its buffer's
       // last reader was the tile before this one, ordered by its barriers)
       fetch(i + NP, (it + 1) & 1);
+      if (kProbe && pb) pb[7] = clock64();
       asm volatile("cp.async.wait_group 1;" ::: "memory");
       // the slot's meta buffer b is free once the combine of its tile n-2
       // is done (checked here: the per-vertex meta is written below)

@@ -68,6 +68,8 @@ if ok:
     d = np.array([[t[1] - t[0], t[2] - t[1], t[5] - t[2], t[6] - t[5], t[3] - t[6], t[4] - t[3]]
                   for t in ok])
     per = np.diff([t[0] for t in ok])
+    print("  of the records phase, issuing the next tile's copies: %.0f"
+          % np.median([t[7] - t[0] for t in ok]))
     print("producer 0 phases (median cycles): records %.0f, encoding %.0f, vertex chunks %.0f, "
           "rows %.0f, slot wait %.0f, stores + meta %.0f; tile interval %.0f"
           % (*np.median(d, axis=0), np.median(per)))
