@@ -283,8 +283,8 @@ def test_concurrent_renders_on_two_streams(nb, nc):
                 assert np.array_equal(a.cpu().numpy(), b), rep
 
 
-@pytest.mark.parametrize("depth", [2, 4])
-def test_warp_specialised_inference_matches_grouped_kernel(nb, depth, monkeypatch):
+@pytest.mark.parametrize("depth,nc", [(2, (16,)), (4, (16,)), (2, (4,)), (2, (6, 5, 1))])
+def test_warp_specialised_inference_matches_grouped_kernel(nb, depth, nc, monkeypatch):
     """k_infer_ws (producer warpgroups + four chain groups, the default for
     nc >= 8 where its shared-memory plan fits) against the grouped k_infer_tc
     (NIRC_INFER_NP=0) on the same frame: same walks, the same deferred
@@ -295,8 +295,17 @@ def test_warp_specialised_inference_matches_grouped_kernel(nb, depth, monkeypatc
     sc = __import__("paper_2412_04634_b200.scene", fromlist=["load_builtin"]).load_builtin(
         "cornell").with_resolution(128, 96)
     cache = Cache.create("nirc", sc, seed=7, init="random", depth=depth)
-    cfg = EstimatorConfig(mode="two-level", nc=(16,), max_cache_vertices=1)
+    # nc = (4,): 25 vertices per tile, the producers' encoding pass runs
+    # three rounds; (6, 5, 1): 18 per tile, three cache vertices per path
+    # (both fit k_infer_ws's shared-memory plan at depth 2)
+    cfg = EstimatorConfig(mode="two-level", nc=nc, max_cache_vertices=len(nc))
     ws = render(sc, cfg, cache=cache, seed=2, spp=2, precision=2)
+    # the configuration runs k_infer_ws: its timing ablation (chains skip
+    # their MMAs, tools only) changes the image
+    monkeypatch.setenv("NIRC_INFER_ABLATE", "2")
+    ablated = render(sc, cfg, cache=cache, seed=2, spp=2, precision=2)
+    assert not np.array_equal(ablated.image, ws.image)
+    monkeypatch.delenv("NIRC_INFER_ABLATE")
     monkeypatch.setenv("NIRC_INFER_NP", "0")
     grouped = render(sc, cfg, cache=cache, seed=2, spp=2, precision=2)
     assert np.array_equal(ws.path_length, grouped.path_length)
