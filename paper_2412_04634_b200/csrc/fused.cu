@@ -84,7 +84,12 @@ __device__ __forceinline__ void encode_default(const nirc_spec_t& sp,
     const LevelCell c = level_cell(ux, uy, uz, sp.res[lvl]);
     // ND is a compile-time count: the 12 levels stay straight-line code and
     // the gathers of all levels overlap in flight
-    const float2 f = lvl < ND ? level_features2_dense(dense + dl.off[lvl], dl.R[lvl], c)
+    // (kPairs: the dense levels are stored as x-pairs, fill_dense_levels_x2)
+    const float2 f = lvl < ND
+                         ? (kPairs ? level_features2_dense_x2(
+                                         reinterpret_cast<const float4*>(dense) + dl.off[lvl],
+                                         dl.R[lvl], c)
+                                   : level_features2_dense(dense + dl.off[lvl], dl.R[lvl], c))
                      : (kPairs ? level_features2_pairs(theta + (size_t)lvl * T * kF, c, T - 1u)
                                : level_features2(theta + (size_t)lvl * T * kF, c, T - 1u));
     x[2 * lvl] = f.x;
@@ -119,7 +124,10 @@ __global__ void __launch_bounds__(NG * 128, 1)
   const bool all_unsafe = w_unsafe != nullptr && *w_unsafe != 0;
   // dense coarse levels live in the region after the group A buffers
   float2* dense = reinterpret_cast<float2*>(smem + L.a_off + NG * L.abuf_bytes);
-  if (ND > 0) fill_dense_levels(sp, dl, theta, dense);
+  if (ND > 0) {
+    if (kPairs) fill_dense_levels_x2(sp, dl, theta, reinterpret_cast<float4*>(dense));
+    else fill_dense_levels(sp, dl, theta, dense);
+  }
   tc::tc_prologue(smem, L, net, NG, wimg, bias_g, tmem_base);
   const uint32_t s0 = tc::smem_u32(smem);
   const int group = threadIdx.x >> 7;
@@ -337,7 +345,13 @@ static int full_forward_impl(const nirc_spec_t* spec, const float* theta, const 
   // paired 16-byte gathers need 16-byte aligned level tables (NIRC_PAIRS=0: 8-byte only)
   dl.pairs = (reinterpret_cast<uintptr_t>(theta) & 15u) == 0;
   if (const char* e = getenv("NIRC_PAIRS")) dl.pairs = dl.pairs && atoi(e) != 0;
-  const tc::TcSmem L = tc::tc_smem_layout(net, ng, (uint32_t)dl.off[dl.n] * 8u);
+  // the paired kernel keeps its dense levels as x-pairs (16 bytes per entry)
+  // where they fit, else the 8-byte layout of the unpaired kernel
+  if (dl.pairs && !(ng == 4 && dl.n == 4 &&
+                    base_total + (uint32_t)dl.off[dl.n] * 16u <= 227u * 1024u - 1024u))
+    dl.pairs = 0;
+  const uint32_t dense_entry = (ng == 4 && dl.n == 4 && dl.pairs) ? 16u : 8u;
+  const tc::TcSmem L = tc::tc_smem_layout(net, ng, (uint32_t)dl.off[dl.n] * dense_entry);
   const int64_t want = (ntiles + ng - 1) / ng;
   const int grid = (int)(want < sm_count() ? want : sm_count());
   auto launch = [&](auto kern, int threads) -> int {
