@@ -492,10 +492,9 @@ __global__ void __launch_bounds__((NG + NP) * 128, 1)
       ws::split8(sh + 8, shi1, slo1);
       const bool unsafe = kind != 0 && s_vf[j < nv ? j : 0].unsafe != 0;
       if (kProbe && pb) pb[6] = clock64();
-      // one warp waits for the slot's A image (layer 0 of its previous tile
-      // complete)
-      if (warp == 0 && n >= 1) ws_wait_sleep(bar0 + 8 * (5 * slot + 1), (uint32_t)((n - 1) & 1));
-      tc::named_bar_sync(pbar, 128);
+      // every warp observes the slot's A image free (layer 0 of its previous
+      // tile complete) itself: no barrier needed before the stores
+      if (n >= 1) ws_wait_sleep(bar0 + 8 * (5 * slot + 1), (uint32_t)((n - 1) & 1));
       if (kProbe && pb) pb[3] = clock64();
       // layer-0 row: chunks 0-2 features, 3-4 SH, 5 aux (K-major, 16-byte chunks)
       {
