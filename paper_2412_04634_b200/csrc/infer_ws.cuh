@@ -51,6 +51,7 @@ struct VMeta {
 struct Layout {
   uint32_t w_off, bias_off, a_off, meta_off, meta_bytes, prod_off, prod_bytes, bar_off,
       holder_off, total;
+  float shk[28];  // the SH constants sh4_f32 reads, as fp32 kernel-parameter operands
 };
 
 // meta buffer: 128 rows x {f.x, f.y, f.z, ci/pdf} doubles (the row's
@@ -320,9 +321,6 @@ __global__ void __launch_bounds__((NG + NP) * 128, 1)
     // are split into s_vx as they are computed)
     uint4* s_vx = reinterpret_cast<uint4*>(pbase + cv_bytes + (uint32_t)(S * 24 * 4 + 15) / 16 * 16);
     ws::VFrame* s_vf = reinterpret_cast<ws::VFrame*>(reinterpret_cast<uint8_t*>(s_vx) + S * 128);
-    float* s_shk = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(s_vf) +
-                                            ((S * (int)sizeof(ws::VFrame) + 15) & ~15));
-    if (tg < 64) s_shk[tg] = (float)sp.sh_k[tg];
     if (tg < S) s_vf[tg].unsafe = 0;  // (ordered by the loop's first barrier)
     const uint32_t pbar = 1 + NG + p;
     const uint32_t T = 1u << sp.table_log2;
@@ -486,7 +484,7 @@ __global__ void __launch_bounds__((NG + NP) * 128, 1)
         }
       }
       float sh[16];
-      sh4_f32(w[0], w[1], w[2], s_shk, sh);
+      sh4_f32(w[0], w[1], w[2], L.shk, sh);
       uint4 shi0, slo0, shi1, slo1;
       ws::split8(sh, shi0, slo0);
       ws::split8(sh + 8, shi1, slo1);

@@ -822,9 +822,10 @@ __device__ inline void lambert_row(const LambertFrame& F, uint64_t key, int64_t 
   // Lambert weight only (hardware sin / cos of 2 pi u2 to ~1e-6 absolute)
   float sp, cp;
   __sincosf(6.28318530717958647692f * u2, &sp, &cp);
-  const float rr = sqrtf(u1);
+  float rr, lz;  // (approximate MUFU square roots, ~1 ulp)
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(rr) : "f"(u1));
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(lz) : "f"(fmaxf(0.0f, 1.0f - u1)));
   const float lx = rr * cp, ly = rr * sp;
-  const float lz = sqrtf(fmaxf(0.0f, 1.0f - u1));
   const float pdf = lz * (float)pt::INV_PI;
   w[0] = F.tx * lx + F.bx * ly + F.nx * lz;
   w[1] = F.ty * lx + F.by * ly + F.ny * lz;
@@ -1534,7 +1535,8 @@ static int render_impl(const nirc_scene_t* scene, const double* cam, const nirc_
       int np_ws = 2;
       if (const char* e = getenv("NIRC_INFER_NP")) np_ws = atoi(e);  // 0 = k_infer_tc
       if (np_ws > 2) np_ws = 2;
-      const ws::Layout WL = ws::layout(net, a.verts_per_tile, np_ws > 0 ? np_ws : 1);
+      ws::Layout WL = ws::layout(net, a.verts_per_tile, np_ws > 0 ? np_ws : 1);
+      for (int q = 0; q < 28; ++q) WL.shk[q] = (float)spec->sh_k[q];
       bool ws_shape = net.K[0] == 48 && net.N[0] == 64 && net.N[net.nl - 1] == 16;
       for (int l = 1; l < net.nl; ++l) ws_shape = ws_shape && net.K[l] == 64;
       for (int l = 0; l < net.nl - 1; ++l) ws_shape = ws_shape && net.N[l] == 64;
