@@ -99,4 +99,4 @@ def test_big_scene_bvh_and_render_match_reference(cuda, golden):
     r = render(sc, EstimatorConfig(mode="two-level", nc=(8, 4), max_cache_vertices=2),
                cache=cache, seed=5, spp=2)
     assert np.array_equal(r.path_length, g["tl_plen"])
-    np.testing.assert_allclose(r.image, g["tl_image"], rtol=1e-3, atol=1e-4)
+    np.testing.assert_allclose(r.image, g["tl_image"], rtol=1e-5, atol=5e-7)

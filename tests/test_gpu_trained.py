@@ -216,7 +216,7 @@ def test_two_level_render_trained_cache(nb, golden, tag, depth):
                    cache=cache, seed=3, spp=1, frame=int(g[f"{tag}_frame"]), precision=prec)
         assert np.array_equal(r.path_length, g[f"{tag}_tl_plen"])
         ref = g[f"{tag}_tl_image"]
-        np.testing.assert_allclose(r.image, ref, rtol=1e-3, atol=1e-4 * max(1.0, ref.max() / 17))
+        np.testing.assert_allclose(r.image, ref, rtol=1e-5, atol=5e-7 * max(1.0, ref.max() / 17))
 
 
 @pytest.mark.parametrize("nc", [8, 16])  # nc = 16: the warp-specialised kernel (k_infer_ws)
@@ -243,7 +243,7 @@ def test_render_fp16_range_guard(nb, golden, nc):
     r2 = render(sc, cfg, cache=cache, seed=3, spp=1, precision=2)
     r0 = render(sc, cfg, cache=cache, seed=3, spp=1, precision=0)
     assert np.all(np.isfinite(r2.image))
-    np.testing.assert_allclose(r2.image, r0.image, rtol=1e-3, atol=1e-4)
+    np.testing.assert_allclose(r2.image, r0.image, rtol=1e-5, atol=5e-7)
 
 
 @pytest.mark.parametrize("nc", [8, 16])
