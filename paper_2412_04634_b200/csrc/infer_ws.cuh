@@ -37,8 +37,10 @@ constexpr int kSlots = 4;
 // what the chain warps release is all the producers may take, or
 // setmaxnreg.inc blocks forever (checked on the host).  NP must divide 4 (a
 // slot's tiles come from one producer, so its barrier phases stay in order).
-template <int NP> constexpr int kChainRegs = NP == 1 ? 88 : (NP == 2 ? 64 : 0);
-template <int NP> constexpr int kProdRegs = NP == 1 ? 128 : (NP == 2 ? 112 : 0);
+// NP = 2 measured (1080p inference): 72 / 96 2.30 ms, 64 / 112 2.33 ms,
+// 80 / 80 2.61 ms (the producers spill).
+template <int NP> constexpr int kChainRegs = NP == 1 ? 88 : (NP == 2 ? 72 : 0);
+template <int NP> constexpr int kProdRegs = NP == 1 ? 128 : (NP == 2 ? 96 : 0);
 
 // Per-vertex data the combine needs (vertex_result), written by the producer.
 struct VMeta {
